@@ -1,0 +1,557 @@
+#!/usr/bin/env python
+"""Benchmark of the LASGD parameter-synchronisation hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the metric's config): ResNet-50 LASGD,
+batch 256 per GPU, parameters in one contiguous fp32 flat buffer of
+n = 25,557,032 (torchvision resnet50).  A "step" is one pass of the hot path
+over one minibatch's synthetic gradient: the fused local SGD step (K5,
+Nesterov momentum 0.9, weight decay 1e-4 — PAPER.md:229) and, every
+`sync_period` steps, the round boundary: wait for the previous mean, fused
+elastic pull + next snapshot (K4+K1), NVLink P2P mean all-reduce on the
+low-priority side stream (K2/K3, overlapping the next steps).  images/s =
+images whose gradients the sync path consumed per second over all ranks.
+
+Also reported (not the headline): the real ResNet-50 training step
+(forward/backward in PyTorch, bf16 autocast, channels_last) with LASGD and
+with sync disabled (the no-sync ceiling) -> exposed sync ms/step.
+
+`--impl reference` times the reference's own CPU algorithm (f64, delta
+bookkeeping, ring-order mean; the C restatement in oracle/, all host threads,
+P workers in-process like LoopbackTransport) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ResNet-50 LASGD images/sec at 1/2/4/8 B200; exposed sync ms/step; sync GB/s vs roofline"
+R50_PARAMS = 25_557_032  # sum of torchvision resnet50() parameter numels (161 tensors)
+NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction, /opt/skills/guides/B200_PROFILING.md
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--sync-period", type=int, default=1)
+    ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--algo", choices=["auto", "oneshot", "twoshot"], default="auto")
+    ap.add_argument("--nblocks", type=int, default=32)
+    ap.add_argument("--train-steps", type=int, default=10)
+    ap.add_argument("--train-warmup", type=int, default=4)
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernels-only", action="store_true", help="short run for ncu: sync path only")
+    return ap.parse_args()
+
+
+def config_dict(args, world):
+    return {
+        "workload": "resnet50-lasgd-sync",
+        "params": R50_PARAMS,
+        "batch_per_gpu": args.batch,
+        "sync_period": args.sync_period,
+        "alpha": args.alpha,
+        "local_step": "sgd momentum=0.9 nesterov weight_decay=1e-4 lr=0.1",
+        "allreduce": args.algo,
+        "sm_budget_ctas": args.nblocks,
+        "parallelism": f"dp{world}",
+        "l2": "no flush: every kernel streams 3-5 buffers of 102 MB (> 126 MB L2); gradients alternate between 2 buffers",
+    }
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-i", str(gpu), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- helpers
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def ncu_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def kernel_bytes(name, n, world, comm, algo_code, sgd_momentum=True):
+    """Algorithmic bytes per launch.  B = 4n."""
+    B = 4 * n
+    if name == "sgd_step":
+        return 5 * B if sgd_momentum else 3 * B, "hbm"
+    if name == "pull":
+        return 5 * B, "hbm"
+    if name == "finalize":
+        return 4 * B, "hbm"
+    if name == "snapshot":
+        return 2 * B, "hbm"
+    if name == "allreduce":
+        return comm.bytes_per_node(algo_code), "nvlink"
+    return 0, "hbm"
+
+
+def cpu_reference_run(n_full, P, k, steps, warmup, threads, target_step_s=1.0):
+    """The reference algorithm on the host (oracle/ C port, f64 like the reference):
+    per step every worker runs sgd_local_step (x and delta, optimizer.py:145-146);
+    every k steps the ring mean of the P snapshots (collective.py:154-203) and P
+    finalizes new = z + delta (optimizer.py:171).  Returns (seconds/step, sample n)."""
+    import numpy as np
+
+    from oracle import c_oracle as C
+
+    C.set_threads(threads)
+    # bounded sample: estimate the per-element cost, keep one step near target_step_s
+    probe_n = min(n_full, 1 << 22)
+    xa, xb, da, db, g = (np.random.default_rng(i).standard_normal(probe_n) for i in range(5))
+    t0 = time.perf_counter()
+    for _ in range(3):
+        C.sgd_delta(xb, db, xa, da, g, 0.1)
+    per_elem = (time.perf_counter() - t0) / 3 / probe_n
+    per_step_elem = per_elem * P * (1.0 + 1.5 / k)  # sgd + amortised mean/finalize
+    n = int(min(n_full, max(1 << 16, target_step_s / per_step_elem)))
+    mem = _mem_available()
+    if mem:
+        n = int(min(n, mem * 0.5 / (8 * (5 * P + 2))))
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal(n) * 1e-2
+    xs = [[rng.standard_normal(n) * 0.1, np.empty(n)] for _ in range(P)]
+    ds = [[np.zeros(n), np.empty(n)] for _ in range(P)]
+    snaps = [x[0].copy() for x in xs]
+    z = np.empty(n)
+    cur = [0] * P
+    reset = [True] * P
+
+    def one_step(t):
+        for r in range(P):
+            c = cur[r]
+            C.sgd_delta(xs[r][1 - c], ds[r][1 - c], xs[r][c], ds[r][c], g, 0.1, delta_reset=reset[r])
+            cur[r] = 1 - c
+            reset[r] = False
+        if (t + 1) % k == 0:
+            if P > 1:
+                C.ring_mean([z], snaps)
+                for r in range(P):
+                    C.finalize(xs[r][cur[r]], z, ds[r][cur[r]])
+                    snaps[r] = xs[r][cur[r]]  # x_local = x_snapshot = new (aliased, optimizer.py:172-173)
+            for r in range(P):
+                reset[r] = True
+
+    for t in range(warmup):
+        one_step(t)
+    t0 = time.perf_counter()
+    for t in range(steps):
+        one_step(warmup + t)
+    dt = (time.perf_counter() - t0) / steps
+    return dt, n
+
+
+def _mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except Exception:
+        return None
+    return None
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    P = world
+    dt, n = cpu_reference_run(R50_PARAMS, P, args.sync_period, max(1, args.steps), max(1, args.warmup), threads)
+    scale = n / R50_PARAMS  # elementwise work is linear in n: full-size step time = dt / scale
+    value = P * args.batch / (dt / scale)
+    sample = (f"reference algorithm (f64, delta bookkeeping, ring-order mean, {P} workers in-process) on "
+              f"{n} of {R50_PARAMS} parameters per step, scaled linearly to the full vector; "
+              f"{args.steps} timed steps after {args.warmup} warm-up; host: {cpu_model()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / scale * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, world),
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from paper_2203_13085_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    algo_code = {"auto": N.ALGO_AUTO, "oneshot": N.ALGO_ONESHOT, "twoshot": N.ALGO_TWOSHOT}[args.algo]
+    n = R50_PARAMS
+    sgd = L.SgdConfig(0.9, 0.0, 1e-4, True)
+    lr = 0.1
+    comm = L.P2PCommunicator(n, nblocks=args.nblocks, timeout_s=60.0) if world > 1 else None
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
+    x = torch.randn(n, device=dev, generator=gen) * 0.02  # identical x0 on every rank
+    grads = []
+    for i in range(2):
+        gen.manual_seed(1000 + 10 * rank + i)
+        grads.append(torch.randn(n, device=dev, generator=gen) * 1e-2)
+    compute = torch.cuda.Stream(device=dev, priority=-1)
+
+    def make_worker(timed, sync=True, g=None):
+        return L.LASGDWorker(x, g if g is not None else grads[0], comm=comm, sync_period=args.sync_period,
+                             alpha=args.alpha, mode="pull", sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
+                             timed=timed, sync=sync)
+
+    def run_sync_path(worker, steps, gsrc):
+        for t in range(steps):
+            worker.g = gsrc(t)
+            worker.step()
+
+    # ---------------- value: HBM-resident gradients, device-timed
+    with torch.cuda.stream(compute):
+        w = make_worker(False)
+        run_sync_path(w, args.warmup, lambda t: grads[t % 2])
+        w.drain()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w.reset_records()
+    with torch.cuda.stream(compute):
+        e0.record(compute)
+        run_sync_path(w, args.steps, lambda t: grads[t % 2])
+        w.drain()
+        e1.record(compute)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = sum(w.launches.values())
+    barrier()
+
+    # ---------------- per-kernel timing (same loop, events around every launch)
+    with torch.cuda.stream(compute):
+        wt = make_worker(True)
+        run_sync_path(wt, args.warmup, lambda t: grads[t % 2])
+        wt.drain()
+    torch.cuda.synchronize()
+    barrier()
+    wt.reset_records()
+    with torch.cuda.stream(compute):
+        run_sync_path(wt, args.steps, lambda t: grads[t % 2])
+        wt.drain()
+    torch.cuda.synchronize()
+    ktimes = wt.kernel_times()
+    barrier()
+
+    # ---------------- e2e: gradients from pinned host memory every step (H2D on a copy
+    # stream, double-buffered) + D2H of the step's status word, through the public API
+    host_g = [grads[i].cpu().pin_memory() for i in range(2)]
+    dev_g = [torch.empty(n, device=dev) for _ in range(2)]
+    status_h = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    copy_stream = torch.cuda.Stream(device=dev)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    for ev in free:
+        ev.record(compute)
+
+    def e2e_loop(worker, steps):
+        def issue(t):
+            b = t % 2
+            copy_stream.wait_event(free[b])
+            with torch.cuda.stream(copy_stream):
+                dev_g[b].copy_(host_g[b], non_blocking=True)
+            ready[b].record(copy_stream)
+
+        issue(0)
+        for t in range(steps):
+            b = t % 2
+            if t + 1 < steps:
+                issue(t + 1)
+            compute.wait_event(ready[b])
+            worker.g = dev_g[b]
+            worker.step()
+            free[b].record(compute)
+            status_h.copy_(worker.state.nonfinite_counter, non_blocking=True)
+        worker.drain()
+
+    with torch.cuda.stream(compute):
+        we = make_worker(False, g=dev_g[0])
+        e2e_loop(we, args.warmup)
+    torch.cuda.synchronize()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(compute):
+        f0.record(compute)
+        e2e_loop(we, args.steps)
+        f1.record(compute)
+    torch.cuda.synchronize()
+    ms_e2e = max_over_ranks(f0.elapsed_time(f1))
+    barrier()
+    clk = clocks.stop() if clocks else None
+
+    # ---------------- isolated kernel timings (each kernel alone, for the roofline detail)
+    iso = {}
+    with torch.cuda.stream(compute):
+        m = torch.zeros_like(x)
+        s0, s1, xb = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+
+        def timeit(fn, reps=20):
+            for _ in range(3):
+                fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(compute)
+            for _ in range(reps):
+                fn()
+            b.record(compute)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        from paper_2203_13085_b200 import kernels as K
+
+        iso["sgd_step"] = timeit(lambda: K.sgd_step(x, grads[0], lr, m=m, momentum=0.9, weight_decay=1e-4,
+                                                    nesterov=True, stream=compute))
+        iso["pull"] = timeit(lambda: K.elastic_pull(x, s0, xb, 1.0, snap_next=s1, stream=compute))
+        iso["snapshot"] = timeit(lambda: K.snapshot(s1, x, stream=compute))
+        if comm is not None:
+            barrier()
+
+            def ar():
+                seq = comm.allreduce(0, algo_code, stream=compute)
+                return seq
+
+            iso["allreduce"] = timeit(ar, reps=10)
+    barrier()
+
+    # ---------------- real training: ResNet-50 fwd/bwd + LASGD vs no-sync ceiling
+    training = None
+    if not args.no_train and not args.kernels_only:
+        training = run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barrier, max_over_ranks)
+
+    # ---------------- report
+    imgs = world * args.batch * args.steps
+    value = imgs / (ms / 1e3)
+    e2e_val = imgs / (ms_e2e / 1e3)
+    hbm_peak, peak_kind = peaks()
+    traffic = ncu_traffic()
+    kernels = {}
+    for name, ts in ktimes.items():
+        byt, bound = kernel_bytes(name, n, world, comm, algo_code)
+        avg = sum(ts) / len(ts)
+        pk = hbm_peak if bound == "hbm" else NVLINK_PEAK_GBS
+        ach = byt / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
+        entry = {"launches": len(ts), "avg_ms": avg, "bytes_per_launch": byt, "bound": bound,
+                 "achieved_gbs": ach, "peak_gbs": pk, "frac": ach / pk, "share_of_step": sum(ts) / ms}
+        if name in iso:
+            ia = byt / (iso[name] * 1e-3) / 1e9
+            entry["isolated_ms"] = iso[name]
+            entry["isolated_gbs"] = ia
+            entry["isolated_frac"] = ia / pk
+        kernels[name] = entry
+    dom = max(kernels, key=lambda k: sum(ktimes[k]))
+    d = kernels[dom]
+    tr = traffic.get(dom)
+    roofline = {"kernel": dom, "bound": "hbm" if d["bound"] == "hbm" else "nvlink", "achieved": d["achieved_gbs"],
+                "peak": d["peak_gbs"], "unit": "GB/s", "frac": d["frac"], "traffic": tr,
+                "algorithmic_bytes": d["bytes_per_launch"],
+                "peak_source": (f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})" if d["bound"] == "hbm"
+                                else "B200_PROFILING.md measured peer copy 770 GB/s/direction")}
+    gpu_launches = int(sum_over_ranks(launches))
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        dt, ns = cpu_reference_run(R50_PARAMS, 1, args.sync_period, 10, 2, threads, target_step_s=0.5)
+        scale = ns / R50_PARAMS
+        cpu_base = {"value": args.batch / (dt / scale), "unit": "images/s", "cores": threads, "kind": "port",
+                    "sample": f"reference algorithm (f64 C port of oracle/, 1 worker, sgd_local_step + finalize) on "
+                              f"{ns} of {R50_PARAMS} parameters, 10 steps, scaled linearly; host {cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args, world),
+            "roofline": roofline,
+            "cpu_baseline": cpu_base,
+            "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,
+                    "ms_per_step": ms_e2e / args.steps,
+                    "path": "public API (LASGDWorker) with gradients from pinned host memory each step"},
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+            "sync_kernels": kernels,
+            "training": training,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        barrier()
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barrier, max_over_ranks):
+    import torch
+    import torchvision
+
+    import paper_2203_13085_b200 as L
+
+    torch.backends.cudnn.benchmark = True
+    model = torchvision.models.resnet50().to(dev).to(memory_format=torch.channels_last)
+    flat = L.FlatParams(model, channels_last=True)
+    assert flat.numel == R50_PARAMS
+    if comm is not None:
+        # identical x0 on every rank (Algorithm 1 line 1)
+        import torch.distributed as dist
+
+        dist.broadcast(flat.x, 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    images = torch.randn(args.batch, 3, 224, 224, device=dev, generator=gen).to(memory_format=torch.channels_last)
+    labels = torch.randint(0, 1000, (args.batch,), device=dev, generator=gen)
+    lossf = torch.nn.CrossEntropyLoss()
+
+    def train(sync, steps, warm):
+        with torch.cuda.stream(compute):
+            w = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=args.sync_period, alpha=args.alpha, mode="pull",
+                              sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute, sync=sync)
+
+            def one():
+                flat.zero_grad()
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    loss = lossf(model(images), labels)
+                loss.backward()
+                w.step()
+
+            for _ in range(warm):
+                one()
+            w.drain()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(compute):
+            a.record(compute)
+            for _ in range(steps):
+                one()
+            w.drain()
+            b.record(compute)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b)) / steps
+
+    t_sync = train(True, args.train_steps, args.train_warmup)
+    t_nosync = train(False, args.train_steps, args.train_warmup)
+    return {
+        "model": "resnet50 (torchvision, random init)", "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params",
+        "steps": args.train_steps, "images_per_s_lasgd": world * args.batch / (t_sync / 1e3),
+        "images_per_s_nosync": world * args.batch / (t_nosync / 1e3), "ms_per_step_lasgd": t_sync,
+        "ms_per_step_nosync": t_nosync, "exposed_sync_ms_per_step": t_sync - t_nosync,
+        "exposed_sync_frac": (t_sync - t_nosync) / t_sync,
+    }
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,169 @@
+/*
+ * lasgd_sync.h — C ABI of the B200-native LASGD parameter-synchronisation path.
+ *
+ * Drop-in boundary for the reference's Python plug-in points
+ * (/root/reference/pkg/src/lasgd; the reference has no FFI, its boundary is
+ * duck-typed Python — SURVEY.md §8(b)).  Every entry point below names the
+ * reference function it replaces.  Plain pointers and sizes only: device
+ * pointers are raw CUDA device addresses, `stream` is a cudaStream_t passed as
+ * void* (NULL = legacy default stream).  All kernel entry points are
+ * stream-ordered and non-blocking.
+ *
+ * Return value: 0 on success, a negative LASGD_ERR_* code otherwise; the
+ * Python layer maps codes to the reference exception types (see
+ * paper_2203_13085_b200/_native.py).  lasgd_last_error() returns a
+ * thread-local diagnostic for the most recent failure on the calling thread.
+ *
+ * Element type: LASGD_F32 (the product path, bit-exact against the fp32
+ * restatement) or LASGD_F64 (bit-exact against the f64 reference itself).
+ * Arithmetic contract: every product and sum is separately rounded (no FMA),
+ * scalars are rounded to the element type first, exactly like the
+ * reference's numpy expressions (params.py:87).
+ */
+#ifndef LASGD_SYNC_H
+#define LASGD_SYNC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LASGD_ABI_VERSION 1
+
+/* error codes (→ Python exception in _native.py) */
+#define LASGD_OK 0
+#define LASGD_ERR_INVALID_ARGUMENT (-1) /* ValueError                       */
+#define LASGD_ERR_DIMENSION (-2)        /* DimensionMismatchError, params.py:15 */
+#define LASGD_ERR_NONFINITE (-3)        /* NonFiniteError, params.py:19       */
+#define LASGD_ERR_CUDA (-4)             /* RuntimeError (CUDA runtime)        */
+#define LASGD_ERR_COLLECTIVE (-5)       /* CollectiveFailure, collective.py:26 */
+#define LASGD_ERR_TIMEOUT (-6)          /* TimeoutError (host wait)           */
+#define LASGD_ERR_STATE (-7)            /* RuntimeError (protocol misuse)     */
+#define LASGD_ERR_UNSUPPORTED (-8)      /* e.g. world size > LASGD_MAX_RANKS  */
+
+/* element types */
+#define LASGD_F32 0
+#define LASGD_F64 1
+
+/* all-reduce algorithms */
+#define LASGD_ALGO_AUTO 0
+#define LASGD_ALGO_ONESHOT 1
+#define LASGD_ALGO_TWOSHOT 2
+
+#define LASGD_MAX_RANKS 8
+#define LASGD_MAX_BLOCKS 128
+#define LASGD_IPC_HANDLE_BYTES 64
+
+int lasgd_abi_version(void);
+const char* lasgd_strerror(int code);
+const char* lasgd_last_error(void);
+
+/* ---- rank-local streaming kernels (HBM-bound) -------------------------- */
+
+/* K0: out = a*u + b*v.  Replaces params.py:80-89 `blend` (out-of-place). */
+int lasgd_blend(void* out, double a, const void* u, double b, const void* v, size_t n, int dtype,
+                unsigned long long* nonfinite, void* stream);
+
+/* K1: snap = x.  Replaces the snapshot of optimizer.py:172-173 (the reference
+ * aliases an immutable vector; the flat fp32 buffer needs a real copy). */
+int lasgd_snapshot(void* snap, const void* x, size_t n, int dtype, void* stream);
+
+typedef struct {
+  double lr;           /* eta_t (problems.py:355 lr_at); kernel uses (T)(-lr)      */
+  double momentum;     /* 0 = reference sgd_local_step                            */
+  double dampening;
+  double weight_decay;
+  int nesterov;
+  int first_step;      /* momentum buffer := direction (torch semantics)          */
+  int delta_reset;     /* delta := 0 + (-lr)*d  (fresh accumulator, optimizer.py:174) */
+} lasgd_sgd_params;
+
+/* K5: fused local step on the flat buffer.
+ *   d = g (+ wd*x);  m = first ? d : mu*m + (1-damp)*d;  d = nesterov ? d + mu*m : m;
+ *   x = x + (-lr)*d;  delta = (reset ? 0 : delta) + (-lr)*d   (delta nullable)
+ * With momentum = wd = 0 this is exactly optimizer.py:145-146 (`sgd_local_step`).
+ * m may be NULL when momentum == 0. */
+int lasgd_sgd_step(void* x, const void* g, void* m, void* delta, size_t n, int dtype,
+                   const lasgd_sgd_params* p, unsigned long long* nonfinite, void* stream);
+
+/* K4a: elastic pull x -= alpha*(snap - xbar), in blend order
+ *   diff = 1*snap + (-1)*xbar;  x = 1*x + (-alpha)*diff;  snap_next = x (nullable).
+ * Replaces Algorithm 1 line 9a for alpha = 1 and the
+ * elastic pull rule of optimizer.py:256-257 for alpha in (0,1]. */
+int lasgd_elastic_pull(void* x, void* snap_next, const void* snap, const void* xbar, size_t n, int dtype,
+                       double alpha, unsigned long long* nonfinite, void* stream);
+
+/* K4b: reference finalize new = 1*z + 1*delta; x = new; snap_next = new (nullable).
+ * Replaces optimizer.py:170-174 (`lasgd_finalize_round`, P > 1 branch). */
+int lasgd_finalize(void* x, void* snap_next, const void* z, const void* delta, size_t n, int dtype,
+                   unsigned long long* nonfinite, void* stream);
+
+/* ---- mean all-reduce over ranks emulated on ONE device ------------------ */
+
+/* Replaces collective.py:154-203 (`execute_allreduce`) for P virtual ranks
+ * whose contributions all live on the calling device — the GPU analogue of
+ * LoopbackTransport (collective.py:229-287).  srcs / outs are HOST arrays of
+ * device pointers.  algo ONESHOT computes outs[0..n_out) directly from all P
+ * sources; TWOSHOT runs the reduce-scatter of every virtual rank into outs[r]
+ * (n_out must equal P) and then the all-gather, exercising exactly the
+ * slicing of the multi-GPU two-shot kernel without its barriers.
+ * Results are bit-identical to the reference ring order. */
+int lasgd_mean_virtual(void* const* outs, int n_out, const void* const* srcs, int P, size_t n, int dtype,
+                       int algo, int nblocks, unsigned long long* nonfinite, void* stream);
+
+/* ---- multi-GPU communicator (NVLink P2P through NVSwitch) -------------- */
+
+typedef struct lasgd_comm lasgd_comm;
+
+typedef struct {
+  int nblocks;          /* SM budget: CTAs of the all-reduce kernel (<= LASGD_MAX_BLOCKS)     */
+  int threads;          /* threads per CTA (multiple of 32, >= world)                         */
+  double timeout_s;     /* watchdog for a peer flag (→ CollectiveFailure), e.g. 30.0          */
+  long long fault_seq;  /* TEST KNOB: skip this rank's flag writes in launch #fault_seq (-1 off) */
+  int fault_phase;      /* 0 entry barrier, 1 mid barrier                                     */
+} lasgd_comm_config;
+
+/* Allocates this rank's IPC-exportable region: signal pad + snapshot slot 0/1
+ * + mean buffer (n elements each, 256-B aligned) + a host-mapped status block. */
+int lasgd_comm_create(int rank, int world, int device, size_t n, int dtype, const lasgd_comm_config* cfg,
+                      lasgd_comm** out);
+/* Export this rank's region handle (LASGD_IPC_HANDLE_BYTES bytes into `out`). */
+int lasgd_comm_ipc_handle(lasgd_comm* c, void* out);
+/* Map every peer's region; `handles` = world * LASGD_IPC_HANDLE_BYTES bytes in rank order. */
+int lasgd_comm_open(lasgd_comm* c, const void* handles);
+/* which: 0 = snapshot slot 0, 1 = snapshot slot 1, 2 = mean (xbar). */
+int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr);
+
+/* K2/K3 (+K6 flags): xbar = mean over ranks of snapshot slot `snap_slot`, in the
+ * reference ring's per-chunk rotated order (bit-identical on every rank).
+ * Replaces LoopbackTransport.submit / execute_allreduce (collective.py:248-260,
+ * 154-203).  Every rank must issue the same sequence of calls.  *seq receives
+ * this launch's sequence number for query/wait. */
+int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, unsigned long long* seq);
+/* Non-blocking completion poll of launch `seq` (collective.py:142-144 `poll`):
+ * 1 complete, 0 in flight, LASGD_ERR_COLLECTIVE failed (diagnostic via
+ * lasgd_comm_diagnostic).  Reads a host-mapped flag: no CUDA call. */
+int lasgd_comm_query(lasgd_comm* c, unsigned long long seq);
+/* Make `stream` wait for launch `seq` (cudaStreamWaitEvent; no host block). */
+int lasgd_comm_stream_wait(lasgd_comm* c, unsigned long long seq, void* stream);
+/* Host wait (collective.py:138-139 `wait`): 1 complete, LASGD_ERR_TIMEOUT, or failure. */
+int lasgd_comm_wait(lasgd_comm* c, unsigned long long seq, double timeout_s);
+int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len);
+/* NVLink bytes this rank's peers read from it in one launch (collective.py:206-226 analogue). */
+unsigned long long lasgd_comm_bytes_per_node(lasgd_comm* c, int algo);
+int lasgd_comm_resolve_algo(lasgd_comm* c, int algo);
+int lasgd_comm_destroy(lasgd_comm* c);
+
+/* ---- host utilities ------------------------------------------------------ */
+
+/* partition_chunks (params.py:130-147): writes num_chunks+1 boundaries. */
+int lasgd_partition_chunks(size_t d, int num_chunks, size_t* bounds);
+/* bytes_per_node (collective.py:206-226); rank < 0 = max over ranks. */
+unsigned long long lasgd_bytes_per_node(size_t d, int num_ranks, int bytes_per_element, int rank);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LASGD_SYNC_H */

@@ -1,0 +1,49 @@
+"""B200-native LASGD parameter-synchronisation path (arXiv 2203.13085).
+
+Drop-in for the reference package's sync path (``lasgd.params``,
+``lasgd.collective``, ``lasgd.optimizer``, ``lasgd.problems.lr_at``): the same
+names and argument order, device buffers instead of host vectors, fused
+sm_100a kernels behind a C ABI (include/lasgd_sync.h) instead of numpy.
+
+Importing this package loads ``_lib/liblasgd_sync.so`` eagerly and raises
+``ImportError`` if it is missing — there is no CPU fallback.
+"""
+
+from . import _native
+
+_native.lib()  # fail loudly at import time when the CUDA library is absent
+
+from ._native import CollectiveFailure, DimensionMismatchError, NonFiniteError, TransportFault  # noqa: E402
+from .collective import (  # noqa: E402
+    CollectiveHandle,
+    CudaLoopbackTransport,
+    CudaP2PTransport,
+    P2PCommunicator,
+    Status,
+    all_reduce_average,
+    bytes_per_node,
+    poll,
+    ring_schedule,
+)
+from .engine import LASGDWorker  # noqa: E402
+from .flat import FlatParams  # noqa: E402
+from .optimizer import (  # noqa: E402
+    HyperParamError,
+    HyperParams,
+    NodeState,
+    SgdConfig,
+    TickAction,
+    lasgd_finalize_round,
+    lasgd_node_tick,
+    sgd_local_step,
+)
+from .params import ChunkSpec, as_device_vector, blend, partition_chunks, require_same_dim  # noqa: E402
+from .problems import LrSchedule, lr_at  # noqa: E402
+
+__all__ = [
+    "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
+    "DimensionMismatchError", "FlatParams", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule",
+    "NodeState", "NonFiniteError", "P2PCommunicator", "SgdConfig", "Status", "TickAction", "TransportFault",
+    "all_reduce_average", "as_device_vector", "blend", "bytes_per_node", "lasgd_finalize_round", "lasgd_node_tick",
+    "lr_at", "partition_chunks", "poll", "require_same_dim", "ring_schedule", "sgd_local_step",
+]

@@ -1,0 +1,729 @@
+// Mean all-reduce of the LASGD snapshot over NVLink P2P (K2 one-shot, K3 two-shot)
+// with epoch-tagged per-CTA flags in IPC-mapped signal pads (K6) and a
+// host-mapped completion word for flag polling.
+//
+// Replaces collective.py:154-203 (`execute_allreduce`) and the
+// LoopbackTransport round (collective.py:229-287).  The arithmetic reproduces the
+// reference ring's per-chunk summation order bit for bit: element j of chunk c
+// (partition_chunks(n, P), params.py:130-147) is summed x_c, x_{c+1}, ..., x_{c-1}
+// (mod P) and the sum is divided by P once (collective.py:200).  Every rank
+// therefore ends with identical bits, like the reference's per_rank copies.
+//
+// One-shot: every rank reads all P snapshots (P-1 over NVLink) and reduces every
+// element itself.   NVLink in-bytes per rank: (P-1)*B.
+// Two-shot: rank c reduces chunk c (reduce-scatter, same order), then copies the
+// other ranks' reduced chunks (all-gather).  NVLink in-bytes: 2(P-1)/P*B — the
+// reference's bytes_per_node (collective.py:206-226).
+//
+// Synchronisation is per CTA: CTA b of every rank slices the data identically, so
+// CTA b only ever waits for CTA b of its peers (no grid-wide barrier).  The entry
+// barrier publishes "my snapshot slot is final"; the two-shot mid barrier publishes
+// "my reduced chunk slice is final" and, implicitly, "I have finished reading your
+// snapshot slice".  Snapshot slots are double-buffered by round parity by the
+// caller, so the next round's writes never race a peer's reads (a peer can only
+// enter round r+1 after finishing round r, and our round r+1 launch completes only
+// after every peer entered it).  A %globaltimer watchdog turns a dead peer into a
+// CollectiveFailure instead of a hung GPU.
+#include <stdarg.h>
+#include <string.h>
+#include <time.h>
+
+#include "lasgd_common.cuh"
+
+namespace lasgd {
+
+constexpr int kMaxR = LASGD_MAX_RANKS;
+constexpr int kMaxB = LASGD_MAX_BLOCKS;
+constexpr int kPhases = 2;
+constexpr size_t kPadBytes = (size_t)kPhases * kMaxB * kMaxR * sizeof(uint32_t);
+constexpr int kDoneSlots = 64;
+constexpr int kEvents = 64;
+
+// host-mapped status block layout (uint32 words)
+enum { ST_ERR = 0, ST_PEER, ST_PHASE, ST_BLOCK, ST_SEQ_LO, ST_SEQ_HI, ST_RANK, ST_WORDS = 16 };
+enum { ERR_NONE = 0, ERR_TIMEOUT = 1, ERR_INJECTED = 2 };
+
+struct CommArgs {
+  const char* snap[kMaxR];
+  char* xbar[kMaxR];
+  uint32_t* pad[kMaxR];
+  size_t n;
+  int rank;
+  int nblocks;
+  uint32_t epoch;
+  int phases;  // bit 0: reduce (one-shot / RS), bit 1: all-gather (two-shot)
+  long long timeout_ns;
+  int skip_signal_phase;
+  uint32_t* status;
+  unsigned int* done_ctr;
+  unsigned long long* done_seq;
+  unsigned long long seq;
+  unsigned long long* nonfinite;
+};
+
+// ------------------------------------------------------------------ primitives
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounds of partition_chunks(n, P): bound(c) = c*base + min(c, rem).
+__device__ __forceinline__ size_t chunk_bound(size_t n, int P, int c) {
+  const size_t base = n / (size_t)P, rem = n % (size_t)P;
+  return (size_t)c * base + ((size_t)c < rem ? (size_t)c : rem);
+}
+
+template <int P>
+__device__ __forceinline__ int chunk_of(size_t j, const size_t (&bnd)[P + 1]) {
+  int c = 0;
+#pragma unroll
+  for (int k = 1; k < P; ++k) c += (j >= bnd[k]);
+  return c;
+}
+
+// Sum v[c], v[c+1], ..., v[c-1] (mod P) left to right: the reference ring order.
+template <typename T, int P>
+__device__ __forceinline__ T rot_sum(const T (&v)[P], int c) {
+  T acc = v[0];
+#pragma unroll
+  for (int cc = 0; cc < P; ++cc) {
+    if (c == cc) {
+      T s = v[cc];
+#pragma unroll
+      for (int k = 1; k < P; ++k) s = add_rn(s, v[(cc + k) % P]);
+      acc = s;
+    }
+  }
+  return acc;
+}
+
+// buf / P (collective.py:200).  For power-of-two P, x*(1/P) is the same correctly
+// rounded value as x/P (exact scaling), so use the cheaper multiply.
+template <typename T, int P>
+__device__ __forceinline__ T mean_div(T s) {
+  if constexpr ((P & (P - 1)) == 0) {
+    return mul_rn(s, T(1.0 / P));
+  } else {
+    return div_rn(s, T(P));
+  }
+}
+
+__device__ void report_failure(const CommArgs& a, int code, int peer, int phase, int block, int rank) {
+  if (atomicCAS(&a.status[ST_ERR], 0u, (uint32_t)code) == 0u) {
+    a.status[ST_PEER] = peer;
+    a.status[ST_PHASE] = phase;
+    a.status[ST_BLOCK] = block;
+    a.status[ST_SEQ_LO] = (uint32_t)(a.seq & 0xffffffffu);
+    a.status[ST_SEQ_HI] = (uint32_t)(a.seq >> 32);
+    a.status[ST_RANK] = rank;
+    __threadfence_system();
+  }
+}
+
+// Per-CTA barrier with the same CTA index on every peer.  Thread q < P signals
+// peer q and waits for peer q's signal.
+template <int P>
+__device__ bool cta_barrier(const CommArgs& a, int phase, int b, int rank) {
+  __syncthreads();
+  int ok = 1;
+  if (threadIdx.x < P) {
+    const int q = threadIdx.x;
+    const size_t slot = ((size_t)phase * kMaxB + b) * kMaxR;
+    if (a.skip_signal_phase != phase) {
+      __threadfence_system();
+      st_release_sys(a.pad[q] + slot + rank, a.epoch);
+    }
+    const uint32_t* f = a.pad[rank] + slot + q;
+    const unsigned long long t0 = globaltimer();
+    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+      if ((long long)(globaltimer() - t0) > a.timeout_ns) {
+        report_failure(a, ERR_TIMEOUT, q, phase, b, rank);
+        ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  return __syncthreads_and(ok) != 0;
+}
+
+// Last CTA of a launch publishes the sequence number to host-mapped memory.
+__device__ void publish_done(const CommArgs& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned slot = (unsigned)(a.seq % kDoneSlots);
+    const unsigned prev = atomicAdd(&a.done_ctr[slot], 1u);
+    if (prev == (unsigned)a.nblocks - 1u) {
+      a.done_ctr[slot] = 0u;
+      __threadfence_system();
+      st_release_sys64(a.done_seq, a.seq);
+    }
+  }
+}
+
+// Even split of `npack` packs over `nb` CTAs.
+__device__ __forceinline__ void split(size_t npack, int nb, int b, size_t& p0, size_t& p1) {
+  const size_t per = (npack + nb - 1) / nb;
+  p0 = (size_t)b * per;
+  if (p0 > npack) p0 = npack;
+  p1 = p0 + per;
+  if (p1 > npack) p1 = npack;
+}
+
+// Slice b of chunk [cs, ce): 16-byte-aligned body split over CTAs, the unaligned
+// head goes to CTA 0 and the tail to the last CTA (identical on every rank).
+template <typename T>
+__device__ __forceinline__ void chunk_slice(size_t cs, size_t ce, int nb, int b, size_t& h0, size_t& h1, size_t& p0,
+                                            size_t& p1, size_t& t0, size_t& t1) {
+  constexpr int W = Pack<T>::W;
+  size_t as = (cs + W - 1) / W * W, ae = ce / W * W;
+  if (as > ae || ae - as < (size_t)W) {  // tiny chunk: all scalar on CTA 0
+    h0 = cs; h1 = (b == 0) ? ce : cs;
+    p0 = p1 = 0; t0 = t1 = 0;
+    return;
+  }
+  h0 = cs; h1 = (b == 0) ? as : cs;
+  t0 = ae; t1 = (b == nb - 1) ? ce : ae;
+  split((ae - as) / W, nb, b, p0, p1);
+  p0 = as / W + p0;
+  p1 = as / W + p1;
+}
+
+// ------------------------------------------------------------------ one-shot (K2)
+template <typename T, int P, bool VIRTUAL, int U>
+__global__ void __launch_bounds__(512) k_oneshot(CommArgs a) {
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int b = blockIdx.x;
+  bool ok = true;
+  if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
+  unsigned bad = 0;
+  if (ok) {
+    const size_t n = a.n;
+    size_t bnd[P + 1];
+#pragma unroll
+    for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
+    const T* src[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
+    T* out = reinterpret_cast<T*>(a.xbar[rank]);
+    size_t p0, p1;
+    split(n / W, a.nblocks, b, p0, p1);
+    for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+      Pack<T> v[U][P];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t pu = p + (size_t)u * blockDim.x;
+        if (pu < p1) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t pu = p + (size_t)u * blockDim.x;
+        if (pu < p1) {
+          const size_t j0 = pu * W;
+          const int c0 = chunk_of<P>(j0, bnd), c1 = chunk_of<P>(j0 + W - 1, bnd);
+          Pack<T> o;
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            T lane[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+            const int c = (c0 == c1) ? c0 : chunk_of<P>(j0 + k, bnd);
+            o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, c));
+            bad += !finite(o.v[k]);
+          }
+          st_stream(out + j0, o);
+        }
+      }
+    }
+    if (b == a.nblocks - 1) {  // scalar tail n % W
+      for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
+        T lane[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) lane[q] = src[q][j];
+        T r = mean_div<T, P>(rot_sum<T, P>(lane, chunk_of<P>(j, bnd)));
+        out[j] = r;
+        bad += !finite(r);
+      }
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  if (!VIRTUAL) publish_done(a);
+}
+
+// ------------------------------------------------------------------ two-shot (K3)
+template <typename T, int P>
+__device__ __forceinline__ T ordered_sum(const T* const (&src)[P], int rank, size_t j) {
+  T v[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) v[q] = src[q][j];
+  return rot_sum<T, P>(v, rank);
+}
+
+template <typename T, int P, bool VIRTUAL, int U, int UAG>
+__global__ void __launch_bounds__(512) k_twoshot(CommArgs a) {
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int b = blockIdx.x;
+  const size_t n = a.n;
+  bool ok = true;
+  unsigned bad = 0;
+  T* out = reinterpret_cast<T*>(a.xbar[rank]);
+  if (a.phases & 1) {
+    if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
+    if (ok) {
+      // reduce-scatter: this rank owns chunk `rank` and sums it in ring order
+      // x_rank, x_rank+1, ..., x_rank-1 (the order the reference ring produces).
+      const T* src[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
+      size_t h0, h1, p0, p1, t0, t1;
+      chunk_slice<T>(chunk_bound(n, P, rank), chunk_bound(n, P, rank + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
+      for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+        Pack<T> v[U][P];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) {
+            Pack<T> o;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+              T lane[P];
+#pragma unroll
+              for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+              o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+              bad += !finite(o.v[k]);
+            }
+            st_plain(out + pu * W, o);
+          }
+        }
+      }
+      for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) {
+        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+        out[j] = r;
+        bad += !finite(r);
+      }
+      for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) {
+        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+        out[j] = r;
+        bad += !finite(r);
+      }
+    }
+  }
+  if (a.phases & 2) {
+    if (!VIRTUAL && ok) ok = cta_barrier<P>(a, 1, b, rank);
+    if (ok) {
+      // all-gather: pull slice b of every other rank's reduced chunk.
+#pragma unroll 1
+      for (int d = 1; d < P; ++d) {
+        const int q = (rank + d) % P;
+        const T* peer = reinterpret_cast<const T*>(a.xbar[q]);
+        size_t h0, h1, p0, p1, t0, t1;
+        chunk_slice<T>(chunk_bound(n, P, q), chunk_bound(n, P, q + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)UAG * blockDim.x) {
+          Pack<T> v[UAG];
+#pragma unroll
+          for (int u = 0; u < UAG; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) v[u] = ld_cg(peer + pu * W);
+          }
+#pragma unroll
+          for (int u = 0; u < UAG; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) st_stream(out + pu * W, v[u]);
+          }
+        }
+        for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) out[j] = peer[j];
+        for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) out[j] = peer[j];
+      }
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  if (!VIRTUAL) publish_done(a);
+}
+
+// ------------------------------------------------------------------ dispatch
+template <int P>
+constexpr int unroll_for() { return P <= 2 ? 4 : (P <= 4 ? 2 : 1); }
+
+template <typename T, bool VIRTUAL>
+int launch_allreduce(int algo, int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
+#define LASGD_CASE(PP)                                                                                    \
+  case PP:                                                                                                \
+    if (algo == LASGD_ALGO_ONESHOT)                                                                       \
+      k_oneshot<T, PP, VIRTUAL, unroll_for<PP>()><<<grid, threads, 0, s>>>(a);                            \
+    else                                                                                                  \
+      k_twoshot<T, PP, VIRTUAL, unroll_for<PP>(), 8><<<grid, threads, 0, s>>>(a);                         \
+    break;
+  switch (P) {
+    LASGD_CASE(1)
+    LASGD_CASE(2)
+    LASGD_CASE(3)
+    LASGD_CASE(4)
+    LASGD_CASE(5)
+    LASGD_CASE(6)
+    LASGD_CASE(7)
+    LASGD_CASE(8)
+    default: return fail(LASGD_ERR_UNSUPPORTED, "world size %d > %d", P, kMaxR);
+  }
+#undef LASGD_CASE
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
+
+int launch_any(int dtype, bool virt, int algo, int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
+  if (dtype == LASGD_F32)
+    return virt ? launch_allreduce<float, true>(algo, P, a, grid, threads, s)
+                : launch_allreduce<float, false>(algo, P, a, grid, threads, s);
+  if (dtype == LASGD_F64)
+    return virt ? launch_allreduce<double, true>(algo, P, a, grid, threads, s)
+                : launch_allreduce<double, false>(algo, P, a, grid, threads, s);
+  return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+}
+
+size_t elem_bytes(int dtype) { return dtype == LASGD_F64 ? 8 : 4; }
+
+// One-shot reads (P-1)*B per rank, two-shot 2(P-1)/P*B plus one extra barrier
+// (~a few microseconds).  P == 2 moves the same bytes either way: one-shot wins.
+int resolve_algo(int algo, int P, size_t bytes) {
+  if (algo != LASGD_ALGO_AUTO) return algo;
+  if (P <= 2) return LASGD_ALGO_ONESHOT;
+  const size_t cutoff = P <= 4 ? (size_t)2 << 20 : (size_t)1 << 20;
+  return bytes <= cutoff ? LASGD_ALGO_ONESHOT : LASGD_ALGO_TWOSHOT;
+}
+
+}  // namespace lasgd
+
+using namespace lasgd;
+
+// ====================================================================== virtual ranks
+extern "C" int lasgd_mean_virtual(void* const* outs, int n_out, const void* const* srcs, int P, size_t n, int dtype,
+                                  int algo, int nblocks, unsigned long long* nonfinite, void* stream) {
+  if (P < 1 || P > kMaxR) return fail(LASGD_ERR_UNSUPPORTED, "P=%d outside [1, %d]", P, kMaxR);
+  if (!outs || !srcs) return fail(LASGD_ERR_INVALID_ARGUMENT, "null pointer array");
+  if (n == 0) return LASGD_OK;
+  if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+  algo = resolve_algo(algo, P, n * elem_bytes(dtype));
+  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown algo %d", algo);
+  if (algo == LASGD_ALGO_TWOSHOT && n_out != P)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "two-shot emulation needs one output per rank (n_out=%d, P=%d)", n_out, P);
+  if (n_out < 1 || n_out > kMaxR) return fail(LASGD_ERR_INVALID_ARGUMENT, "n_out=%d", n_out);
+  if (nblocks <= 0) nblocks = 2 * num_sms();
+  if (nblocks > 65535) nblocks = 65535;
+  CommArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < P; ++q) {
+    if (!srcs[q] || !aligned16(srcs[q])) return fail(LASGD_ERR_INVALID_ARGUMENT, "source %d null or not 16-B aligned", q);
+    a.snap[q] = reinterpret_cast<const char*>(srcs[q]);
+  }
+  for (int r = 0; r < n_out; ++r) {
+    if (!outs[r] || !aligned16(outs[r])) return fail(LASGD_ERR_INVALID_ARGUMENT, "output %d null or not 16-B aligned", r);
+    a.xbar[r] = reinterpret_cast<char*>(outs[r]);
+  }
+  a.n = n;
+  a.nblocks = nblocks;
+  a.skip_signal_phase = -1;
+  a.nonfinite = nonfinite;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid(nblocks, n_out);
+  if (algo == LASGD_ALGO_ONESHOT) {
+    a.phases = 1;
+    return launch_any(dtype, true, algo, P, a, grid, 512, s);
+  }
+  a.phases = 1;  // reduce-scatter of every virtual rank ...
+  int rc = launch_any(dtype, true, algo, P, a, grid, 512, s);
+  if (rc) return rc;
+  a.phases = 2;  // ... then the all-gather (stream order replaces the mid barrier)
+  a.nonfinite = nullptr;
+  return launch_any(dtype, true, algo, P, a, grid, 512, s);
+}
+
+// ====================================================================== communicator
+struct lasgd_comm {
+  int rank = 0, world = 1, device = 0, dtype = LASGD_F32;
+  size_t n = 0, elem = 4;
+  int nblocks = 32, threads = 512;
+  long long timeout_ns = 30LL * 1000000000LL;
+  long long fault_seq = -1;
+  int fault_phase = 0;
+  char* base = nullptr;
+  size_t region_bytes = 0, off_snap[2] = {0, 0}, off_xbar = 0;
+  char* peer_base[kMaxR] = {nullptr};
+  bool opened = false;
+  bool poisoned = false;
+  uint32_t* status_host = nullptr;  // ST_WORDS uint32 + u64 done_seq (host-mapped)
+  uint32_t* status_dev = nullptr;
+  unsigned long long* done_host = nullptr;
+  unsigned long long* done_dev = nullptr;
+  unsigned int* done_ctr = nullptr;
+  unsigned long long seq = 0;  // launches issued
+  cudaEvent_t ev[kEvents];
+  int nev = 0;
+};
+
+static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int dtype, const lasgd_comm_config* cfg,
+                                 lasgd_comm** out) {
+  if (!out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null out");
+  *out = nullptr;
+  if (world < 1 || world > kMaxR) return fail(LASGD_ERR_UNSUPPORTED, "world size %d outside [1, %d]", world, kMaxR);
+  if (rank < 0 || rank >= world) return fail(LASGD_ERR_INVALID_ARGUMENT, "rank %d outside [0, %d)", rank, world);
+  if (n < 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "d must be positive");
+  if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+  lasgd_comm* c = new lasgd_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->dtype = dtype;
+  c->n = n;
+  c->elem = elem_bytes(dtype);
+  if (cfg) {
+    if (cfg->nblocks > 0) c->nblocks = cfg->nblocks;
+    if (cfg->threads > 0) c->threads = cfg->threads;
+    if (cfg->timeout_s > 0) c->timeout_ns = (long long)(cfg->timeout_s * 1e9);
+    c->fault_seq = cfg->fault_seq;
+    c->fault_phase = cfg->fault_phase;
+  }
+  if (c->nblocks < 1 || c->nblocks > kMaxB) {
+    int nb = c->nblocks;
+    delete c;
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d outside [1, %d]", nb, kMaxB);
+  }
+  if (c->threads < 64 || c->threads > 512 || c->threads % 32) {
+    int t = c->threads;
+    delete c;
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "threads=%d must be a multiple of 32 in [64, 512]", t);
+  }
+  DeviceGuard g(device);
+  const size_t bytes = n * c->elem;
+  c->off_snap[0] = round_up(kPadBytes, 4096);
+  c->off_snap[1] = round_up(c->off_snap[0] + bytes, 4096);
+  c->off_xbar = round_up(c->off_snap[1] + bytes, 4096);
+  c->region_bytes = round_up(c->off_xbar + bytes, (size_t)2 << 20);
+  cudaError_t e = cudaMalloc(&c->base, c->region_bytes);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(comm region)");
+  }
+  e = cudaMemset(c->base, 0, c->region_bytes);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->status_host, 4096, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    memset(c->status_host, 0, 4096);
+    e = cudaHostGetDevicePointer((void**)&c->status_dev, c->status_host, 0);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&c->done_ctr, kDoneSlots * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->done_ctr, 0, kDoneSlots * sizeof(unsigned int));
+  for (int i = 0; e == cudaSuccess && i < kEvents; ++i) {
+    e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) c->nev++;
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    int rc = cuda_fail(e, "lasgd_comm_create");
+    lasgd_comm_destroy(c);
+    return rc;
+  }
+  c->done_host = reinterpret_cast<unsigned long long*>(c->status_host + 64);
+  c->done_dev = reinterpret_cast<unsigned long long*>(c->status_dev + 64);
+  c->peer_base[rank] = c->base;
+  *out = c;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_ipc_handle(lasgd_comm* c, void* out) {
+  if (!c || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == LASGD_IPC_HANDLE_BYTES, "IPC handle size");
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  LASGD_CUDA_TRY(cudaIpcGetMemHandle(&h, c->base));
+  memcpy(out, &h, sizeof(h));
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_open(lasgd_comm* c, const void* handles) {
+  if (!c || !handles) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  if (c->opened) return fail(LASGD_ERR_STATE, "communicator already opened");
+  DeviceGuard g(c->device);
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + (size_t)r * LASGD_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle(peer region)");
+    c->peer_base[r] = (char*)p;
+  }
+  c->opened = true;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr) {
+  if (!c || !ptr) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  if (which == 0 || which == 1) *ptr = c->base + c->off_snap[which];
+  else if (which == 2) *ptr = c->base + c->off_xbar;
+  else return fail(LASGD_ERR_INVALID_ARGUMENT, "buffer index %d", which);
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_resolve_algo(lasgd_comm* c, int algo) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  return resolve_algo(algo, c->world, c->n * c->elem);
+}
+
+extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, unsigned long long* seq) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (!c->opened && c->world > 1) return fail(LASGD_ERR_STATE, "lasgd_comm_open has not been called");
+  if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
+  if (c->poisoned || c->status_host[ST_ERR] != ERR_NONE) {
+    c->poisoned = true;
+    return fail(LASGD_ERR_COLLECTIVE, "communicator failed earlier; re-create it");
+  }
+  algo = resolve_algo(algo, c->world, c->n * c->elem);
+  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
+  DeviceGuard g(c->device);
+  const unsigned long long s = ++c->seq;
+  CommArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int r = 0; r < c->world; ++r) {
+    a.snap[r] = c->peer_base[r] + c->off_snap[snap_slot];
+    a.xbar[r] = c->peer_base[r] + c->off_xbar;
+    a.pad[r] = reinterpret_cast<uint32_t*>(c->peer_base[r]);
+  }
+  a.n = c->n;
+  a.rank = c->rank;
+  a.nblocks = c->nblocks;
+  a.epoch = (uint32_t)s;
+  a.phases = 3;
+  a.timeout_ns = c->timeout_ns;
+  a.skip_signal_phase = -1;
+  if ((long long)s == c->fault_seq) {
+    a.skip_signal_phase = c->fault_phase;
+    // collective.py:271-279: the faulting round fails on every rank, this one included
+    uint32_t* st = c->status_host;
+    st[ST_PEER] = c->rank;
+    st[ST_PHASE] = c->fault_phase;
+    st[ST_BLOCK] = 0;
+    st[ST_SEQ_LO] = (uint32_t)(s & 0xffffffffu);
+    st[ST_SEQ_HI] = (uint32_t)(s >> 32);
+    st[ST_RANK] = c->rank;
+    __atomic_store_n(&st[ST_ERR], (uint32_t)ERR_INJECTED, __ATOMIC_SEQ_CST);
+  }
+  a.status = c->status_dev;
+  a.done_ctr = c->done_ctr;
+  a.done_seq = c->done_dev;
+  a.seq = s;
+  a.nonfinite = nullptr;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  int rc = launch_any(c->dtype, false, algo, c->world, a, dim3(c->nblocks, 1), c->threads, cs);
+  if (rc) return rc;
+  LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+  if (seq) *seq = s;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_query(lasgd_comm* c, unsigned long long seq) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  const uint32_t err = __atomic_load_n(&c->status_host[ST_ERR], __ATOMIC_ACQUIRE);
+  if (err != ERR_NONE) {
+    const unsigned long long fs =
+        (unsigned long long)c->status_host[ST_SEQ_LO] | ((unsigned long long)c->status_host[ST_SEQ_HI] << 32);
+    if (seq >= fs) {
+      c->poisoned = true;
+      char buf[256];
+      lasgd_comm_diagnostic(c, buf, sizeof(buf));
+      return fail(LASGD_ERR_COLLECTIVE, "%s", buf);
+    }
+  }
+  if (seq == 0 || seq > c->seq) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown launch %llu", seq);
+  const unsigned long long done = __atomic_load_n(c->done_host, __ATOMIC_ACQUIRE);
+  return done >= seq ? 1 : 0;
+}
+
+extern "C" int lasgd_comm_stream_wait(lasgd_comm* c, unsigned long long seq, void* stream) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (seq == 0 || seq > c->seq) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown launch %llu", seq);
+  DeviceGuard g(c->device);
+  LASGD_CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), c->ev[seq % kEvents], 0));
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_wait(lasgd_comm* c, unsigned long long seq, double timeout_s) {
+  struct timespec t0, t;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (;;) {
+    int rc = lasgd_comm_query(c, seq);
+    if (rc != 0) return rc;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    double el = (t.tv_sec - t0.tv_sec) + 1e-9 * (t.tv_nsec - t0.tv_nsec);
+    if (timeout_s >= 0 && el > timeout_s) return fail(LASGD_ERR_TIMEOUT, "launch %llu not complete after %.3fs", seq, el);
+    struct timespec ns = {0, 20000};
+    nanosleep(&ns, nullptr);
+  }
+}
+
+extern "C" int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len) {
+  if (!c || !buf || !len) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  const uint32_t* st = c->status_host;
+  const unsigned long long fs = (unsigned long long)st[ST_SEQ_LO] | ((unsigned long long)st[ST_SEQ_HI] << 32);
+  const char* phase = st[ST_PHASE] == 0 ? "entry" : "mid";
+  switch (st[ST_ERR]) {
+    case ERR_NONE: snprintf(buf, len, "ok"); break;
+    case ERR_TIMEOUT:
+      snprintf(buf, len, "rank %u timed out waiting for rank %u at the %s barrier of launch %llu (CTA %u)", st[ST_RANK],
+               st[ST_PEER], phase, fs, st[ST_BLOCK]);
+      break;
+    case ERR_INJECTED:
+      snprintf(buf, len, "injected fault in launch %llu at the %s barrier (rank %u)", fs, phase, st[ST_RANK]);
+      break;
+    default: snprintf(buf, len, "unknown failure code %u", st[ST_ERR]);
+  }
+  return LASGD_OK;
+}
+
+extern "C" unsigned long long lasgd_comm_bytes_per_node(lasgd_comm* c, int algo) {
+  if (!c || c->world <= 1) return 0;
+  algo = resolve_algo(algo, c->world, c->n * c->elem);
+  const unsigned long long B = (unsigned long long)c->n * c->elem;
+  if (algo == LASGD_ALGO_ONESHOT) return (unsigned long long)(c->world - 1) * B;
+  return lasgd_bytes_per_node(c->n, c->world, (int)c->elem, -1);
+}
+
+extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
+  if (!c) return LASGD_OK;
+  DeviceGuard g(c->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->world; ++r)
+    if (r != c->rank && c->peer_base[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
+  for (int i = 0; i < c->nev; ++i) cudaEventDestroy(c->ev[i]);
+  if (c->done_ctr) cudaFree(c->done_ctr);
+  if (c->status_host) cudaFreeHost(c->status_host);
+  if (c->base) cudaFree(c->base);
+  delete c;
+  return LASGD_OK;
+}

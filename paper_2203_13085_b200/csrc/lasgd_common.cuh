@@ -1,0 +1,97 @@
+// Shared device/host helpers for the LASGD sync kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "lasgd_sync.h"
+
+namespace lasgd {
+
+// ---------------------------------------------------------------- errors
+void set_last_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define LASGD_CUDA_TRY(expr)                                 \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return ::lasgd::cuda_fail(_e, #expr); \
+  } while (0)
+
+int num_sms();  // SM count of the current device (cached per device)
+
+// ---------------------------------------------------------------- arithmetic
+// Separately rounded ops (the reference's numpy never contracts a*b+c).
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ bool finite(float a) { return isfinite(a); }
+__device__ __forceinline__ bool finite(double a) { return isfinite(a); }
+
+// ---------------------------------------------------------------- 128-bit packs
+template <typename T>
+struct alignas(16) Pack {
+  static constexpr int W = 16 / sizeof(T);
+  T v[W];
+};
+
+// Streaming loads/stores (evict-first): the sync path touches every byte once per
+// launch and every buffer is >> L2 at ResNet-50 size.
+template <typename T>
+__device__ __forceinline__ Pack<T> ld_stream(const T* p) {
+  uint4 r = __ldcs(reinterpret_cast<const uint4*>(p));
+  return *reinterpret_cast<Pack<T>*>(&r);
+}
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, const Pack<T>& v) {
+  __stcs(reinterpret_cast<uint4*>(p), *reinterpret_cast<const uint4*>(&v));
+}
+// L2-only (L1-bypassing) load, used for peer (NVLink-mapped) memory.
+template <typename T>
+__device__ __forceinline__ Pack<T> ld_cg(const T* p) {
+  uint4 r = __ldcg(reinterpret_cast<const uint4*>(p));
+  return *reinterpret_cast<Pack<T>*>(&r);
+}
+template <typename T>
+__device__ __forceinline__ void st_plain(T* p, const Pack<T>& v) {
+  *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(&v);
+}
+
+// Warp-aggregated non-finite counter (one atomic per warp, only when non-zero).
+__device__ __forceinline__ void report_nonfinite(unsigned long long* ctr, unsigned bad) {
+  if (ctr == nullptr) return;
+  unsigned total = __reduce_add_sync(0xffffffffu, bad);
+  if (total != 0 && (threadIdx.x & 31) == 0) atomicAdd(ctr, (unsigned long long)total);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Grid for a streaming kernel: enough CTAs to fill every SM `per_sm` times, never more
+// than the work needs.
+inline int stream_grid(size_t work_items, int threads, int per_sm = 8) {
+  size_t need = (work_items + threads - 1) / threads;
+  size_t cap = (size_t)num_sms() * per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+// RAII device switch for comm calls.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace lasgd

@@ -1,0 +1,344 @@
+// Rank-local streaming kernels of the LASGD sync path: K0 blend, K1 snapshot,
+// K4 elastic pull / reference finalize, K5 fused local SGD step.
+//
+// All are HBM-bound elementwise passes over the flat parameter buffer: 128-bit
+// evict-first loads/stores, U independent packs in flight per thread,
+// grid = 8 CTAs x 256 threads per SM (full occupancy), scalar tail for n % W,
+// warp-aggregated non-finite counter fused into the pass (the reference checks
+// every blend result, params.py:88).  No tensor cores: there is no reuse.
+//
+// Reference anchors: blend params.py:80-89; sgd_local_step optimizer.py:136-149;
+// lasgd_finalize_round optimizer.py:152-178; pull = blend order of
+// optimizer.py:256-257 (Algorithm 1 line 9a, PAPER.md:182 for alpha = 1).
+
+#include <stdarg.h>
+#include <string.h>
+
+#include "lasgd_common.cuh"
+
+namespace lasgd {
+
+// ------------------------------------------------------------- generic driver
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+template <typename T, typename Op, int U>
+__global__ void __launch_bounds__(kThreads) k_stream(Op op, size_t n, unsigned long long* nonfinite) {
+  constexpr int W = Pack<T>::W;
+  const size_t npack = n / W;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned bad = 0;
+  for (; i + (U - 1) * stride < npack; i += U * stride) {
+    typename Op::Loaded L[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) op.load(L[u], (i + u * stride) * W);
+#pragma unroll
+    for (int u = 0; u < U; ++u) bad += op.compute_store(L[u], (i + u * stride) * W);
+  }
+  for (; i < npack; i += stride) {
+    typename Op::Loaded L;
+    op.load(L, i * W);
+    bad += op.compute_store(L, i * W);
+  }
+  const size_t t = npack * W + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) bad += op.scalar(t);
+  report_nonfinite(nonfinite, bad);
+}
+
+// Fallback for buffers that are not 16-byte aligned (e.g. arbitrary views).
+template <typename T, typename Op>
+__global__ void __launch_bounds__(kThreads) k_scalar(Op op, size_t n, unsigned long long* nonfinite) {
+  unsigned bad = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    bad += op.scalar(i);
+  report_nonfinite(nonfinite, bad);
+}
+
+template <typename T, typename Op>
+int launch(const Op& op, size_t n, bool aligned, unsigned long long* nonfinite, void* stream) {
+  if (n == 0) return LASGD_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (aligned) {
+    const size_t npack = n / Pack<T>::W;
+    const size_t work = npack > (size_t)kThreads ? npack : (size_t)kThreads;
+    k_stream<T, Op, kUnroll><<<stream_grid(work, kThreads), kThreads, 0, s>>>(op, n, nonfinite);
+  } else {
+    k_scalar<T, Op><<<stream_grid(n, kThreads), kThreads, 0, s>>>(op, n, nonfinite);
+  }
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
+
+// ------------------------------------------------------------- K0 blend
+template <typename T>
+struct BlendOp {
+  T* out;
+  const T* u;
+  const T* v;
+  T a, b;
+  struct Loaded { Pack<T> u, v; };
+  __device__ __forceinline__ unsigned elem(T uu, T vv, T& o) const {
+    o = add_rn(mul_rn(a, uu), mul_rn(b, vv));
+    return !finite(o);
+  }
+  __device__ __forceinline__ void load(Loaded& L, size_t j) const {
+    L.u = ld_stream(u + j);
+    L.v = ld_stream(v + j);
+  }
+  __device__ __forceinline__ unsigned compute_store(const Loaded& L, size_t j) const {
+    Pack<T> o;
+    unsigned bad = 0;
+#pragma unroll
+    for (int k = 0; k < Pack<T>::W; ++k) bad += elem(L.u.v[k], L.v.v[k], o.v[k]);
+    st_stream(out + j, o);
+    return bad;
+  }
+  __device__ __forceinline__ unsigned scalar(size_t j) const {
+    T o;
+    unsigned bad = elem(u[j], v[j], o);
+    out[j] = o;
+    return bad;
+  }
+};
+
+// ------------------------------------------------------------- K1 snapshot
+template <typename T>
+struct CopyOp {
+  T* dst;
+  const T* src;
+  struct Loaded { Pack<T> s; };
+  __device__ __forceinline__ void load(Loaded& L, size_t j) const { L.s = ld_stream(src + j); }
+  __device__ __forceinline__ unsigned compute_store(const Loaded& L, size_t j) const {
+    st_stream(dst + j, L.s);
+    return 0;
+  }
+  __device__ __forceinline__ unsigned scalar(size_t j) const {
+    dst[j] = src[j];
+    return 0;
+  }
+};
+
+// ------------------------------------------------------------- K5 local step
+template <typename T>
+struct SgdOp {
+  T* x;
+  const T* g;
+  T* m;
+  T* delta;
+  T neg_lr, mu, omd, wd;
+  bool use_wd, use_mom, nesterov, first, use_delta, reset;
+  struct Loaded { Pack<T> x, g, m, d; };
+
+  __device__ __forceinline__ unsigned elem(T& xv, T gv, T& mv, T& dv) const {
+    T dir = gv;
+    if (use_wd) dir = add_rn(dir, mul_rn(wd, xv));
+    if (use_mom) {
+      mv = first ? dir : add_rn(mul_rn(mu, mv), mul_rn(omd, dir));
+      dir = nesterov ? add_rn(dir, mul_rn(mu, mv)) : mv;
+    }
+    const T s = mul_rn(neg_lr, dir);
+    xv = add_rn(xv, s);
+    unsigned bad = !finite(xv);
+    if (use_delta) {
+      dv = add_rn(reset ? T(0) : dv, s);
+      bad += !finite(dv);
+    }
+    return bad;
+  }
+  __device__ __forceinline__ void load(Loaded& L, size_t j) const {
+    L.x = ld_stream(x + j);
+    L.g = ld_stream(g + j);
+    if (use_mom && !first) L.m = ld_stream(m + j);
+    if (use_delta && !reset) L.d = ld_stream(delta + j);
+  }
+  __device__ __forceinline__ unsigned compute_store(Loaded& L, size_t j) const {
+    unsigned bad = 0;
+#pragma unroll
+    for (int k = 0; k < Pack<T>::W; ++k) bad += elem(L.x.v[k], L.g.v[k], L.m.v[k], L.d.v[k]);
+    st_stream(x + j, L.x);
+    if (use_mom) st_stream(m + j, L.m);
+    if (use_delta) st_stream(delta + j, L.d);
+    return bad;
+  }
+  __device__ __forceinline__ unsigned scalar(size_t j) const {
+    T xv = x[j], mv = (use_mom && !first) ? m[j] : T(0), dv = (use_delta && !reset) ? delta[j] : T(0);
+    unsigned bad = elem(xv, g[j], mv, dv);
+    x[j] = xv;
+    if (use_mom) m[j] = mv;
+    if (use_delta) delta[j] = dv;
+    return bad;
+  }
+};
+
+// ------------------------------------------------------------- K4 pull / finalize
+template <typename T>
+struct PullOp {
+  T* x;
+  T* snap_next;
+  const T* snap;
+  const T* xbar;
+  T neg_alpha;
+  struct Loaded { Pack<T> x, s, z; };
+  __device__ __forceinline__ unsigned elem(T& xv, T sv, T zv) const {
+    const T diff = add_rn(sv, mul_rn(T(-1), zv));  // blend(1, snap, -1, xbar)
+    xv = add_rn(xv, mul_rn(neg_alpha, diff));      // blend(1, x, -alpha, diff)
+    return !finite(diff) + !finite(xv);
+  }
+  __device__ __forceinline__ void load(Loaded& L, size_t j) const {
+    L.x = ld_stream(x + j);
+    L.s = ld_stream(snap + j);
+    L.z = ld_stream(xbar + j);
+  }
+  __device__ __forceinline__ unsigned compute_store(Loaded& L, size_t j) const {
+    unsigned bad = 0;
+#pragma unroll
+    for (int k = 0; k < Pack<T>::W; ++k) bad += elem(L.x.v[k], L.s.v[k], L.z.v[k]);
+    st_stream(x + j, L.x);
+    if (snap_next) st_stream(snap_next + j, L.x);
+    return bad;
+  }
+  __device__ __forceinline__ unsigned scalar(size_t j) const {
+    T xv = x[j];
+    unsigned bad = elem(xv, snap[j], xbar[j]);
+    x[j] = xv;
+    if (snap_next) snap_next[j] = xv;
+    return bad;
+  }
+};
+
+template <typename T>
+struct FinalizeOp {
+  T* x;
+  T* snap_next;
+  const T* z;
+  const T* delta;
+  struct Loaded { Pack<T> z, d; };
+  __device__ __forceinline__ void load(Loaded& L, size_t j) const {
+    L.z = ld_stream(z + j);
+    L.d = ld_stream(delta + j);
+  }
+  __device__ __forceinline__ unsigned compute_store(Loaded& L, size_t j) const {
+    Pack<T> o;
+    unsigned bad = 0;
+#pragma unroll
+    for (int k = 0; k < Pack<T>::W; ++k) {
+      o.v[k] = add_rn(L.z.v[k], L.d.v[k]);  // blend(1, z, 1, delta), optimizer.py:171
+      bad += !finite(o.v[k]);
+    }
+    st_stream(x + j, o);
+    if (snap_next) st_stream(snap_next + j, o);
+    return bad;
+  }
+  __device__ __forceinline__ unsigned scalar(size_t j) const {
+    T o = add_rn(z[j], delta[j]);
+    x[j] = o;
+    if (snap_next) snap_next[j] = o;
+    return !finite(o);
+  }
+};
+
+// ------------------------------------------------------------- typed entry points
+template <typename T>
+int blend_t(void* out, double a, const void* u, double b, const void* v, size_t n, unsigned long long* nf,
+            void* s) {
+  BlendOp<T> op{(T*)out, (const T*)u, (const T*)v, (T)a, (T)b};
+  return launch<T>(op, n, aligned16(out) && aligned16(u) && aligned16(v), nf, s);
+}
+
+template <typename T>
+int copy_t(void* dst, const void* src, size_t n, void* s) {
+  CopyOp<T> op{(T*)dst, (const T*)src};
+  return launch<T>(op, n, aligned16(dst) && aligned16(src), nullptr, s);
+}
+
+template <typename T>
+int sgd_t(void* x, const void* g, void* m, void* delta, size_t n, const lasgd_sgd_params* p,
+          unsigned long long* nf, void* s) {
+  SgdOp<T> op;
+  op.x = (T*)x;
+  op.g = (const T*)g;
+  op.m = (T*)m;
+  op.delta = (T*)delta;
+  op.neg_lr = (T)(-p->lr);
+  op.mu = (T)p->momentum;
+  op.omd = (T)(1.0 - p->dampening);
+  op.wd = (T)p->weight_decay;
+  op.use_wd = p->weight_decay != 0.0;
+  op.use_mom = p->momentum != 0.0;
+  op.nesterov = p->nesterov != 0;
+  op.first = p->first_step != 0;
+  op.use_delta = delta != nullptr;
+  op.reset = p->delta_reset != 0;
+  bool al = aligned16(x) && aligned16(g) && (!op.use_mom || aligned16(m)) && (!op.use_delta || aligned16(delta));
+  return launch<T>(op, n, al, nf, s);
+}
+
+template <typename T>
+int pull_t(void* x, void* snap_next, const void* snap, const void* xbar, size_t n, double alpha,
+           unsigned long long* nf, void* s) {
+  PullOp<T> op{(T*)x, (T*)snap_next, (const T*)snap, (const T*)xbar, (T)(-alpha)};
+  bool al = aligned16(x) && aligned16(snap) && aligned16(xbar) && (!snap_next || aligned16(snap_next));
+  return launch<T>(op, n, al, nf, s);
+}
+
+template <typename T>
+int finalize_t(void* x, void* snap_next, const void* z, const void* delta, size_t n, unsigned long long* nf,
+               void* s) {
+  FinalizeOp<T> op{(T*)x, (T*)snap_next, (const T*)z, (const T*)delta};
+  bool al = aligned16(x) && aligned16(z) && aligned16(delta) && (!snap_next || aligned16(snap_next));
+  return launch<T>(op, n, al, nf, s);
+}
+
+}  // namespace lasgd
+
+// ============================================================== C ABI
+using namespace lasgd;
+
+#define DISPATCH_DTYPE(dtype, CALL_F32, CALL_F64)                                   \
+  do {                                                                              \
+    if ((dtype) == LASGD_F32) return CALL_F32;                                      \
+    if ((dtype) == LASGD_F64) return CALL_F64;                                      \
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)(dtype));      \
+  } while (0)
+
+extern "C" int lasgd_blend(void* out, double a, const void* u, double b, const void* v, size_t n, int dtype,
+                           unsigned long long* nonfinite, void* stream) {
+  if (n && (!out || !u || !v)) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_blend: null buffer");
+  DISPATCH_DTYPE(dtype, blend_t<float>(out, a, u, b, v, n, nonfinite, stream),
+                 blend_t<double>(out, a, u, b, v, n, nonfinite, stream));
+}
+
+extern "C" int lasgd_snapshot(void* snap, const void* x, size_t n, int dtype, void* stream) {
+  if (n && (!snap || !x)) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_snapshot: null buffer");
+  if (snap == x) return LASGD_OK;
+  DISPATCH_DTYPE(dtype, copy_t<float>(snap, x, n, stream), copy_t<double>(snap, x, n, stream));
+}
+
+extern "C" int lasgd_sgd_step(void* x, const void* g, void* m, void* delta, size_t n, int dtype,
+                              const lasgd_sgd_params* p, unsigned long long* nonfinite, void* stream) {
+  if (!p) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_sgd_step: null params");
+  if (n && (!x || !g)) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_sgd_step: null buffer");
+  if (p->momentum != 0.0 && !m) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_sgd_step: momentum needs m");
+  if (p->momentum < 0.0 || p->weight_decay < 0.0 || p->dampening < 0.0 || p->dampening > 1.0)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_sgd_step: invalid hyper-parameters");
+  if (p->nesterov && (p->momentum <= 0.0 || p->dampening != 0.0))
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "Nesterov momentum requires a momentum and zero dampening");
+  DISPATCH_DTYPE(dtype, sgd_t<float>(x, g, m, delta, n, p, nonfinite, stream),
+                 sgd_t<double>(x, g, m, delta, n, p, nonfinite, stream));
+}
+
+extern "C" int lasgd_elastic_pull(void* x, void* snap_next, const void* snap, const void* xbar, size_t n,
+                                  int dtype, double alpha, unsigned long long* nonfinite, void* stream) {
+  if (n && (!x || !snap || !xbar)) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_elastic_pull: null buffer");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(LASGD_ERR_INVALID_ARGUMENT, "alpha must be in [0, 1], got %g", alpha);
+  DISPATCH_DTYPE(dtype, pull_t<float>(x, snap_next, snap, xbar, n, alpha, nonfinite, stream),
+                 pull_t<double>(x, snap_next, snap, xbar, n, alpha, nonfinite, stream));
+}
+
+extern "C" int lasgd_finalize(void* x, void* snap_next, const void* z, const void* delta, size_t n, int dtype,
+                              unsigned long long* nonfinite, void* stream) {
+  if (n && (!x || !z || !delta)) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_finalize: null buffer");
+  DISPATCH_DTYPE(dtype, finalize_t<float>(x, snap_next, z, delta, n, nonfinite, stream),
+                 finalize_t<double>(x, snap_next, z, delta, n, nonfinite, stream));
+}

@@ -1,0 +1,54 @@
+"""Flat parameter / gradient buffers behind a torch module.
+
+Every trainable parameter becomes a view into ONE contiguous fp32 buffer ``x``
+and its ``.grad`` a view into ONE contiguous buffer ``g``, so cuDNN's backward
+accumulates gradients straight into the buffer the sync kernels stream over.
+The layout is the module's parameter order, each tensor row-major — for an MLP
+this is exactly the reference MlpOracle's flat vector (problems.py:202-205:
+W_l row-major then b_l).  4-D weights can be exposed as channels_last-strided
+views over the same contiguous storage.  BatchNorm running statistics are
+buffers, not parameters: they stay rank-local (not averaged).
+"""
+
+from __future__ import annotations
+
+import torch
+
+
+class FlatParams:
+    def __init__(self, module: torch.nn.Module, dtype: torch.dtype = torch.float32, device=None,
+                 channels_last: bool = False):
+        params = [p for p in module.parameters() if p.requires_grad]
+        if not params:
+            raise ValueError("module has no trainable parameters")
+        device = device or params[0].device
+        self.numel = sum(p.numel() for p in params)
+        self.x = torch.empty(self.numel, dtype=dtype, device=device)
+        self.g = torch.zeros(self.numel, dtype=dtype, device=device)
+        self.params = params
+        self.offsets = []
+        off = 0
+        with torch.no_grad():
+            for p in params:
+                n = p.numel()
+                v = self._view(self.x, off, p.shape, channels_last)
+                v.copy_(p.detach())
+                p.data = v
+                p.grad = self._view(self.g, off, p.shape, channels_last)
+                self.offsets.append(off)
+                off += n
+
+    @staticmethod
+    def _view(buf: torch.Tensor, off: int, shape, channels_last: bool) -> torch.Tensor:
+        n = 1
+        for s in shape:
+            n *= s
+        flat = buf[off:off + n]
+        if channels_last and len(shape) == 4:
+            o, i, h, w = shape
+            return flat.view(o, h, w, i).permute(0, 3, 1, 2)  # NHWC storage, NCHW shape
+        return flat.view(shape)
+
+    def zero_grad(self) -> None:
+        """One memset over the flat gradient buffer (grads stay attached as views)."""
+        self.g.zero_()

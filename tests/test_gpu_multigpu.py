@@ -1,0 +1,161 @@
+"""Multi-GPU parity of the NVLink P2P path (one process per GPU, IPC-mapped peers):
+K2 one-shot / K3 two-shot bit-exact against the ring-order oracle on every rank,
+the LASGDWorker round protocol (double-buffered snapshots, side stream) bit-exact
+against the oracle's deterministic-k loop, and the watchdog turning a missing
+peer flag into CollectiveFailure on every rank.  Skipped with < 2 GPUs."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _init(rank, world, port):
+    import torch.distributed as dist
+
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+
+def _same_bits(a, b):
+    iv = {4: np.uint32, 8: np.uint64}[a.dtype.itemsize]
+    return a.shape == b.shape and np.array_equal(a.view(iv), b.view(iv))
+
+
+def _vec(seed, n, dtype=np.float32):
+    return np.random.default_rng(seed).standard_normal(n).astype(dtype)
+
+
+def _w_allreduce(rank, world, port):
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+    from paper_2203_13085_b200 import _native as N
+
+    _init(rank, world, port)
+    for dtype in (torch.float32, torch.float64):
+        npdt = np.float32 if dtype == torch.float32 else np.float64
+        for n in (3, 1001, 65_537, 4_000_037):
+            comm = L.P2PCommunicator(n, dtype=dtype, nblocks=24, timeout_s=20.0)
+            for rnd in range(4):
+                for algo in (N.ALGO_ONESHOT, N.ALGO_TWOSHOT):
+                    slot = rnd % 2
+                    vecs = [_vec(1000 * rnd + 10 * r + algo + n, n, npdt) for r in range(world)]
+                    comm.snapshots[slot].copy_(torch.from_numpy(vecs[rank]))
+                    torch.cuda.synchronize()
+                    seq = comm.allreduce(slot, algo)
+                    assert comm.wait(seq, 30.0) == 1
+                    torch.cuda.synchronize()
+                    got = comm.xbar.cpu().numpy()
+                    assert _same_bits(got, O.ring_mean(vecs)), (n, rnd, algo, rank)
+            dist.barrier()
+            comm.close()
+    dist.destroy_process_group()
+
+
+def _w_worker_loop(rank, world, port):
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+
+    _init(rank, world, port)
+    n, steps = 100_003, 9
+    x0 = _vec(7, n)
+    grads = np.stack([np.stack([_vec(100 * t + r, n) for r in range(world)]) for t in range(steps)])
+    for k, alpha, sgd in [(2, 1.0, None), (1, 0.5, L.SgdConfig(0.9, 0.0, 1e-4, True)), (3, 0.25, None)]:
+        comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
+        x = torch.from_numpy(x0.copy()).cuda()
+        g = torch.empty_like(x)
+        compute = torch.cuda.Stream(priority=-1)
+        with torch.cuda.stream(compute):
+            w = L.LASGDWorker(x, g, comm=comm, sync_period=k, alpha=alpha, sgd=sgd, lr=0.05, mode="pull",
+                              compute_stream=compute)
+            for t in range(steps):
+                g.copy_(torch.from_numpy(grads[t, rank]), non_blocking=False)
+                w.step()
+            w.drain()
+        torch.cuda.synchronize()
+        cfg = None if sgd is None else O.SgdConfig(0.05, sgd.momentum, sgd.dampening, sgd.weight_decay, sgd.nesterov)
+        xs, _, _, _ = O.run_lasgd_pull(x0, grads, np.full(steps, 0.05), world, k, alpha, sgd=cfg)
+        assert _same_bits(x.cpu().numpy(), xs[rank]), (k, alpha, rank)
+        dist.barrier()
+        comm.close()
+    # reference bookkeeping (delta mode) through the worker
+    comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
+    x = torch.from_numpy(x0.copy()).cuda()
+    g = torch.empty_like(x)
+    w = L.LASGDWorker(x, g, comm=comm, sync_period=2, lr=0.05, mode="delta")
+    for t in range(steps):
+        g.copy_(torch.from_numpy(grads[t, rank]))
+        w.step()
+    w.drain()
+    torch.cuda.synchronize()
+    xs, _, _, _ = O.run_lasgd_delta(x0, grads, np.full(steps, 0.05), world, 2)
+    assert _same_bits(x.cpu().numpy(), xs[rank])
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+
+
+def _w_fault(rank, world, port):
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from paper_2203_13085_b200 import _native as N
+
+    _init(rank, world, port)
+    for algo, phase in ((N.ALGO_TWOSHOT, 1), (N.ALGO_ONESHOT, 0)):
+        comm = L.P2PCommunicator(4096, nblocks=8, timeout_s=1.0, fault_seq=2 if rank == 1 else -1, fault_phase=phase)
+        tr = L.CudaP2PTransport(comm, algo=algo)
+        h1 = tr.submit(0, rank, comm.snapshots[0])
+        assert h1.wait(30.0) and h1.status is L.Status.COMPLETE
+        h2 = tr.submit(1, rank, comm.snapshots[1])
+        assert h2.wait(30.0)
+        assert h2.status is L.Status.FAILED, (rank, h2.status)
+        assert ("timed out" in h2.diagnostic) or ("injected" in h2.diagnostic)
+        with pytest.raises(L.CollectiveFailure):
+            h2.result
+        with pytest.raises(L.CollectiveFailure):
+            tr.submit(2, rank, comm.snapshots[0])  # poisoned communicator
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.close()
+    dist.destroy_process_group()
+
+
+def _spawn(fn):
+    import torch.multiprocessing as mp
+
+    world = min(NGPU, 4)
+    mp.spawn(fn, args=(world, _free_port()), nprocs=world, join=True)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_p2p_allreduce_bit_exact():
+    _spawn(_w_allreduce)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_worker_round_protocol_bit_exact():
+    _spawn(_w_worker_loop)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_watchdog_fault_fails_every_rank():
+    _spawn(_w_fault)
