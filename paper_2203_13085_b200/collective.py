@@ -269,6 +269,23 @@ class _CudaBuf:
         self._owner = owner
 
 
+def exchange_handles(mine: bytes, world: int, group=None) -> bytes:
+    """All-gather every rank's fixed-size IPC handle, concatenated in rank order
+    (the layout lasgd_comm_open expects).  Works over any torch.distributed backend."""
+    import torch.distributed as dist
+
+    if len(mine) != N.IPC_HANDLE_BYTES:
+        raise ValueError(f"IPC handle must be {N.IPC_HANDLE_BYTES} bytes, got {len(mine)}")
+    if world == 1:
+        return mine
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine, group=group)
+    for r, h in enumerate(gathered):
+        if not isinstance(h, bytes) or len(h) != N.IPC_HANDLE_BYTES:
+            raise RuntimeError(f"rank {r} sent a malformed IPC handle")
+    return b"".join(gathered)
+
+
 class P2PCommunicator:
     """One rank's endpoint of the NVLink P2P mean all-reduce (K2/K3/K6).
 
@@ -302,9 +319,7 @@ class P2PCommunicator:
         N.check(N.lib().lasgd_comm_ipc_handle(self._h, buf), "lasgd_comm_ipc_handle")
         mine = bytes(buf.raw)
         if world > 1:
-            gathered = [None] * world
-            dist.all_gather_object(gathered, mine, group=group)
-            allh = b"".join(gathered)
+            allh = exchange_handles(mine, world, group)
             N.check(N.lib().lasgd_comm_open(self._h, allh), "lasgd_comm_open")
         typestr = "<f4" if dtype == torch.float32 else "<f8"
         self.snapshots = []
