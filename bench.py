@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--sync-period", type=int, default=1)
     ap.add_argument("--alpha", type=float, default=1.0)
     ap.add_argument("--algo", choices=["auto", "oneshot", "twoshot"], default="auto")
-    ap.add_argument("--nblocks", type=int, default=32)
+    ap.add_argument("--nblocks", type=int, default=128)
     ap.add_argument("--train-steps", type=int, default=10)
     ap.add_argument("--train-warmup", type=int, default=4)
     ap.add_argument("--no-train", action="store_true")

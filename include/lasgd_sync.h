@@ -53,7 +53,7 @@ extern "C" {
 #define LASGD_ALGO_TWOSHOT 2
 
 #define LASGD_MAX_RANKS 8
-#define LASGD_MAX_BLOCKS 128
+#define LASGD_MAX_BLOCKS 256
 #define LASGD_IPC_HANDLE_BYTES 64
 
 int lasgd_abi_version(void);
@@ -61,6 +61,10 @@ const char* lasgd_strerror(int code);
 const char* lasgd_last_error(void);
 
 /* ---- rank-local streaming kernels (HBM-bound) -------------------------- */
+
+/* Occupancy of the streaming kernels (CTAs of 256 threads per SM, default 2).
+ * Lower values leave room for the side-stream all-reduce to run concurrently. */
+int lasgd_set_stream_ctas_per_sm(int ctas_per_sm);
 
 /* K0: out = a*u + b*v.  Replaces params.py:80-89 `blend` (out-of-place). */
 int lasgd_blend(void* out, double a, const void* u, double b, const void* v, size_t n, int dtype,
@@ -119,7 +123,7 @@ typedef struct lasgd_comm lasgd_comm;
 
 typedef struct {
   int nblocks;          /* SM budget: CTAs of the all-reduce kernel (<= LASGD_MAX_BLOCKS)     */
-  int threads;          /* threads per CTA (multiple of 32, >= world)                         */
+  int threads;          /* threads per CTA (multiple of 32 in [64, 256]; <= 128 regs each)     */
   double timeout_s;     /* watchdog for a peer flag (→ CollectiveFailure), e.g. 30.0          */
   long long fault_seq;  /* TEST KNOB: skip this rank's flag writes in launch #fault_seq (-1 off) */
   int fault_phase;      /* 0 entry barrier, 1 mid barrier                                     */
@@ -154,6 +158,14 @@ int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len);
 /* NVLink bytes this rank's peers read from it in one launch (collective.py:206-226 analogue). */
 unsigned long long lasgd_comm_bytes_per_node(lasgd_comm* c, int algo);
 int lasgd_comm_resolve_algo(lasgd_comm* c, int algo);
+/* Change the SM budget (CTAs per launch) for subsequent launches; every rank must
+ * make the same call between the same two launches. */
+int lasgd_comm_set_nblocks(lasgd_comm* c, int nblocks);
+/* Tracing: when on, every CTA of each launch records %globaltimer stamps (start,
+ * entry barrier passed, mid barrier passed, end) — the timeline of the last launch
+ * is read back (synchronising) with lasgd_comm_read_trace into out[ctas][4]. */
+int lasgd_comm_set_trace(lasgd_comm* c, int on);
+int lasgd_comm_read_trace(lasgd_comm* c, unsigned long long* out, int max_ctas);
 int lasgd_comm_destroy(lasgd_comm* c);
 
 /* ---- host utilities ------------------------------------------------------ */

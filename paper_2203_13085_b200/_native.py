@@ -31,7 +31,7 @@ ALGO_AUTO = 0
 ALGO_ONESHOT = 1
 ALGO_TWOSHOT = 2
 MAX_RANKS = 8
-MAX_BLOCKS = 128
+MAX_BLOCKS = 256
 IPC_HANDLE_BYTES = 64
 
 
@@ -84,6 +84,7 @@ SIGNATURES = {
     "lasgd_abi_version": (_I, []),
     "lasgd_strerror": (ctypes.c_char_p, [_I]),
     "lasgd_last_error": (ctypes.c_char_p, []),
+    "lasgd_set_stream_ctas_per_sm": (_I, [_I]),
     "lasgd_blend": (_I, [_P, _D, _P, _D, _P, _SZ, _I, _P, _P]),
     "lasgd_snapshot": (_I, [_P, _P, _SZ, _I, _P]),
     "lasgd_sgd_step": (_I, [_P, _P, _P, _P, _SZ, _I, ctypes.POINTER(SgdParams), _P, _P]),
@@ -101,6 +102,9 @@ SIGNATURES = {
     "lasgd_comm_diagnostic": (_I, [_P, ctypes.c_char_p, _SZ]),
     "lasgd_comm_bytes_per_node": (ctypes.c_ulonglong, [_P, _I]),
     "lasgd_comm_resolve_algo": (_I, [_P, _I]),
+    "lasgd_comm_set_nblocks": (_I, [_P, _I]),
+    "lasgd_comm_set_trace": (_I, [_P, _I]),
+    "lasgd_comm_read_trace": (_I, [_P, _P, _I]),
     "lasgd_comm_destroy": (_I, [_P]),
     "lasgd_partition_chunks": (_I, [_SZ, _I, ctypes.POINTER(_SZ)]),
     "lasgd_bytes_per_node": (ctypes.c_ulonglong, [_SZ, _I, _I, _I]),

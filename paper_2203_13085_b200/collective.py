@@ -296,7 +296,7 @@ class P2PCommunicator:
     """
 
     def __init__(self, n: int, *, dtype: torch.dtype = torch.float32, rank: Optional[int] = None,
-                 world: Optional[int] = None, device=None, group=None, nblocks: int = 32, threads: int = 512,
+                 world: Optional[int] = None, device=None, group=None, nblocks: int = 96, threads: int = 256,
                  timeout_s: float = 30.0, fault_seq: int = -1, fault_phase: int = 0, stream_priority: int = 0):
         import torch.distributed as dist
 
@@ -365,6 +365,20 @@ class P2PCommunicator:
 
     def resolve_algo(self, algo: int = N.ALGO_AUTO) -> int:
         return N.lib().lasgd_comm_resolve_algo(self._h, algo)
+
+    def set_nblocks(self, nblocks: int) -> None:
+        """SM budget of later launches (collective: every rank must call it identically)."""
+        N.check(N.lib().lasgd_comm_set_nblocks(self._h, int(nblocks)), "set_nblocks")
+
+    def set_trace(self, on: bool) -> None:
+        N.check(N.lib().lasgd_comm_set_trace(self._h, int(bool(on))))
+
+    def read_trace(self):
+        """Per-CTA globaltimer stamps (ns) of the last traced launch: list of
+        (start, entry_passed, mid_passed, end); synchronises the device."""
+        buf = (ctypes.c_ulonglong * (N.MAX_BLOCKS * 4))()
+        nb = N.check(N.lib().lasgd_comm_read_trace(self._h, buf, N.MAX_BLOCKS), "read_trace")
+        return [tuple(buf[4 * b + k] for k in range(4)) for b in range(nb)]
 
     def bytes_per_node(self, algo: int = N.ALGO_AUTO) -> int:
         return int(N.lib().lasgd_comm_bytes_per_node(self._h, algo))

@@ -59,7 +59,14 @@ struct CommArgs {
   unsigned long long* done_seq;
   unsigned long long seq;
   unsigned long long* nonfinite;
+  unsigned long long* trace;  // optional per-CTA timeline: [b][0..3] = start, entry passed, mid passed, end
 };
+
+__device__ __forceinline__ unsigned long long globaltimer();
+
+__device__ __forceinline__ void trace_mark(const CommArgs& a, int b, int k) {
+  if (a.trace != nullptr && threadIdx.x == 0) a.trace[b * 4 + k] = globaltimer();
+}
 
 // ------------------------------------------------------------------ primitives
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -204,12 +211,14 @@ __device__ __forceinline__ void chunk_slice(size_t cs, size_t ce, int nb, int b,
 
 // ------------------------------------------------------------------ one-shot (K2)
 template <typename T, int P, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(512) k_oneshot(CommArgs a) {
+__global__ void __launch_bounds__(256, 2) k_oneshot(CommArgs a) {
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int b = blockIdx.x;
   bool ok = true;
+  trace_mark(a, b, 0);
   if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
+  trace_mark(a, b, 1);
   unsigned bad = 0;
   if (ok) {
     const size_t n = a.n;
@@ -264,6 +273,7 @@ __global__ void __launch_bounds__(512) k_oneshot(CommArgs a) {
     }
   }
   report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
   if (!VIRTUAL) publish_done(a);
 }
 
@@ -277,7 +287,7 @@ __device__ __forceinline__ T ordered_sum(const T* const (&src)[P], int rank, siz
 }
 
 template <typename T, int P, bool VIRTUAL, int U, int UAG>
-__global__ void __launch_bounds__(512) k_twoshot(CommArgs a) {
+__global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int b = blockIdx.x;
@@ -285,8 +295,10 @@ __global__ void __launch_bounds__(512) k_twoshot(CommArgs a) {
   bool ok = true;
   unsigned bad = 0;
   T* out = reinterpret_cast<T*>(a.xbar[rank]);
+  trace_mark(a, b, 0);
   if (a.phases & 1) {
     if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
+    trace_mark(a, b, 1);
     if (ok) {
       // reduce-scatter: this rank owns chunk `rank` and sums it in ring order
       // x_rank, x_rank+1, ..., x_rank-1 (the order the reference ring produces).
@@ -336,6 +348,7 @@ __global__ void __launch_bounds__(512) k_twoshot(CommArgs a) {
   }
   if (a.phases & 2) {
     if (!VIRTUAL && ok) ok = cta_barrier<P>(a, 1, b, rank);
+    trace_mark(a, b, 2);
     if (ok) {
       // all-gather: pull slice b of every other rank's reduced chunk.
 #pragma unroll 1
@@ -363,12 +376,13 @@ __global__ void __launch_bounds__(512) k_twoshot(CommArgs a) {
     }
   }
   report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
   if (!VIRTUAL) publish_done(a);
 }
 
 // ------------------------------------------------------------------ dispatch
 template <int P>
-constexpr int unroll_for() { return P <= 2 ? 4 : (P <= 4 ? 2 : 1); }
+constexpr int unroll_for() { return P <= 2 ? 8 : (P <= 4 ? 4 : 2); }
 
 template <typename T, bool VIRTUAL>
 int launch_allreduce(int algo, int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
@@ -453,21 +467,21 @@ extern "C" int lasgd_mean_virtual(void* const* outs, int n_out, const void* cons
   dim3 grid(nblocks, n_out);
   if (algo == LASGD_ALGO_ONESHOT) {
     a.phases = 1;
-    return launch_any(dtype, true, algo, P, a, grid, 512, s);
+    return launch_any(dtype, true, algo, P, a, grid, 256, s);
   }
   a.phases = 1;  // reduce-scatter of every virtual rank ...
-  int rc = launch_any(dtype, true, algo, P, a, grid, 512, s);
+  int rc = launch_any(dtype, true, algo, P, a, grid, 256, s);
   if (rc) return rc;
   a.phases = 2;  // ... then the all-gather (stream order replaces the mid barrier)
   a.nonfinite = nullptr;
-  return launch_any(dtype, true, algo, P, a, grid, 512, s);
+  return launch_any(dtype, true, algo, P, a, grid, 256, s);
 }
 
 // ====================================================================== communicator
 struct lasgd_comm {
   int rank = 0, world = 1, device = 0, dtype = LASGD_F32;
   size_t n = 0, elem = 4;
-  int nblocks = 32, threads = 512;
+  int nblocks = 96, threads = 256;
   long long timeout_ns = 30LL * 1000000000LL;
   long long fault_seq = -1;
   int fault_phase = 0;
@@ -481,6 +495,8 @@ struct lasgd_comm {
   unsigned long long* done_host = nullptr;
   unsigned long long* done_dev = nullptr;
   unsigned int* done_ctr = nullptr;
+  unsigned long long* trace_buf = nullptr;  // [kMaxB][4] globaltimer stamps of the last traced launch
+  bool trace_on = false;
   unsigned long long seq = 0;  // launches issued
   cudaEvent_t ev[kEvents];
   int nev = 0;
@@ -515,10 +531,10 @@ extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int 
     delete c;
     return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d outside [1, %d]", nb, kMaxB);
   }
-  if (c->threads < 64 || c->threads > 512 || c->threads % 32) {
+  if (c->threads < 64 || c->threads > 256 || c->threads % 32) {
     int t = c->threads;
     delete c;
-    return fail(LASGD_ERR_INVALID_ARGUMENT, "threads=%d must be a multiple of 32 in [64, 512]", t);
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "threads=%d must be a multiple of 32 in [64, 256]", t);
   }
   DeviceGuard g(device);
   const size_t bytes = n * c->elem;
@@ -539,6 +555,8 @@ extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int 
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->done_ctr, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->done_ctr, 0, kDoneSlots * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->trace_buf, (size_t)kMaxB * 4 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->trace_buf, 0, (size_t)kMaxB * 4 * sizeof(unsigned long long));
   for (int i = 0; e == cudaSuccess && i < kEvents; ++i) {
     e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess) c->nev++;
@@ -596,6 +614,28 @@ extern "C" int lasgd_comm_resolve_algo(lasgd_comm* c, int algo) {
   return resolve_algo(algo, c->world, c->n * c->elem);
 }
 
+extern "C" int lasgd_comm_set_trace(lasgd_comm* c, int on) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  c->trace_on = on != 0;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_read_trace(lasgd_comm* c, unsigned long long* out, int max_ctas) {
+  if (!c || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  const int nb = max_ctas < c->nblocks ? max_ctas : c->nblocks;
+  DeviceGuard g(c->device);
+  LASGD_CUDA_TRY(cudaDeviceSynchronize());
+  LASGD_CUDA_TRY(cudaMemcpy(out, c->trace_buf, (size_t)nb * 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return nb;
+}
+
+extern "C" int lasgd_comm_set_nblocks(lasgd_comm* c, int nblocks) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (nblocks < 1 || nblocks > kMaxB) return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d outside [1, %d]", nblocks, kMaxB);
+  c->nblocks = nblocks;
+  return LASGD_OK;
+}
+
 extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   if (!c->opened && c->world > 1) return fail(LASGD_ERR_STATE, "lasgd_comm_open has not been called");
@@ -639,6 +679,7 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
   a.done_seq = c->done_dev;
   a.seq = s;
   a.nonfinite = nullptr;
+  a.trace = c->trace_on ? c->trace_buf : nullptr;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   int rc = launch_any(c->dtype, false, algo, c->world, a, dim3(c->nblocks, 1), c->threads, cs);
   if (rc) return rc;
@@ -722,6 +763,7 @@ extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
     if (r != c->rank && c->peer_base[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
   for (int i = 0; i < c->nev; ++i) cudaEventDestroy(c->ev[i]);
   if (c->done_ctr) cudaFree(c->done_ctr);
+  if (c->trace_buf) cudaFree(c->trace_buf);
   if (c->status_host) cudaFreeHost(c->status_host);
   if (c->base) cudaFree(c->base);
   delete c;

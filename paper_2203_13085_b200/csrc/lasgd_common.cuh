@@ -71,9 +71,15 @@ __device__ __forceinline__ void report_nonfinite(unsigned long long* ctr, unsign
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// CTAs per SM of the streaming kernels (tunable, lasgd_set_stream_ctas_per_sm).  The
+// default leaves half of every SM's registers/threads free so the all-reduce CTAs on
+// the side stream can co-reside with a local step instead of queueing behind it.
+int stream_ctas_per_sm();
+
 // Grid for a streaming kernel: enough CTAs to fill every SM `per_sm` times, never more
 // than the work needs.
-inline int stream_grid(size_t work_items, int threads, int per_sm = 8) {
+inline int stream_grid(size_t work_items, int threads, int per_sm = 0) {
+  if (per_sm <= 0) per_sm = stream_ctas_per_sm();
   size_t need = (work_items + threads - 1) / threads;
   size_t cap = (size_t)num_sms() * per_sm;
   if (need < 1) need = 1;

@@ -3,7 +3,8 @@
 //
 // All are HBM-bound elementwise passes over the flat parameter buffer: 128-bit
 // evict-first loads/stores, U independent packs in flight per thread,
-// grid = 8 CTAs x 256 threads per SM (full occupancy), scalar tail for n % W,
+// grid = 2 CTAs x 256 threads per SM by default (<= 64 registers per thread: half of
+// each SM stays free for the side-stream all-reduce), scalar tail for n % W,
 // warp-aggregated non-finite counter fused into the pass (the reference checks
 // every blend result, params.py:88).  No tensor cores: there is no reuse.
 //
@@ -20,10 +21,11 @@ namespace lasgd {
 
 // ------------------------------------------------------------- generic driver
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
+// Each Op declares U, the packs in flight per thread, sized so the loaded data stays
+// near 32 registers (<= 64 total under __launch_bounds__(256, 4), no spills).
 
 template <typename T, typename Op, int U>
-__global__ void __launch_bounds__(kThreads) k_stream(Op op, size_t n, unsigned long long* nonfinite) {
+__global__ void __launch_bounds__(kThreads, 4) k_stream(Op op, size_t n, unsigned long long* nonfinite) {
   constexpr int W = Pack<T>::W;
   const size_t npack = n / W;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -48,7 +50,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(Op op, size_t n, unsigned l
 
 // Fallback for buffers that are not 16-byte aligned (e.g. arbitrary views).
 template <typename T, typename Op>
-__global__ void __launch_bounds__(kThreads) k_scalar(Op op, size_t n, unsigned long long* nonfinite) {
+__global__ void __launch_bounds__(kThreads, 4) k_scalar(Op op, size_t n, unsigned long long* nonfinite) {
   unsigned bad = 0;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     bad += op.scalar(i);
@@ -62,7 +64,7 @@ int launch(const Op& op, size_t n, bool aligned, unsigned long long* nonfinite, 
   if (aligned) {
     const size_t npack = n / Pack<T>::W;
     const size_t work = npack > (size_t)kThreads ? npack : (size_t)kThreads;
-    k_stream<T, Op, kUnroll><<<stream_grid(work, kThreads), kThreads, 0, s>>>(op, n, nonfinite);
+    k_stream<T, Op, Op::U><<<stream_grid(work, kThreads), kThreads, 0, s>>>(op, n, nonfinite);
   } else {
     k_scalar<T, Op><<<stream_grid(n, kThreads), kThreads, 0, s>>>(op, n, nonfinite);
   }
@@ -77,6 +79,7 @@ struct BlendOp {
   const T* u;
   const T* v;
   T a, b;
+  static constexpr int U = 4;
   struct Loaded { Pack<T> u, v; };
   __device__ __forceinline__ unsigned elem(T uu, T vv, T& o) const {
     o = add_rn(mul_rn(a, uu), mul_rn(b, vv));
@@ -107,6 +110,7 @@ template <typename T>
 struct CopyOp {
   T* dst;
   const T* src;
+  static constexpr int U = 4;
   struct Loaded { Pack<T> s; };
   __device__ __forceinline__ void load(Loaded& L, size_t j) const { L.s = ld_stream(src + j); }
   __device__ __forceinline__ unsigned compute_store(const Loaded& L, size_t j) const {
@@ -128,6 +132,7 @@ struct SgdOp {
   T* delta;
   T neg_lr, mu, omd, wd;
   bool use_wd, use_mom, nesterov, first, use_delta, reset;
+  static constexpr int U = 2;
   struct Loaded { Pack<T> x, g, m, d; };
 
   __device__ __forceinline__ unsigned elem(T& xv, T gv, T& mv, T& dv) const {
@@ -179,6 +184,7 @@ struct PullOp {
   const T* snap;
   const T* xbar;
   T neg_alpha;
+  static constexpr int U = 2;
   struct Loaded { Pack<T> x, s, z; };
   __device__ __forceinline__ unsigned elem(T& xv, T sv, T zv) const {
     const T diff = add_rn(sv, mul_rn(T(-1), zv));  // blend(1, snap, -1, xbar)
@@ -213,6 +219,7 @@ struct FinalizeOp {
   T* snap_next;
   const T* z;
   const T* delta;
+  static constexpr int U = 2;
   struct Loaded { Pack<T> z, d; };
   __device__ __forceinline__ void load(Loaded& L, size_t j) const {
     L.z = ld_stream(z + j);

@@ -46,9 +46,18 @@ int num_sms() {
   return cache[dev];
 }
 
+static int g_stream_ctas_per_sm = 2;
+int stream_ctas_per_sm() { return g_stream_ctas_per_sm; }
+
 }  // namespace lasgd
 
 using namespace lasgd;
+
+extern "C" int lasgd_set_stream_ctas_per_sm(int v) {
+  if (v < 1 || v > 32) return fail(LASGD_ERR_INVALID_ARGUMENT, "ctas per SM %d outside [1, 32]", v);
+  g_stream_ctas_per_sm = v;
+  return LASGD_OK;
+}
 
 extern "C" int lasgd_abi_version(void) { return LASGD_ABI_VERSION; }
 
