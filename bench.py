@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--alpha", type=float, default=1.0)
     ap.add_argument("--algo", choices=["auto", "oneshot", "twoshot"], default="auto")
     ap.add_argument("--nblocks", type=int, default=128)
+    ap.add_argument("--pipeline", choices=["overlap", "fused"], default="fused",
+                    help="overlap: K5 | K4 | K2/K3 on a side stream; fused: one K7 pass per round boundary")
+    ap.add_argument("--fused-nblocks", type=int, default=0, help="CTAs of the fused kernel (0 = 2 per SM)")
     ap.add_argument("--train-steps", type=int, default=10)
     ap.add_argument("--train-warmup", type=int, default=4)
     ap.add_argument("--no-train", action="store_true")
@@ -68,6 +71,7 @@ def config_dict(args, world):
         "alpha": args.alpha,
         "local_step": "sgd momentum=0.9 nesterov weight_decay=1e-4 lr=0.1",
         "allreduce": args.algo,
+        "pipeline": args.pipeline,
         "sm_budget_ctas": args.nblocks,
         "parallelism": f"dp{world}",
         "l2": "no flush: every kernel streams 3-5 buffers of 102 MB (> 126 MB L2); gradients alternate between 2 buffers",
@@ -134,8 +138,15 @@ def ncu_traffic():
 
 
 def kernel_bytes(name, n, world, comm, algo_code, sgd_momentum=True):
-    """Algorithmic bytes per launch.  B = 4n."""
+    """Algorithmic bytes per launch.  B = 4n.  Returns (bytes, bound)
+    where bound is the resource whose roofline time is longest."""
     B = 4 * n
+    if name == "fused_round":
+        hbm = (7 if world > 1 else 6) * B  # read x,g,m(,own snap); write x,m,next snap
+        nvl = (world - 1) * B  # every peer's snapshot over NVLink
+        if nvl / NVLINK_PEAK_GBS > hbm / peaks()[0]:
+            return nvl, "nvlink"
+        return hbm, "hbm"
     if name == "sgd_step":
         return 5 * B if sgd_momentum else 3 * B, "hbm"
     if name == "pull":
@@ -304,7 +315,7 @@ def main():
     def make_worker(timed, sync=True, g=None):
         return L.LASGDWorker(x, g if g is not None else grads[0], comm=comm, sync_period=args.sync_period,
                              alpha=args.alpha, mode="pull", sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
-                             timed=timed, sync=sync)
+                             timed=timed, sync=sync, pipeline=args.pipeline, fused_nblocks=args.fused_nblocks)
 
     def run_sync_path(worker, steps, gsrc):
         for t in range(steps):
@@ -423,6 +434,20 @@ def main():
                 return seq
 
             iso["allreduce"] = timeit(ar, reps=10)
+        fk = dict(m=m, momentum=0.9, weight_decay=1e-4, nesterov=True, alpha=args.alpha,
+                  nblocks=args.fused_nblocks, stream=compute)
+        if comm is not None:
+            barrier()
+            slot = [0]
+
+            def fused():
+                comm.fused_round(slot[0], x, grads[0], lr, **fk)
+                slot[0] ^= 1
+
+            iso["fused_round"] = timeit(fused, reps=10)
+        else:
+            iso["fused_round"] = timeit(lambda: K.fused_round_virtual(
+                [x], [grads[0]], [s0], [s1], lr, ms=[m], **{k: v for k, v in fk.items() if k != "m"}))
     barrier()
 
     # ---------------- real training: ResNet-50 fwd/bwd + LASGD vs no-sync ceiling
@@ -518,7 +543,8 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     def train(sync, steps, warm):
         with torch.cuda.stream(compute):
             w = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=args.sync_period, alpha=args.alpha, mode="pull",
-                              sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute, sync=sync)
+                              sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute, sync=sync,
+                              pipeline=args.pipeline, fused_nblocks=args.fused_nblocks)
 
             def one():
                 flat.zero_grad()

@@ -53,7 +53,7 @@ extern "C" {
 #define LASGD_ALGO_TWOSHOT 2
 
 #define LASGD_MAX_RANKS 8
-#define LASGD_MAX_BLOCKS 256
+#define LASGD_MAX_BLOCKS 512
 #define LASGD_IPC_HANDLE_BYTES 64
 
 int lasgd_abi_version(void);
@@ -146,6 +146,26 @@ int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr);
  * 154-203).  Every rank must issue the same sequence of calls.  *seq receives
  * this launch's sequence number for query/wait. */
 int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, unsigned long long* seq);
+
+/* K7: the fused round boundary of the deterministic schedule, one pass per element:
+ *   K5 local step on (x, g, m[, delta]);  xbar = ring-order mean of every rank's
+ *   snapshot slot `snap_slot`, read from the peers over NVLink;
+ *   mode 0 (pull):     x = x + (-alpha)*(snap_own + (-1)*xbar)
+ *   mode 1 (finalize): x = xbar + delta            (optimizer.py:171; delta then resets)
+ *   snapshot slot 1-snap_slot = x.
+ * Bit-identical to lasgd_sgd_step -> lasgd_comm_allreduce -> lasgd_elastic_pull /
+ * lasgd_finalize under the same schedule; launched on `stream` with `nblocks` CTAs
+ * (<= 0: the communicator's budget); a launch like lasgd_comm_allreduce (same
+ * sequence numbers, query / wait / stream_wait apply). */
+int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, void* x, const void* g, void* m, void* delta,
+                           const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+                           unsigned long long* nonfinite, void* stream, unsigned long long* seq);
+/* K7 over P virtual ranks on ONE device (host arrays of P device pointers each;
+ * m / delta arrays may be NULL).  Test path for the fused arithmetic. */
+int lasgd_fused_round_virtual(int P, void* const* x, const void* const* g, void* const* m, void* const* delta,
+                              const void* const* snaps, void* const* snap_next, size_t n, int dtype,
+                              const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+                              unsigned long long* nonfinite, void* stream);
 /* Non-blocking completion poll of launch `seq` (collective.py:142-144 `poll`):
  * 1 complete, 0 in flight, LASGD_ERR_COLLECTIVE failed (diagnostic via
  * lasgd_comm_diagnostic).  Reads a host-mapped flag: no CUDA call. */

@@ -33,7 +33,7 @@
 namespace lasgd {
 
 constexpr int kMaxR = LASGD_MAX_RANKS;
-constexpr int kMaxB = LASGD_MAX_BLOCKS;
+constexpr int kMaxB = LASGD_MAX_BLOCKS;  // flag slots per phase and rank
 constexpr int kPhases = 2;
 constexpr size_t kPadBytes = (size_t)kPhases * kMaxB * kMaxR * sizeof(uint32_t);
 constexpr int kDoneSlots = 64;
@@ -380,6 +380,190 @@ __global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
   if (!VIRTUAL) publish_done(a);
 }
 
+// ------------------------------------------------------------------ fused round (K7)
+// One pass at a round boundary of the deterministic schedule: the local step (K5) of
+// this minibatch, the mean of the round's snapshots read straight from every peer over
+// NVLink (K2 order), the pull / finalize (K4) and the next snapshot (K1), per element:
+//   x' = K5(x, g, m)                          (sgd_elem)
+//   xbar = (sum_k snap_{(c+k)%P}) / P         (rot_sum / mean_div, ring order)
+//   pull:     x'' = x' + (-alpha)*(snap_own + (-1)*xbar)       (pull_elem)
+//   finalize: x'' = xbar + delta'             (optimizer.py:171; delta' = delta + s)
+//   snap_next = x''
+// Same element functions as the separate kernels, so the result is bit-identical to
+// K5 -> (K2 completes) -> K4 under the deterministic schedule; HBM and NVLink stream
+// concurrently instead of back to back, and xbar never touches HBM.
+template <typename T>
+struct FusedRound {
+  T* x[kMaxR];
+  const T* g[kMaxR];
+  T* m[kMaxR];
+  T* delta[kMaxR];
+  T* snap_next[kMaxR];
+  SgdCoef<T> c;
+  T neg_alpha;
+  int mode;  // 0 pull, 1 reference finalize (delta)
+};
+
+template <typename T, int P, bool VIRTUAL, int U>
+__global__ void __launch_bounds__(256, 2) k_fused_round(CommArgs a, FusedRound<T> f) {
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
+  const int b = blockIdx.x;
+  bool ok = true;
+  trace_mark(a, b, 0);
+  if (!VIRTUAL && P > 1) ok = cta_barrier<P>(a, 0, b, rank);
+  trace_mark(a, b, 1);
+  unsigned bad = 0;
+  if (ok) {
+    const size_t n = a.n;
+    size_t bnd[P + 1];
+#pragma unroll
+    for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
+    const T* src[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
+    T* const x = f.x[vr];
+    const T* const g = f.g[vr];
+    T* const m = f.m[vr];
+    T* const dl = f.delta[vr];
+    T* const sn = f.snap_next[vr];
+    const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
+    const bool store_d = f.c.use_delta && (P == 1 || f.mode == 0);  // finalize resets delta
+    auto element = [&](T& xv, T gv, T& mv, T& dv, const T (&lane)[P], int cidx) -> T {
+      unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+      if constexpr (P > 1) {
+        const T zb = mean_div<T, P>(rot_sum<T, P>(lane, cidx));
+        if (f.mode == 0) {
+          T own = lane[0];
+#pragma unroll
+          for (int q = 1; q < P; ++q) own = (q == rank) ? lane[q] : own;  // no dynamic register indexing
+          bb += pull_elem(f.neg_alpha, xv, own, zb);
+        } else {
+          xv = add_rn(zb, dv);
+          bb += !finite(xv);
+        }
+      }
+      bad += bb;
+      return xv;
+    };
+    size_t p0, p1;
+    split(n / W, a.nblocks, b, p0, p1);
+    for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+      Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U][P];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t pu = p + (size_t)u * blockDim.x;
+        if (pu < p1) {
+          const size_t j = pu * W;
+          vx[u] = ld_stream(x + j);
+          vg[u] = ld_stream(g + j);
+          if (load_m) vm[u] = ld_stream(m + j);
+          if (load_d) vd[u] = ld_stream(dl + j);
+          if constexpr (P > 1) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) vs[u][q] = ld_cg(src[q] + j);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t pu = p + (size_t)u * blockDim.x;
+        if (pu < p1) {
+          const size_t j0 = pu * W;
+          const int c0 = chunk_of<P>(j0, bnd), c1 = chunk_of<P>(j0 + W - 1, bnd);
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            T lane[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) lane[q] = (P > 1) ? vs[u][q].v[k] : T(0);
+            const int cidx = (c0 == c1) ? c0 : chunk_of<P>(j0 + k, bnd);
+            element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], lane, cidx);
+          }
+          st_stream(x + j0, vx[u]);
+          if (f.c.use_mom) st_stream(m + j0, vm[u]);
+          if (store_d) st_stream(dl + j0, vd[u]);
+          st_stream(sn + j0, vx[u]);
+        }
+      }
+    }
+    if (b == a.nblocks - 1) {  // scalar tail n % W
+      for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
+        T lane[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) lane[q] = (P > 1) ? src[q][j] : T(0);
+        T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+        element(xv, g[j], mv, dv, lane, chunk_of<P>(j, bnd));
+        x[j] = xv;
+        if (f.c.use_mom) m[j] = mv;
+        if (store_d) dl[j] = dv;
+        sn[j] = xv;
+      }
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
+  if (!VIRTUAL) publish_done(a);
+}
+
+template <typename T, bool VIRTUAL>
+int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s) {
+#define LASGD_FCASE(PP)                                                                             \
+  case PP:                                                                                          \
+    k_fused_round<T, PP, VIRTUAL, (PP <= 2 ? 2 : 1)><<<grid, threads, 0, s>>>(a, f);               \
+    break;
+  switch (P) {
+    LASGD_FCASE(1)
+    LASGD_FCASE(2)
+    LASGD_FCASE(3)
+    LASGD_FCASE(4)
+    LASGD_FCASE(5)
+    LASGD_FCASE(6)
+    LASGD_FCASE(7)
+    LASGD_FCASE(8)
+    default: return fail(LASGD_ERR_UNSUPPORTED, "world size %d > %d", P, kMaxR);
+  }
+#undef LASGD_FCASE
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
+
+template <typename T>
+FusedRound<T> make_fused(int nr, void* const* x, const void* const* g, void* const* m, void* const* delta,
+                         void* const* snap_next, const lasgd_sgd_params* sgd, double alpha, int mode) {
+  FusedRound<T> f;
+  memset(&f, 0, sizeof(f));
+  for (int r = 0; r < nr; ++r) {
+    f.x[r] = (T*)x[r];
+    f.g[r] = (const T*)g[r];
+    f.m[r] = m ? (T*)m[r] : nullptr;
+    f.delta[r] = delta ? (T*)delta[r] : nullptr;
+    f.snap_next[r] = (T*)snap_next[r];
+  }
+  f.c = make_sgd_coef<T>(sgd, delta != nullptr && delta[0] != nullptr);
+  f.neg_alpha = (T)(-alpha);
+  f.mode = mode;
+  return f;
+}
+
+int check_fused_args(int nr, void* const* x, const void* const* g, void* const* m, void* const* delta,
+                     void* const* snap_next, const lasgd_sgd_params* sgd, double alpha, int mode) {
+  if (!sgd) return fail(LASGD_ERR_INVALID_ARGUMENT, "null sgd params");
+  if (mode != 0 && mode != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "mode %d (0 pull, 1 finalize)", mode);
+  if (mode == 0 && !(alpha > 0.0 && alpha <= 1.0)) return fail(LASGD_ERR_INVALID_ARGUMENT, "alpha must be in (0, 1], got %g", alpha);
+  if (mode == 1 && (!delta || !delta[0])) return fail(LASGD_ERR_INVALID_ARGUMENT, "finalize mode needs the delta buffer");
+  if (sgd->momentum != 0.0 && !m) return fail(LASGD_ERR_INVALID_ARGUMENT, "momentum needs m");
+  if (sgd->nesterov && (sgd->momentum <= 0.0 || sgd->dampening != 0.0))
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "Nesterov momentum requires a momentum and zero dampening");
+  for (int r = 0; r < nr; ++r) {
+    if (!x[r] || !g[r] || !snap_next[r] || !aligned16(x[r]) || !aligned16(g[r]) || !aligned16(snap_next[r]) ||
+        (m && m[r] && !aligned16(m[r])) || (delta && delta[r] && !aligned16(delta[r])))
+      return fail(LASGD_ERR_INVALID_ARGUMENT, "fused round buffers must be non-null and 16-B aligned");
+    if (sgd->momentum != 0.0 && !m[r]) return fail(LASGD_ERR_INVALID_ARGUMENT, "momentum needs m");
+  }
+  return LASGD_OK;
+}
+
 // ------------------------------------------------------------------ dispatch
 template <int P>
 constexpr int unroll_for() { return P <= 2 ? 8 : (P <= 4 ? 4 : 2); }
@@ -475,6 +659,33 @@ extern "C" int lasgd_mean_virtual(void* const* outs, int n_out, const void* cons
   a.phases = 2;  // ... then the all-gather (stream order replaces the mid barrier)
   a.nonfinite = nullptr;
   return launch_any(dtype, true, algo, P, a, grid, 256, s);
+}
+
+extern "C" int lasgd_fused_round_virtual(int P, void* const* x, const void* const* g, void* const* m,
+                                         void* const* delta, const void* const* snaps, void* const* snap_next,
+                                         size_t n, int dtype, const lasgd_sgd_params* sgd, double alpha, int mode,
+                                         int nblocks, unsigned long long* nonfinite, void* stream) {
+  if (P < 1 || P > kMaxR) return fail(LASGD_ERR_UNSUPPORTED, "P=%d outside [1, %d]", P, kMaxR);
+  if (!x || !g || !snaps || !snap_next) return fail(LASGD_ERR_INVALID_ARGUMENT, "null pointer array");
+  if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+  int rc = check_fused_args(P, x, g, m, delta, snap_next, sgd, alpha, mode);
+  if (rc) return rc;
+  if (n == 0) return LASGD_OK;
+  if (nblocks <= 0) nblocks = 2 * num_sms();
+  CommArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < P; ++q) {
+    if (!snaps[q] || !aligned16(snaps[q])) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot %d null or unaligned", q);
+    a.snap[q] = reinterpret_cast<const char*>(snaps[q]);
+  }
+  a.n = n;
+  a.nblocks = nblocks;
+  a.skip_signal_phase = -1;
+  a.nonfinite = nonfinite;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == LASGD_F32)
+    return launch_fused<float, true>(P, a, make_fused<float>(P, x, g, m, delta, snap_next, sgd, alpha, mode), dim3(nblocks, P), 256, s);
+  return launch_fused<double, true>(P, a, make_fused<double>(P, x, g, m, delta, snap_next, sgd, alpha, mode), dim3(nblocks, P), 256, s);
 }
 
 // ====================================================================== communicator
@@ -636,7 +847,10 @@ extern "C" int lasgd_comm_set_nblocks(lasgd_comm* c, int nblocks) {
   return LASGD_OK;
 }
 
-extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, unsigned long long* seq) {
+// Common launch preparation: validates the communicator state, assigns the next
+// sequence number (the epoch of every flag written by this launch) and fills the
+// pointer tables for snapshot slot `snap_slot`.
+static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned long long& s) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   if (!c->opened && c->world > 1) return fail(LASGD_ERR_STATE, "lasgd_comm_open has not been called");
   if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
@@ -644,11 +858,7 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
     c->poisoned = true;
     return fail(LASGD_ERR_COLLECTIVE, "communicator failed earlier; re-create it");
   }
-  algo = resolve_algo(algo, c->world, c->n * c->elem);
-  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
-  DeviceGuard g(c->device);
-  const unsigned long long s = ++c->seq;
-  CommArgs a;
+  s = ++c->seq;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < c->world; ++r) {
     a.snap[r] = c->peer_base[r] + c->off_snap[snap_slot];
@@ -680,8 +890,53 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
   a.seq = s;
   a.nonfinite = nullptr;
   a.trace = c->trace_on ? c->trace_buf : nullptr;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, unsigned long long* seq) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  algo = resolve_algo(algo, c->world, c->n * c->elem);
+  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
+  DeviceGuard g(c->device);
+  CommArgs a;
+  unsigned long long s = 0;
+  int rc = prepare_launch(c, snap_slot, a, s);
+  if (rc) return rc;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-  int rc = launch_any(c->dtype, false, algo, c->world, a, dim3(c->nblocks, 1), c->threads, cs);
+  rc = launch_any(c->dtype, false, algo, c->world, a, dim3(c->nblocks, 1), c->threads, cs);
+  if (rc) return rc;
+  LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+  if (seq) *seq = s;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, void* x, const void* g, void* m, void* delta,
+                                      const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+                                      unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  void* xs[1] = {x};
+  const void* gs[1] = {g};
+  void* ms[1] = {m};
+  void* ds[1] = {delta};
+  void* ns[1] = {nullptr};
+  if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
+  ns[0] = c->base + c->off_snap[1 - snap_slot];
+  int rc = check_fused_args(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode);
+  if (rc) return rc;
+  if (nblocks <= 0) nblocks = c->nblocks;
+  if (nblocks > kMaxB) return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d > %d", nblocks, kMaxB);
+  DeviceGuard dg(c->device);
+  CommArgs a;
+  unsigned long long s = 0;
+  rc = prepare_launch(c, snap_slot, a, s);
+  if (rc) return rc;
+  a.nblocks = nblocks;
+  a.nonfinite = nonfinite;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (c->dtype == LASGD_F32)
+    rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs);
+  else
+    rc = launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs);
   if (rc) return rc;
   LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
   if (seq) *seq = s;

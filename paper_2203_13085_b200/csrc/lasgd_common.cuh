@@ -71,6 +71,63 @@ __device__ __forceinline__ void report_nonfinite(unsigned long long* ctr, unsign
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// ---------------------------------------------------------------- element math
+// Shared by the standalone kernels and the fused round kernel, so both produce the
+// same bits by construction.
+
+// K5 coefficients, already rounded to T on the host side of the launch.
+template <typename T>
+struct SgdCoef {
+  T neg_lr, mu, omd, wd;
+  bool use_wd, use_mom, nesterov, first, use_delta, reset;
+};
+
+template <typename T>
+SgdCoef<T> make_sgd_coef(const lasgd_sgd_params* p, bool use_delta) {
+  SgdCoef<T> c;
+  c.neg_lr = (T)(-p->lr);
+  c.mu = (T)p->momentum;
+  c.omd = (T)(1.0 - p->dampening);
+  c.wd = (T)p->weight_decay;
+  c.use_wd = p->weight_decay != 0.0;
+  c.use_mom = p->momentum != 0.0;
+  c.nesterov = p->nesterov != 0;
+  c.first = p->first_step != 0;
+  c.use_delta = use_delta;
+  c.reset = p->delta_reset != 0;
+  return c;
+}
+
+// One local step on one element (optimizer.py:145-146 at momentum = wd = 0):
+//   d = g (+ wd*x); m = first ? d : mu*m + (1-damp)*d; d = nesterov ? d + mu*m : m;
+//   s = (-lr)*d; x = x + s; delta = (reset ? 0 : delta) + s.   Returns #non-finite.
+template <typename T>
+__device__ __forceinline__ unsigned sgd_elem(const SgdCoef<T>& c, T& xv, T gv, T& mv, T& dv) {
+  T dir = gv;
+  if (c.use_wd) dir = add_rn(dir, mul_rn(c.wd, xv));
+  if (c.use_mom) {
+    mv = c.first ? dir : add_rn(mul_rn(c.mu, mv), mul_rn(c.omd, dir));
+    dir = c.nesterov ? add_rn(dir, mul_rn(c.mu, mv)) : mv;
+  }
+  const T s = mul_rn(c.neg_lr, dir);
+  xv = add_rn(xv, s);
+  unsigned bad = !finite(xv);
+  if (c.use_delta) {
+    dv = add_rn(c.reset ? T(0) : dv, s);
+    bad += !finite(dv);
+  }
+  return bad;
+}
+
+// Elastic pull on one element: diff = 1*snap + (-1)*xbar; x = 1*x + (-alpha)*diff
+// (blend order of optimizer.py:256-257).  Returns #non-finite.
+template <typename T>
+__device__ __forceinline__ unsigned pull_elem(T neg_alpha, T& xv, T sv, T zv) {
+  const T diff = add_rn(sv, mul_rn(T(-1), zv));
+  xv = add_rn(xv, mul_rn(neg_alpha, diff));
+  return !finite(diff) + !finite(xv);
+}
+
 // CTAs per SM of the streaming kernels (tunable, lasgd_set_stream_ctas_per_sm).  The
 // default leaves half of every SM's registers/threads free so the all-reduce CTAs on
 // the side stream can co-reside with a local step instead of queueing behind it.

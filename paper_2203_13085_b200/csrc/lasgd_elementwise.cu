@@ -130,48 +130,31 @@ struct SgdOp {
   const T* g;
   T* m;
   T* delta;
-  T neg_lr, mu, omd, wd;
-  bool use_wd, use_mom, nesterov, first, use_delta, reset;
+  SgdCoef<T> c;
   static constexpr int U = 2;
   struct Loaded { Pack<T> x, g, m, d; };
 
-  __device__ __forceinline__ unsigned elem(T& xv, T gv, T& mv, T& dv) const {
-    T dir = gv;
-    if (use_wd) dir = add_rn(dir, mul_rn(wd, xv));
-    if (use_mom) {
-      mv = first ? dir : add_rn(mul_rn(mu, mv), mul_rn(omd, dir));
-      dir = nesterov ? add_rn(dir, mul_rn(mu, mv)) : mv;
-    }
-    const T s = mul_rn(neg_lr, dir);
-    xv = add_rn(xv, s);
-    unsigned bad = !finite(xv);
-    if (use_delta) {
-      dv = add_rn(reset ? T(0) : dv, s);
-      bad += !finite(dv);
-    }
-    return bad;
-  }
   __device__ __forceinline__ void load(Loaded& L, size_t j) const {
     L.x = ld_stream(x + j);
     L.g = ld_stream(g + j);
-    if (use_mom && !first) L.m = ld_stream(m + j);
-    if (use_delta && !reset) L.d = ld_stream(delta + j);
+    if (c.use_mom && !c.first) L.m = ld_stream(m + j);
+    if (c.use_delta && !c.reset) L.d = ld_stream(delta + j);
   }
   __device__ __forceinline__ unsigned compute_store(Loaded& L, size_t j) const {
     unsigned bad = 0;
 #pragma unroll
-    for (int k = 0; k < Pack<T>::W; ++k) bad += elem(L.x.v[k], L.g.v[k], L.m.v[k], L.d.v[k]);
+    for (int k = 0; k < Pack<T>::W; ++k) bad += sgd_elem(c, L.x.v[k], L.g.v[k], L.m.v[k], L.d.v[k]);
     st_stream(x + j, L.x);
-    if (use_mom) st_stream(m + j, L.m);
-    if (use_delta) st_stream(delta + j, L.d);
+    if (c.use_mom) st_stream(m + j, L.m);
+    if (c.use_delta) st_stream(delta + j, L.d);
     return bad;
   }
   __device__ __forceinline__ unsigned scalar(size_t j) const {
-    T xv = x[j], mv = (use_mom && !first) ? m[j] : T(0), dv = (use_delta && !reset) ? delta[j] : T(0);
-    unsigned bad = elem(xv, g[j], mv, dv);
+    T xv = x[j], mv = (c.use_mom && !c.first) ? m[j] : T(0), dv = (c.use_delta && !c.reset) ? delta[j] : T(0);
+    unsigned bad = sgd_elem(c, xv, g[j], mv, dv);
     x[j] = xv;
-    if (use_mom) m[j] = mv;
-    if (use_delta) delta[j] = dv;
+    if (c.use_mom) m[j] = mv;
+    if (c.use_delta) delta[j] = dv;
     return bad;
   }
 };
@@ -186,11 +169,7 @@ struct PullOp {
   T neg_alpha;
   static constexpr int U = 2;
   struct Loaded { Pack<T> x, s, z; };
-  __device__ __forceinline__ unsigned elem(T& xv, T sv, T zv) const {
-    const T diff = add_rn(sv, mul_rn(T(-1), zv));  // blend(1, snap, -1, xbar)
-    xv = add_rn(xv, mul_rn(neg_alpha, diff));      // blend(1, x, -alpha, diff)
-    return !finite(diff) + !finite(xv);
-  }
+  __device__ __forceinline__ unsigned elem(T& xv, T sv, T zv) const { return pull_elem(neg_alpha, xv, sv, zv); }
   __device__ __forceinline__ void load(Loaded& L, size_t j) const {
     L.x = ld_stream(x + j);
     L.s = ld_stream(snap + j);
@@ -267,17 +246,8 @@ int sgd_t(void* x, const void* g, void* m, void* delta, size_t n, const lasgd_sg
   op.g = (const T*)g;
   op.m = (T*)m;
   op.delta = (T*)delta;
-  op.neg_lr = (T)(-p->lr);
-  op.mu = (T)p->momentum;
-  op.omd = (T)(1.0 - p->dampening);
-  op.wd = (T)p->weight_decay;
-  op.use_wd = p->weight_decay != 0.0;
-  op.use_mom = p->momentum != 0.0;
-  op.nesterov = p->nesterov != 0;
-  op.first = p->first_step != 0;
-  op.use_delta = delta != nullptr;
-  op.reset = p->delta_reset != 0;
-  bool al = aligned16(x) && aligned16(g) && (!op.use_mom || aligned16(m)) && (!op.use_delta || aligned16(delta));
+  op.c = make_sgd_coef<T>(p, delta != nullptr);
+  bool al = aligned16(x) && aligned16(g) && (!op.c.use_mom || aligned16(m)) && (!op.c.use_delta || aligned16(delta));
   return launch<T>(op, n, al, nf, s);
 }
 

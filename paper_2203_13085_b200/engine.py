@@ -16,6 +16,13 @@ Round boundaries are either deterministic (exactly ``sync_period`` local steps
 per round — the parity schedule) or adaptive (finalize as soon as the
 host-mapped completion flag says the mean landed, or block the compute stream
 when ``tau_max`` steps have been taken — the paper's dynamic rate, Table 3).
+
+``pipeline="fused"`` (deterministic only) replaces the boundary step's
+K5 -> (mean lands) -> K4 -> K2/K3 chain by ONE kernel (K7) that applies the local
+step, reads every peer's snapshot over NVLink, forms the ring-order mean, pulls and
+writes the next snapshot in the same pass — bit-identical results, HBM and NVLink
+streamed concurrently.  ``pipeline="overlap"`` (default) keeps the mean on the side
+stream so it overlaps the next minibatches' forward/backward.
 """
 
 from __future__ import annotations
@@ -36,7 +43,8 @@ class LASGDWorker:
                  mode: str = "pull", sgd: Optional[SgdConfig] = None, schedule: Optional[LrSchedule] = None,
                  lr: Optional[float] = None, adaptive: bool = False, tau_max: Optional[int] = None,
                  algo: int = N.ALGO_AUTO, compute_stream: Optional[torch.cuda.Stream] = None, sync: bool = True,
-                 timed: bool = False, check_finite: str = "lazy", max_host_lead: int = 2):
+                 timed: bool = False, check_finite: str = "lazy", max_host_lead: int = 2,
+                 pipeline: str = "overlap", fused_nblocks: int = 0):
         if (schedule is None) == (lr is None):
             raise ValueError("give exactly one of schedule / lr")
         if sync_period < 1:
@@ -45,6 +53,12 @@ class LASGDWorker:
             raise ValueError("alpha must be in (0, 1]")
         if mode not in ("pull", "delta"):
             raise ValueError("mode must be 'pull' or 'delta'")
+        if pipeline not in ("overlap", "fused"):
+            raise ValueError("pipeline must be 'overlap' or 'fused'")
+        if pipeline == "fused" and adaptive:
+            raise ValueError("the fused pipeline implements the deterministic schedule only")
+        self.pipeline = pipeline
+        self.fused_nblocks = fused_nblocks
         self.comm = comm
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
@@ -71,7 +85,7 @@ class LASGDWorker:
         self._max_lead = max_host_lead
         with torch.cuda.stream(self.compute):
             self._launch("snapshot", self.compute, lambda: K.snapshot(self.state.snapshots[0], x))
-            if self.sync and self.world > 1:
+            if self.sync and self.world > 1 and pipeline == "overlap":
                 self._submit(0)
 
     # ------------------------------------------------------------------ helpers
@@ -102,6 +116,9 @@ class LASGDWorker:
         st = self.state
         c = st.sgd
         lr = self.current_lr()
+        if self.pipeline == "fused" and self.sync and st.tau_i + 1 == self.k:
+            self._fused_round(lr)
+            return True
         self._launch("sgd_step", self.compute, lambda: K.sgd_step(
             st.x_local, self.g, lr, m=st.momentum_buf, delta=st.delta, momentum=c.momentum, dampening=c.dampening,
             weight_decay=c.weight_decay, nesterov=c.nesterov, first_step=not st._momentum_started,
@@ -123,6 +140,38 @@ class LASGDWorker:
             self._round()
             return True
         return False
+
+    def _fused_round(self, lr: float) -> None:
+        st = self.state
+        c = st.sgd
+        cur, nxt = st.snap_idx, 1 - st.snap_idx
+        mode = 1 if (self.mode == "delta" and self.alpha == 1.0) else 0
+        kw = dict(momentum=c.momentum, dampening=c.dampening, weight_decay=c.weight_decay, nesterov=c.nesterov,
+                  first_step=not st._momentum_started, delta_reset=st._delta_fresh, alpha=self.alpha, mode=mode,
+                  nonfinite=st.nonfinite_counter)
+        self.tau_hist[st.tau_i + 1] += 1
+        if self.world == 1:
+            # P == 1 (optimizer.py:168-169): local step + snapshot in one pass, no mean
+            self._launch("fused_round", self.compute, lambda: K.fused_round_virtual(
+                [st.x_local], [self.g], [st.snapshots[cur]], [st.snapshots[nxt]], lr,
+                ms=None if st.momentum_buf is None else [st.momentum_buf],
+                deltas=None if st.delta is None else [st.delta], nblocks=self.fused_nblocks, stream=self.compute,
+                **kw))
+        else:
+            box = {}
+            self._launch("fused_round", self.compute, lambda: box.setdefault("s", self.comm.fused_round(
+                cur, st.x_local, self.g, lr, m=st.momentum_buf, delta=st.delta, nblocks=self.fused_nblocks,
+                stream=self.compute, **kw)))
+            self.seq = box["s"]
+        st._momentum_started = st.momentum_buf is not None
+        st._delta_fresh = st.delta is not None
+        st.snap_idx = nxt
+        st.tau_i = 0
+        st.local_clock += 1
+        st.global_clock += 1
+        if st.check_mode == "lazy":
+            with torch.cuda.stream(self.compute):
+                st._finite.poll(st.x_local.numel())
 
     def _throttle(self) -> None:
         ev = torch.cuda.Event()
@@ -162,7 +211,7 @@ class LASGDWorker:
 
     def drain(self) -> None:
         """Order the compute stream after the in-flight all-reduce."""
-        if self.world > 1 and self.seq:
+        if self.world > 1 and self.seq and self.pipeline == "overlap":
             self.comm.stream_wait(self.seq, self.compute)
 
     # ------------------------------------------------------------------ measurement

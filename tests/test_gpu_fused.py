@@ -1,0 +1,116 @@
+"""K7 fused round (local step + ring-order mean + pull/finalize + next snapshot in one
+pass) — bit-exact against the oracle's composition of the separate operations, which
+is what the overlapped schedule computes."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2203_13085_b200 as L
+from oracle import lasgd_oracle as O
+from paper_2203_13085_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def same_bits(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    iv = {4: np.uint32, 8: np.uint64}[a.dtype.itemsize]
+    return a.shape == b.shape and np.array_equal(a.view(iv), b.view(iv))
+
+
+CFGS = [O.SgdConfig(0.1, 0.9, 0.0, 1e-4, True), O.SgdConfig(0.05, 0.0, 0.0, 0.0, False),
+        O.SgdConfig(0.07, 0.8, 0.1, 5e-4, False)]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("n", [1, 7, 4099, 1_000_003])
+@pytest.mark.parametrize("ci", [0, 1, 2])
+@pytest.mark.parametrize("first", [True, False])
+def test_fused_pull_bit_exact(P, n, ci, first):
+    cfg = CFGS[ci]
+    rng = np.random.default_rng(P * 100 + n % 97 + ci)
+    xs = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
+    gs = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
+    ms = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
+    snaps = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
+    alpha = 0.5 if ci == 1 else 1.0
+    xt, gt, st = [dev(v) for v in xs], [dev(v) for v in gs], [dev(v) for v in snaps]
+    mt = [dev(v) for v in ms] if cfg.momentum else None
+    nt = [torch.full_like(x, float("nan")) for x in xt]
+    K.fused_round_virtual(xt, gt, st, nt, cfg.lr, ms=mt, momentum=cfg.momentum, dampening=cfg.dampening,
+                          weight_decay=cfg.weight_decay, nesterov=cfg.nesterov, first_step=first, alpha=alpha)
+    torch.cuda.synchronize()
+    zbar = O.ring_mean(snaps) if P > 1 else None
+    for r in range(P):
+        x1, m1, _ = O.sgd_step_momentum(xs[r], gs[r], ms[r], cfg, first_step=first)
+        ref = O.elastic_pull(x1, snaps[r], zbar, alpha) if P > 1 else x1
+        assert same_bits(xt[r].cpu().numpy(), ref), (P, n, r)
+        assert same_bits(nt[r].cpu().numpy(), ref), (P, n, r)
+        if cfg.momentum:
+            assert same_bits(mt[r].cpu().numpy(), m1)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_fused_finalize_matches_reference_bookkeeping(P):
+    n = 10_007
+    rng = np.random.default_rng(P)
+    xs = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
+    gs = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
+    ds = [rng.standard_normal(n).astype(np.float32) * 1e-2 for _ in range(P)]
+    snaps = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
+    xt, gt, st, dt_ = [dev(v) for v in xs], [dev(v) for v in gs], [dev(v) for v in snaps], [dev(v) for v in ds]
+    nt = [torch.empty_like(x) for x in xt]
+    K.fused_round_virtual(xt, gt, st, nt, 0.03, deltas=dt_, mode=1)
+    torch.cuda.synchronize()
+    z = O.ring_mean(snaps)
+    for r in range(P):
+        _, d1 = O.sgd_step_delta(xs[r], ds[r], gs[r], 0.03)
+        ref = O.finalize_delta(z, d1, None, P)
+        assert same_bits(xt[r].cpu().numpy(), ref)
+        assert same_bits(nt[r].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("mode", ["pull", "delta"])
+@pytest.mark.parametrize("k", [1, 3])
+def test_worker_fused_equals_overlap_single_gpu(mode, k):
+    n, steps = 100_003, 7
+    rng = np.random.default_rng(5)
+    x0 = rng.standard_normal(n).astype(np.float32)
+    grads = [dev(rng.standard_normal(n).astype(np.float32)) for _ in range(steps)]
+    sgd = L.SgdConfig(0.9, 0.0, 1e-4, True) if mode == "pull" else None
+    out = {}
+    for pipe in ("overlap", "fused"):
+        x = dev(x0.copy())
+        w = L.LASGDWorker(x, grads[0], sync_period=k, lr=0.05, mode=mode, sgd=sgd, pipeline=pipe)
+        for t in range(steps):
+            w.g = grads[t]
+            w.step()
+        torch.cuda.synchronize()
+        out[pipe] = (x.cpu().numpy(), w.state.x_snapshot.cpu().numpy())
+    assert same_bits(out["overlap"][0], out["fused"][0])
+    assert same_bits(out["overlap"][1], out["fused"][1])
+    # and both equal plain sequential SGD (P = 1)
+    ref = x0.copy()
+    m = np.zeros_like(ref)
+    for t in range(steps):
+        g = grads[t].cpu().numpy()
+        if sgd is None:
+            ref = O.sgd_step_plain(ref, g, 0.05)
+        else:
+            ref, m, _ = O.sgd_step_momentum(ref, g, m, O.SgdConfig(0.05, 0.9, 0.0, 1e-4, True), t == 0)
+    assert same_bits(out["fused"][0], ref)
+
+
+def test_fused_rejects_bad_arguments():
+    x = torch.zeros(16, device="cuda")
+    with pytest.raises(ValueError):
+        K.fused_round_virtual([x], [x], [x], [x], 0.1, alpha=0.0)
+    with pytest.raises(ValueError):
+        K.fused_round_virtual([x], [x], [x], [x], 0.1, mode=1)  # finalize needs delta
+    with pytest.raises(ValueError):
+        K.fused_round_virtual([x], [x], [x], [x], 0.1, momentum=0.9)  # momentum needs m
