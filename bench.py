@@ -143,7 +143,10 @@ def kernel_bytes(name, n, world, comm, algo_code, sgd_momentum=True):
     B = 4 * n
     if name == "fused_round":
         hbm = (7 if world > 1 else 6) * B  # read x,g,m(,own snap); write x,m,next snap
-        nvl = (world - 1) * B  # every peer's snapshot over NVLink
+        nvl = (world - 1) * B  # one-shot: every peer's whole snapshot over NVLink
+        if world > 1 and comm.resolve_algo(algo_code) == 2:  # two-shot: RS in + AG in, own chunk mean via HBM
+            nvl = comm.bytes_per_node(2)
+            hbm += 2 * B // world
         if nvl / NVLINK_PEAK_GBS > hbm / peaks()[0]:
             return nvl, "nvlink"
         return hbm, "hbm"
@@ -441,7 +444,7 @@ def main():
             slot = [0]
 
             def fused():
-                comm.fused_round(slot[0], x, grads[0], lr, **fk)
+                comm.fused_round(slot[0], x, grads[0], lr, algo=algo_code, **fk)
                 slot[0] ^= 1
 
             iso["fused_round"] = timeit(fused, reps=10)

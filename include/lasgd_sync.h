@@ -155,17 +155,20 @@ int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, u
  *   snapshot slot 1-snap_slot = x.
  * Bit-identical to lasgd_sgd_step -> lasgd_comm_allreduce -> lasgd_elastic_pull /
  * lasgd_finalize under the same schedule; launched on `stream` with `nblocks` CTAs
- * (<= 0: the communicator's budget); a launch like lasgd_comm_allreduce (same
+ * (<= 0: the communicator's budget), `algo` one-shot (every peer's whole snapshot) or
+ * two-shot (reduce-scatter of the own chunk, per-CTA mid barrier, then the pull reads
+ * each chunk's mean from its owner); a launch like lasgd_comm_allreduce (same
  * sequence numbers, query / wait / stream_wait apply). */
-int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, void* x, const void* g, void* m, void* delta,
+int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, void* x, const void* g, void* m, void* delta,
                            const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                            unsigned long long* nonfinite, void* stream, unsigned long long* seq);
 /* K7 over P virtual ranks on ONE device (host arrays of P device pointers each;
- * m / delta arrays may be NULL).  Test path for the fused arithmetic. */
-int lasgd_fused_round_virtual(int P, void* const* x, const void* const* g, void* const* m, void* const* delta,
-                              const void* const* snaps, void* const* snap_next, size_t n, int dtype,
-                              const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
-                              unsigned long long* nonfinite, void* stream);
+ * m / delta / xbars arrays may be NULL; two-shot needs per-rank xbars scratch).
+ * Test path for the fused arithmetic and slicing. */
+int lasgd_fused_round_virtual(int P, int algo, void* const* x, const void* const* g, void* const* m,
+                              void* const* delta, const void* const* snaps, void* const* xbars,
+                              void* const* snap_next, size_t n, int dtype, const lasgd_sgd_params* sgd,
+                              double alpha, int mode, int nblocks, unsigned long long* nonfinite, void* stream);
 /* Non-blocking completion poll of launch `seq` (collective.py:142-144 `poll`):
  * 1 complete, 0 in flight, LASGD_ERR_COLLECTIVE failed (diagnostic via
  * lasgd_comm_diagnostic).  Reads a host-mapped flag: no CUDA call. */

@@ -96,9 +96,10 @@ SIGNATURES = {
     "lasgd_comm_open": (_I, [_P, _P]),
     "lasgd_comm_buffer": (_I, [_P, _I, ctypes.POINTER(_P)]),
     "lasgd_comm_allreduce": (_I, [_P, _I, _I, _P, _ULLP]),
-    "lasgd_comm_fused_round": (_I, [_P, _I, _P, _P, _P, _P, ctypes.POINTER(SgdParams), _D, _I, _I, _P, _P, _ULLP]),
-    "lasgd_fused_round_virtual": (_I, [_I, _P, _P, _P, _P, _P, _P, _SZ, _I, ctypes.POINTER(SgdParams), _D, _I, _I,
-                                       _P, _P]),
+    "lasgd_comm_fused_round": (_I, [_P, _I, _I, _P, _P, _P, _P, ctypes.POINTER(SgdParams), _D, _I, _I, _P, _P,
+                                    _ULLP]),
+    "lasgd_fused_round_virtual": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _SZ, _I, ctypes.POINTER(SgdParams), _D,
+                                       _I, _I, _P, _P]),
     "lasgd_comm_query": (_I, [_P, ctypes.c_ulonglong]),
     "lasgd_comm_stream_wait": (_I, [_P, ctypes.c_ulonglong, _P]),
     "lasgd_comm_wait": (_I, [_P, ctypes.c_ulonglong, _D]),

@@ -351,8 +351,8 @@ class P2PCommunicator:
 
     def fused_round(self, slot: int, x: torch.Tensor, g: torch.Tensor, lr: float, *, m=None, delta=None,
                     momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False, first_step=False,
-                    delta_reset=False, alpha: float = 1.0, mode: int = 0, nblocks: int = 0, nonfinite=None,
-                    stream=None) -> int:
+                    delta_reset=False, alpha: float = 1.0, mode: int = 0, algo: int = N.ALGO_AUTO, nblocks: int = 0,
+                    nonfinite=None, stream=None) -> int:
         """K7: local step + mean of snapshot slot ``slot`` over all ranks (NVLink) + pull
         (mode 0) / finalize (mode 1) + write snapshot slot ``1 - slot``, one launch on
         ``stream`` (default: the current stream)."""
@@ -360,7 +360,7 @@ class P2PCommunicator:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         p = K.sgd_params(lr, momentum, dampening, weight_decay, nesterov, first_step, delta_reset)
         seq = ctypes.c_ulonglong()
-        N.check(N.lib().lasgd_comm_fused_round(self._h, slot, K._ptr(x), K._ptr(g), K._ptr(m), K._ptr(delta),
+        N.check(N.lib().lasgd_comm_fused_round(self._h, slot, int(algo), K._ptr(x), K._ptr(g), K._ptr(m), K._ptr(delta),
                                                ctypes.byref(p), float(alpha), int(mode), int(nblocks),
                                                K._ptr(nonfinite), ctypes.c_void_p(s.cuda_stream), ctypes.byref(seq)),
                 "lasgd_comm_fused_round")

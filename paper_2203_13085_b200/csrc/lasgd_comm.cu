@@ -506,11 +506,155 @@ __global__ void __launch_bounds__(256, 2) k_fused_round(CommArgs a, FusedRound<T
   if (!VIRTUAL) publish_done(a);
 }
 
+// Two-shot form of K7 for larger P: (1) reduce-scatter of this rank's chunk slice into
+// its xbar buffer (ring order, same as K3), (2) per-CTA mid barrier, (3) for every chunk
+// q, slice b: local step + pull with chunk q's mean read straight from its owner's
+// xbar over NVLink (own chunk: local), next snapshot.  NVLink in-bytes 2(P-1)/P*B; xbar
+// is written only for the own chunk.  Phase bits as in k_twoshot (virtual ranks run
+// phase 1 and phase 2 as two launches).
+template <typename T, int P, bool VIRTUAL, int U>
+__global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound<T> f) {
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
+  const int b = blockIdx.x;
+  const size_t n = a.n;
+  bool ok = true;
+  unsigned bad = 0;
+  T* own_xbar = reinterpret_cast<T*>(a.xbar[rank]);
+  trace_mark(a, b, 0);
+  if (a.phases & 1) {
+    if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
+    trace_mark(a, b, 1);
+    if (ok) {
+      const T* src[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
+      size_t h0, h1, p0, p1, t0, t1;
+      chunk_slice<T>(chunk_bound(n, P, rank), chunk_bound(n, P, rank + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
+      for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+        Pack<T> v[U][P];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) {
+            Pack<T> o;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+              T lane[P];
+#pragma unroll
+              for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+              o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+              bad += !finite(o.v[k]);
+            }
+            st_plain(own_xbar + pu * W, o);
+          }
+        }
+      }
+      for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) {
+        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+        own_xbar[j] = r;
+        bad += !finite(r);
+      }
+      for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) {
+        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+        own_xbar[j] = r;
+        bad += !finite(r);
+      }
+    }
+  }
+  if (a.phases & 2) {
+    if (!VIRTUAL && ok) ok = cta_barrier<P>(a, 1, b, rank);
+    trace_mark(a, b, 2);
+    if (ok) {
+      T* const x = f.x[vr];
+      const T* const g = f.g[vr];
+      T* const m = f.m[vr];
+      T* const dl = f.delta[vr];
+      T* const sn = f.snap_next[vr];
+      const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+      const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
+      const bool store_d = f.c.use_delta && f.mode == 0;
+      auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
+        unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+        if (f.mode == 0) {
+          bb += pull_elem(f.neg_alpha, xv, sv, zb);
+        } else {
+          xv = add_rn(zb, dv);
+          bb += !finite(xv);
+        }
+        bad += bb;
+      };
+#pragma unroll 1
+      for (int d = 0; d < P; ++d) {
+        const int q = (rank + d) % P;
+        const T* zq = reinterpret_cast<const T*>(a.xbar[q]);  // owner's reduced chunk (NVLink unless q == rank)
+        size_t h0, h1, p0, p1, t0, t1;
+        chunk_slice<T>(chunk_bound(n, P, q), chunk_bound(n, P, q + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+              vz[u] = ld_cg(zq + j);
+              vx[u] = ld_stream(x + j);
+              vg[u] = ld_stream(g + j);
+              if (load_m) vm[u] = ld_stream(m + j);
+              if (load_d) vd[u] = ld_stream(dl + j);
+              if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+#pragma unroll
+              for (int k = 0; k < W; ++k) element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
+              st_stream(x + j, vx[u]);
+              if (f.c.use_mom) st_stream(m + j, vm[u]);
+              if (store_d) st_stream(dl + j, vd[u]);
+              st_stream(sn + j, vx[u]);
+            }
+          }
+        }
+        auto scalar = [&](size_t j) {
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), zq[j]);
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+        };
+        for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) scalar(j);
+        for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) scalar(j);
+      }
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
+  if (!VIRTUAL) publish_done(a);
+}
+
 template <typename T, bool VIRTUAL>
-int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s) {
+int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s,
+                 int algo = LASGD_ALGO_ONESHOT) {
 #define LASGD_FCASE(PP)                                                                             \
   case PP:                                                                                          \
-    k_fused_round<T, PP, VIRTUAL, (PP <= 2 ? 2 : 1)><<<grid, threads, 0, s>>>(a, f);               \
+    if (algo == LASGD_ALGO_TWOSHOT && PP > 1)                                                       \
+      k_fused_twoshot<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)><<<grid, threads, 0, s>>>(a, f);           \
+    else                                                                                            \
+      k_fused_round<T, PP, VIRTUAL, (PP <= 2 ? 2 : 1)><<<grid, threads, 0, s>>>(a, f);             \
     break;
   switch (P) {
     LASGD_FCASE(1)
@@ -661,15 +805,19 @@ extern "C" int lasgd_mean_virtual(void* const* outs, int n_out, const void* cons
   return launch_any(dtype, true, algo, P, a, grid, 256, s);
 }
 
-extern "C" int lasgd_fused_round_virtual(int P, void* const* x, const void* const* g, void* const* m,
-                                         void* const* delta, const void* const* snaps, void* const* snap_next,
-                                         size_t n, int dtype, const lasgd_sgd_params* sgd, double alpha, int mode,
-                                         int nblocks, unsigned long long* nonfinite, void* stream) {
+extern "C" int lasgd_fused_round_virtual(int P, int algo, void* const* x, const void* const* g, void* const* m,
+                                         void* const* delta, const void* const* snaps, void* const* xbars,
+                                         void* const* snap_next, size_t n, int dtype, const lasgd_sgd_params* sgd,
+                                         double alpha, int mode, int nblocks, unsigned long long* nonfinite,
+                                         void* stream) {
   if (P < 1 || P > kMaxR) return fail(LASGD_ERR_UNSUPPORTED, "P=%d outside [1, %d]", P, kMaxR);
   if (!x || !g || !snaps || !snap_next) return fail(LASGD_ERR_INVALID_ARGUMENT, "null pointer array");
   if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
   int rc = check_fused_args(P, x, g, m, delta, snap_next, sgd, alpha, mode);
   if (rc) return rc;
+  algo = P == 1 ? LASGD_ALGO_ONESHOT : resolve_algo(algo, P, n * elem_bytes(dtype));
+  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
+  if (algo == LASGD_ALGO_TWOSHOT && !xbars) return fail(LASGD_ERR_INVALID_ARGUMENT, "two-shot needs per-rank mean buffers");
   if (n == 0) return LASGD_OK;
   if (nblocks <= 0) nblocks = 2 * num_sms();
   CommArgs a;
@@ -677,15 +825,28 @@ extern "C" int lasgd_fused_round_virtual(int P, void* const* x, const void* cons
   for (int q = 0; q < P; ++q) {
     if (!snaps[q] || !aligned16(snaps[q])) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot %d null or unaligned", q);
     a.snap[q] = reinterpret_cast<const char*>(snaps[q]);
+    if (xbars) {
+      if (!xbars[q] || !aligned16(xbars[q])) return fail(LASGD_ERR_INVALID_ARGUMENT, "mean buffer %d null or unaligned", q);
+      a.xbar[q] = reinterpret_cast<char*>(xbars[q]);
+    }
   }
   a.n = n;
   a.nblocks = nblocks;
   a.skip_signal_phase = -1;
   a.nonfinite = nonfinite;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (dtype == LASGD_F32)
-    return launch_fused<float, true>(P, a, make_fused<float>(P, x, g, m, delta, snap_next, sgd, alpha, mode), dim3(nblocks, P), 256, s);
-  return launch_fused<double, true>(P, a, make_fused<double>(P, x, g, m, delta, snap_next, sgd, alpha, mode), dim3(nblocks, P), 256, s);
+  const int nph = algo == LASGD_ALGO_TWOSHOT ? 2 : 1;
+  for (int ph = 0; ph < nph; ++ph) {  // two-shot: reduce-scatter launch, then the pull launch
+    a.phases = algo == LASGD_ALGO_TWOSHOT ? (1 << ph) : 3;
+    if (dtype == LASGD_F32)
+      rc = launch_fused<float, true>(P, a, make_fused<float>(P, x, g, m, delta, snap_next, sgd, alpha, mode),
+                                     dim3(nblocks, P), 256, s, algo);
+    else
+      rc = launch_fused<double, true>(P, a, make_fused<double>(P, x, g, m, delta, snap_next, sgd, alpha, mode),
+                                      dim3(nblocks, P), 256, s, algo);
+    if (rc) return rc;
+  }
+  return LASGD_OK;
 }
 
 // ====================================================================== communicator
@@ -910,10 +1071,12 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
   return LASGD_OK;
 }
 
-extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, void* x, const void* g, void* m, void* delta,
-                                      const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, void* x, const void* g, void* m,
+                                      void* delta, const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                                       unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  algo = c->world == 1 ? LASGD_ALGO_ONESHOT : resolve_algo(algo, c->world, c->n * c->elem);
+  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   void* xs[1] = {x};
   const void* gs[1] = {g};
   void* ms[1] = {m};
@@ -934,9 +1097,9 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, void* x, con
   a.nonfinite = nonfinite;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (c->dtype == LASGD_F32)
-    rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs);
+    rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, algo);
   else
-    rc = launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs);
+    rc = launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, algo);
   if (rc) return rc;
   LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
   if (seq) *seq = s;

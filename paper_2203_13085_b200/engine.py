@@ -160,7 +160,8 @@ class LASGDWorker:
         else:
             box = {}
             self._launch("fused_round", self.compute, lambda: box.setdefault("s", self.comm.fused_round(
-                cur, st.x_local, self.g, lr, m=st.momentum_buf, delta=st.delta, nblocks=self.fused_nblocks,
+                cur, st.x_local, self.g, lr, m=st.momentum_buf, delta=st.delta, algo=self.algo,
+                nblocks=self.fused_nblocks,
                 stream=self.compute, **kw)))
             self.seq = box["s"]
         st._momentum_started = st.momentum_buf is not None

@@ -103,20 +103,23 @@ def sgd_params(lr: float, momentum=0.0, dampening=0.0, weight_decay=0.0, nestero
 
 def fused_round_virtual(xs, gs, snaps, snap_nexts, lr: float, *, ms=None, deltas=None, momentum=0.0,
                         dampening=0.0, weight_decay=0.0, nesterov=False, first_step=False, delta_reset=False,
-                        alpha: float = 1.0, mode: int = 0, nblocks: int = 0, nonfinite=None, stream=None) -> None:
+                        alpha: float = 1.0, mode: int = 0, algo: int = N.ALGO_ONESHOT, xbars=None, nblocks: int = 0,
+                        nonfinite=None, stream=None) -> None:
     """K7 for P ranks on one device: local step + ring-order mean of ``snaps`` + pull
-    (mode 0) or finalize (mode 1) + next snapshot, one pass."""
+    (mode 0) or finalize (mode 1) + next snapshot, one pass (two launches for the
+    two-shot form, which needs per-rank ``xbars`` scratch)."""
     P = len(xs)
-    flat = list(xs) + list(gs) + list(snaps) + list(snap_nexts) + list(ms or []) + list(deltas or [])
+    flat = list(xs) + list(gs) + list(snaps) + list(snap_nexts) + list(ms or []) + list(deltas or []) + list(xbars or [])
     code, n = _check(*flat)
 
     def arr(ts):
         return None if ts is None else (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
 
     p = sgd_params(lr, momentum, dampening, weight_decay, nesterov, first_step, delta_reset)
-    N.check(N.lib().lasgd_fused_round_virtual(P, arr(xs), arr(gs), arr(ms), arr(deltas), arr(snaps),
-                                              arr(snap_nexts), n, code, ctypes.byref(p), float(alpha), int(mode),
-                                              int(nblocks), _ptr(nonfinite), _stream(stream)), "fused_round_virtual")
+    N.check(N.lib().lasgd_fused_round_virtual(P, int(algo), arr(xs), arr(gs), arr(ms), arr(deltas), arr(snaps),
+                                              arr(xbars), arr(snap_nexts), n, code, ctypes.byref(p), float(alpha),
+                                              int(mode), int(nblocks), _ptr(nonfinite), _stream(stream)),
+            "fused_round_virtual")
 
 
 def mean_virtual(outs: Sequence[torch.Tensor], srcs: Sequence[torch.Tensor], algo: int = N.ALGO_ONESHOT,

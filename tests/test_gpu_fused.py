@@ -27,11 +27,12 @@ CFGS = [O.SgdConfig(0.1, 0.9, 0.0, 1e-4, True), O.SgdConfig(0.05, 0.0, 0.0, 0.0,
         O.SgdConfig(0.07, 0.8, 0.1, 5e-4, False)]
 
 
+@pytest.mark.parametrize("algo", [1, 2])
 @pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 8])
 @pytest.mark.parametrize("n", [1, 7, 4099, 1_000_003])
 @pytest.mark.parametrize("ci", [0, 1, 2])
 @pytest.mark.parametrize("first", [True, False])
-def test_fused_pull_bit_exact(P, n, ci, first):
+def test_fused_pull_bit_exact(algo, P, n, ci, first):
     cfg = CFGS[ci]
     rng = np.random.default_rng(P * 100 + n % 97 + ci)
     xs = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
@@ -42,8 +43,10 @@ def test_fused_pull_bit_exact(P, n, ci, first):
     xt, gt, st = [dev(v) for v in xs], [dev(v) for v in gs], [dev(v) for v in snaps]
     mt = [dev(v) for v in ms] if cfg.momentum else None
     nt = [torch.full_like(x, float("nan")) for x in xt]
+    xb = [torch.full_like(x, float("nan")) for x in xt] if algo == 2 else None
     K.fused_round_virtual(xt, gt, st, nt, cfg.lr, ms=mt, momentum=cfg.momentum, dampening=cfg.dampening,
-                          weight_decay=cfg.weight_decay, nesterov=cfg.nesterov, first_step=first, alpha=alpha)
+                          weight_decay=cfg.weight_decay, nesterov=cfg.nesterov, first_step=first, alpha=alpha,
+                          algo=algo, xbars=xb, nblocks=(7 if n > 1000 else 0))
     torch.cuda.synchronize()
     zbar = O.ring_mean(snaps) if P > 1 else None
     for r in range(P):
@@ -55,8 +58,9 @@ def test_fused_pull_bit_exact(P, n, ci, first):
             assert same_bits(mt[r].cpu().numpy(), m1)
 
 
+@pytest.mark.parametrize("algo", [1, 2])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_fused_finalize_matches_reference_bookkeeping(P):
+def test_fused_finalize_matches_reference_bookkeeping(algo, P):
     n = 10_007
     rng = np.random.default_rng(P)
     xs = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
@@ -65,7 +69,8 @@ def test_fused_finalize_matches_reference_bookkeeping(P):
     snaps = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
     xt, gt, st, dt_ = [dev(v) for v in xs], [dev(v) for v in gs], [dev(v) for v in snaps], [dev(v) for v in ds]
     nt = [torch.empty_like(x) for x in xt]
-    K.fused_round_virtual(xt, gt, st, nt, 0.03, deltas=dt_, mode=1)
+    xb = [torch.empty_like(x) for x in xt] if algo == 2 else None
+    K.fused_round_virtual(xt, gt, st, nt, 0.03, deltas=dt_, mode=1, algo=algo, xbars=xb)
     torch.cuda.synchronize()
     z = O.ring_mean(snaps)
     for r in range(P):

@@ -78,16 +78,17 @@ def _w_worker_loop(rank, world, port):
     n, steps = 100_003, 9
     x0 = _vec(7, n)
     grads = np.stack([np.stack([_vec(100 * t + r, n) for r in range(world)]) for t in range(steps)])
-    cases = [(2, 1.0, None, "overlap"), (1, 0.5, L.SgdConfig(0.9, 0.0, 1e-4, True), "overlap"), (3, 0.25, None, "overlap"),
-             (1, 1.0, L.SgdConfig(0.9, 0.0, 1e-4, True), "fused"), (2, 0.5, None, "fused")]
-    for k, alpha, sgd, pipe in cases:
+    mom = L.SgdConfig(0.9, 0.0, 1e-4, True)
+    cases = [(2, 1.0, None, "overlap", 1), (1, 0.5, mom, "overlap", 2), (3, 0.25, None, "overlap", 1),
+             (1, 1.0, mom, "fused", 1), (2, 0.5, None, "fused", 1), (1, 0.5, mom, "fused", 2), (3, 1.0, None, "fused", 2)]
+    for k, alpha, sgd, pipe, algo in cases:
         comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
         x = torch.from_numpy(x0.copy()).cuda()
         g = torch.empty_like(x)
         compute = torch.cuda.Stream(priority=-1)
         with torch.cuda.stream(compute):
             w = L.LASGDWorker(x, g, comm=comm, sync_period=k, alpha=alpha, sgd=sgd, lr=0.05, mode="pull",
-                              compute_stream=compute, pipeline=pipe)
+                              compute_stream=compute, pipeline=pipe, algo=algo)
             for t in range(steps):
                 g.copy_(torch.from_numpy(grads[t, rank]), non_blocking=False)
                 w.step()
@@ -95,7 +96,7 @@ def _w_worker_loop(rank, world, port):
         torch.cuda.synchronize()
         cfg = None if sgd is None else O.SgdConfig(0.05, sgd.momentum, sgd.dampening, sgd.weight_decay, sgd.nesterov)
         xs, _, _, _ = O.run_lasgd_pull(x0, grads, np.full(steps, 0.05), world, k, alpha, sgd=cfg)
-        assert _same_bits(x.cpu().numpy(), xs[rank]), (k, alpha, pipe, rank)
+        assert _same_bits(x.cpu().numpy(), xs[rank]), (k, alpha, pipe, algo, rank)
         dist.barrier()
         comm.close()
     # reference bookkeeping (delta mode) through the worker
@@ -103,9 +104,9 @@ def _w_worker_loop(rank, world, port):
     x = torch.from_numpy(x0.copy()).cuda()
     g = torch.empty_like(x)
     xs, _, _, _ = O.run_lasgd_delta(x0, grads, np.full(steps, 0.05), world, 2)
-    for pipe in ("overlap", "fused"):
+    for pipe, algo in (("overlap", 2), ("fused", 1), ("fused", 2)):
         x = torch.from_numpy(x0.copy()).cuda()
-        w = L.LASGDWorker(x, g, comm=comm, sync_period=2, lr=0.05, mode="delta", pipeline=pipe)
+        w = L.LASGDWorker(x, g, comm=comm, sync_period=2, lr=0.05, mode="delta", pipeline=pipe, algo=algo)
         for t in range(steps):
             g.copy_(torch.from_numpy(grads[t, rank]))
             w.step()
