@@ -1086,7 +1086,9 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
   ns[0] = c->base + c->off_snap[1 - snap_slot];
   int rc = check_fused_args(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode);
   if (rc) return rc;
-  if (nblocks <= 0) nblocks = c->nblocks;
+  // default: 2 CTAs per SM (the fused pass owns the GPU at a round boundary); every
+  // rank computes the same value, so the per-CTA flag slots line up
+  if (nblocks <= 0) nblocks = 2 * num_sms() <= kMaxB ? 2 * num_sms() : kMaxB;
   if (nblocks > kMaxB) return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d > %d", nblocks, kMaxB);
   DeviceGuard dg(c->device);
   CommArgs a;
