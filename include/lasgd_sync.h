@@ -191,6 +191,58 @@ int lasgd_comm_set_trace(lasgd_comm* c, int on);
 int lasgd_comm_read_trace(lasgd_comm* c, unsigned long long* out, int max_ctas);
 int lasgd_comm_destroy(lasgd_comm* c);
 
+/* rank, world size and the mean buffer of a communicator (any pointer may be NULL). */
+int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar);
+
+/* ---- native per-rank worker: the round protocol (optimizer.py:181-207) ---- */
+
+typedef struct lasgd_worker lasgd_worker;
+
+#define LASGD_TAU_HIST 64
+#define LASGD_KERNEL_KINDS 6 /* sgd_step, snapshot, pull, finalize, allreduce, fused_round */
+
+typedef struct {
+  int sync_period;     /* deterministic schedule: local steps per round (tau)                    */
+  double alpha;        /* elastic coefficient, (0, 1]                                            */
+  int mode;            /* 0 pull x -= alpha*(snap - xbar); 1 reference finalize z + delta (alpha 1) */
+  int pipeline;        /* 0 overlap (K5 | K4 | K2/K3 on the side stream); 1 fused (K7)           */
+  int algo;            /* LASGD_ALGO_*                                                           */
+  int fused_nblocks;   /* CTAs of K7 (<= 0: 2 per SM)                                            */
+  double momentum, dampening, weight_decay;
+  int nesterov;
+  int sync;            /* 0: local steps only (the no-sync ceiling)                              */
+  int adaptive;        /* 1: close a round as soon as the mean landed (overlap pipeline only)    */
+  int tau_max;         /* adaptive budget (optimizer.py:141-144); <= 0: sync_period              */
+  int max_host_lead;   /* adaptive: host may run at most this many steps ahead of the GPU        */
+} lasgd_worker_config;
+
+typedef struct {
+  int tau_i, snap_idx;
+  long long local_clock, global_clock;
+  unsigned long long seq;
+  int momentum_started, delta_fresh;
+  long long launches[LASGD_KERNEL_KINDS];
+  long long tau_hist[LASGD_TAU_HIST]; /* rounds closed after t local steps */
+} lasgd_worker_state;
+
+/* comm NULL = single rank (snap0/snap1 required); with a communicator the snapshot
+ * slots and the mean buffer are the communicator's.  x, m (momentum != 0), delta
+ * (mode 1) are caller-owned device buffers of n elements.  Issues the initial
+ * snapshot (and, overlap pipeline, the round-0 launch) on compute_stream. */
+int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* delta, void* snap0, void* snap1, size_t n,
+                        int dtype, const lasgd_worker_config* cfg, void* compute_stream, void* side_stream,
+                        unsigned long long* nonfinite, lasgd_worker** out);
+/* One local step from gradient g at rate lr (lr_at of the local clock, problems.py:355);
+ * returns 1 when the step closed a round, 0 otherwise, < 0 on error. */
+int lasgd_worker_step(lasgd_worker* w, const void* g, double lr);
+/* Order the compute stream after the in-flight mean (overlap pipeline). */
+int lasgd_worker_drain(lasgd_worker* w);
+int lasgd_worker_get_state(lasgd_worker* w, lasgd_worker_state* s);
+int lasgd_worker_set_timing(lasgd_worker* w, int on);
+int lasgd_worker_timings(lasgd_worker* w, int kind, float* out_ms, int max);
+int lasgd_worker_reset_stats(lasgd_worker* w);
+int lasgd_worker_destroy(lasgd_worker* w);
+
 /* ---- host utilities ------------------------------------------------------ */
 
 /* partition_chunks (params.py:130-147): writes num_chunks+1 boundaries. */

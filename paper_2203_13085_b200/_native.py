@@ -73,6 +73,43 @@ class CommConfig(ctypes.Structure):
     ]
 
 
+TAU_HIST = 64
+KERNEL_KINDS = ("sgd_step", "snapshot", "pull", "finalize", "allreduce", "fused_round")
+
+
+class WorkerConfig(ctypes.Structure):
+    _fields_ = [
+        ("sync_period", ctypes.c_int),
+        ("alpha", ctypes.c_double),
+        ("mode", ctypes.c_int),
+        ("pipeline", ctypes.c_int),
+        ("algo", ctypes.c_int),
+        ("fused_nblocks", ctypes.c_int),
+        ("momentum", ctypes.c_double),
+        ("dampening", ctypes.c_double),
+        ("weight_decay", ctypes.c_double),
+        ("nesterov", ctypes.c_int),
+        ("sync", ctypes.c_int),
+        ("adaptive", ctypes.c_int),
+        ("tau_max", ctypes.c_int),
+        ("max_host_lead", ctypes.c_int),
+    ]
+
+
+class WorkerState(ctypes.Structure):
+    _fields_ = [
+        ("tau_i", ctypes.c_int),
+        ("snap_idx", ctypes.c_int),
+        ("local_clock", ctypes.c_longlong),
+        ("global_clock", ctypes.c_longlong),
+        ("seq", ctypes.c_ulonglong),
+        ("momentum_started", ctypes.c_int),
+        ("delta_fresh", ctypes.c_int),
+        ("launches", ctypes.c_longlong * len(KERNEL_KINDS)),
+        ("tau_hist", ctypes.c_longlong * TAU_HIST),
+    ]
+
+
 _P = ctypes.c_void_p
 _SZ = ctypes.c_size_t
 _I = ctypes.c_int
@@ -110,6 +147,16 @@ SIGNATURES = {
     "lasgd_comm_set_trace": (_I, [_P, _I]),
     "lasgd_comm_read_trace": (_I, [_P, _P, _I]),
     "lasgd_comm_destroy": (_I, [_P]),
+    "lasgd_comm_info": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_P)]),
+    "lasgd_worker_create": (_I, [_P, _P, _P, _P, _P, _P, _SZ, _I, ctypes.POINTER(WorkerConfig), _P, _P, _P,
+                                 ctypes.POINTER(_P)]),
+    "lasgd_worker_step": (_I, [_P, _P, _D]),
+    "lasgd_worker_drain": (_I, [_P]),
+    "lasgd_worker_get_state": (_I, [_P, ctypes.POINTER(WorkerState)]),
+    "lasgd_worker_set_timing": (_I, [_P, _I]),
+    "lasgd_worker_timings": (_I, [_P, _I, ctypes.POINTER(ctypes.c_float), _I]),
+    "lasgd_worker_reset_stats": (_I, [_P]),
+    "lasgd_worker_destroy": (_I, [_P]),
     "lasgd_partition_chunks": (_I, [_SZ, _I, ctypes.POINTER(_SZ)]),
     "lasgd_bytes_per_node": (ctypes.c_ulonglong, [_SZ, _I, _I, _I]),
 }

@@ -986,6 +986,14 @@ extern "C" int lasgd_comm_resolve_algo(lasgd_comm* c, int algo) {
   return resolve_algo(algo, c->world, c->n * c->elem);
 }
 
+extern "C" int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (xbar) *xbar = c->base + c->off_xbar;
+  return LASGD_OK;
+}
+
 extern "C" int lasgd_comm_set_trace(lasgd_comm* c, int on) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   c->trace_on = on != 0;

@@ -1,0 +1,355 @@
+// Native per-rank LASGD worker: the round protocol of Algorithm 1 (
+// optimizer.py:181-207) as a host-side state machine over CUDA streams and events,
+// so one C call issues a whole local step (the Python layer only forwards the
+// gradient pointer and the learning rate).
+//
+// pipeline OVERLAP: compute stream K5 every step; at a round boundary the compute
+//   stream waits for the previous launch (event), applies K4 (pull or reference
+//   finalize, writing the next snapshot slot) and hands the snapshot to the side
+//   stream, where K2/K3 runs while the next minibatches proceed.
+// pipeline FUSED (deterministic only): the boundary step is one K7 launch (local step
+//   + NVLink mean + pull + next snapshot); other steps are K5.
+// adaptive: a round closes as soon as the host-mapped completion flag of the
+//   in-flight launch is set, or when tau_max local steps have been taken (then the
+//   compute stream waits on the event; the host never blocks except for the optional
+//   run-ahead throttle that bounds how far the host's view runs ahead of the GPU).
+#include <string.h>
+
+#include <vector>
+
+#include "lasgd_common.cuh"
+
+namespace lasgd {
+
+enum Kind { K_SGD = 0, K_SNAPSHOT, K_PULL, K_FINALIZE, K_ALLREDUCE, K_FUSED, K_KINDS };
+
+struct TimingRec {
+  int kind;
+  cudaEvent_t e0, e1;
+};
+
+}  // namespace lasgd
+
+using namespace lasgd;
+
+struct lasgd_worker {
+  lasgd_comm* comm = nullptr;
+  int world = 1, rank = 0, dtype = LASGD_F32;
+  size_t n = 0;
+  void* x = nullptr;
+  void* m = nullptr;
+  void* delta = nullptr;
+  void* snap[2] = {nullptr, nullptr};
+  void* xbar = nullptr;
+  lasgd_worker_config cfg;
+  cudaStream_t compute = nullptr, side = nullptr;
+  unsigned long long* nonfinite = nullptr;
+  // protocol state (mirrors NodeState, optimizer.py:79-104)
+  int tau = 0, snap_idx = 0;
+  long long local_clock = 0, global_clock = 0;
+  bool mom_started = false, delta_fresh = false;
+  unsigned long long seq = 0;
+  cudaEvent_t ev_snap = nullptr;
+  std::vector<cudaEvent_t> lead;  // adaptive run-ahead throttle ring
+  size_t lead_pos = 0;
+  long long lead_count = 0;
+  // instrumentation
+  bool timed = false;
+  std::vector<TimingRec> recs;
+  std::vector<cudaEvent_t> pool;
+  long long launches[K_KINDS] = {0};
+  long long tau_hist[LASGD_TAU_HIST] = {0};
+};
+
+static cudaEvent_t pool_get(lasgd_worker* w) {
+  if (!w->pool.empty()) {
+    cudaEvent_t e = w->pool.back();
+    w->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Issue one kernel launch with optional timing events around it on `s`.
+template <typename F>
+static int issue(lasgd_worker* w, int kind, cudaStream_t s, F&& fn) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (w->timed) {
+    e0 = pool_get(w);
+    e1 = pool_get(w);
+    cudaEventRecord(e0, s);
+  }
+  int rc = fn();
+  if (rc) return rc;
+  if (w->timed) {
+    cudaEventRecord(e1, s);
+    w->recs.push_back({kind, e0, e1});
+  }
+  w->launches[kind]++;
+  return LASGD_OK;
+}
+
+static lasgd_sgd_params sgd_params(const lasgd_worker* w, double lr) {
+  lasgd_sgd_params p;
+  p.lr = lr;
+  p.momentum = w->cfg.momentum;
+  p.dampening = w->cfg.dampening;
+  p.weight_decay = w->cfg.weight_decay;
+  p.nesterov = w->cfg.nesterov;
+  p.first_step = !w->mom_started;
+  p.delta_reset = w->delta_fresh;
+  return p;
+}
+
+static bool finalize_mode(const lasgd_worker* w) { return w->cfg.mode == 1 && w->cfg.alpha == 1.0; }
+
+static int submit_allreduce(lasgd_worker* w, int slot) {
+  LASGD_CUDA_TRY(cudaEventRecord(w->ev_snap, w->compute));
+  LASGD_CUDA_TRY(cudaStreamWaitEvent(w->side, w->ev_snap, 0));
+  unsigned long long s = 0;
+  int rc = issue(w, K_ALLREDUCE, w->side,
+                 [&] { return lasgd_comm_allreduce(w->comm, slot, w->cfg.algo, (void*)w->side, &s); });
+  if (rc) return rc;
+  w->seq = s;
+  return LASGD_OK;
+}
+
+static void close_round_bookkeeping(lasgd_worker* w, int closed_tau) {
+  w->tau_hist[closed_tau < LASGD_TAU_HIST ? closed_tau : LASGD_TAU_HIST - 1]++;
+  w->snap_idx = 1 - w->snap_idx;
+  w->delta_fresh = w->delta != nullptr;
+  w->tau = 0;
+  w->global_clock++;
+}
+
+// Round boundary of the overlap pipeline (optimizer.py:152-178 + the next submit).
+static int close_round(lasgd_worker* w) {
+  const int cur = w->snap_idx, nxt = 1 - cur;
+  int rc;
+  if (w->world == 1) {
+    // optimizer.py:168-169: P == 1 keeps the live model; only the snapshot moves
+    rc = issue(w, K_SNAPSHOT, w->compute,
+               [&] { return lasgd_snapshot(w->snap[nxt], w->x, w->n, w->dtype, (void*)w->compute); });
+  } else {
+    rc = lasgd_comm_stream_wait(w->comm, w->seq, (void*)w->compute);
+    if (rc) return rc;
+    if (finalize_mode(w))
+      rc = issue(w, K_FINALIZE, w->compute, [&] {
+        return lasgd_finalize(w->x, w->snap[nxt], w->xbar, w->delta, w->n, w->dtype, w->nonfinite, (void*)w->compute);
+      });
+    else
+      rc = issue(w, K_PULL, w->compute, [&] {
+        return lasgd_elastic_pull(w->x, w->snap[nxt], w->snap[cur], w->xbar, w->n, w->dtype, w->cfg.alpha,
+                                  w->nonfinite, (void*)w->compute);
+      });
+  }
+  if (rc) return rc;
+  close_round_bookkeeping(w, w->tau);
+  if (w->world > 1) return submit_allreduce(w, w->snap_idx);
+  return LASGD_OK;
+}
+
+static int fused_step(lasgd_worker* w, const void* g, double lr) {
+  const int cur = w->snap_idx, nxt = 1 - cur;
+  lasgd_sgd_params p = sgd_params(w, lr);
+  const int mode = finalize_mode(w) ? 1 : 0;
+  int rc;
+  if (w->world == 1) {
+    void* xs[1] = {w->x};
+    const void* gs[1] = {g};
+    void* ms[1] = {w->m};
+    void* ds[1] = {w->delta};
+    const void* ss[1] = {w->snap[cur]};
+    void* ns[1] = {w->snap[nxt]};
+    rc = issue(w, K_FUSED, w->compute, [&] {
+      return lasgd_fused_round_virtual(1, LASGD_ALGO_ONESHOT, xs, gs, w->m ? ms : nullptr, w->delta ? ds : nullptr,
+                                       ss, nullptr, ns, w->n, w->dtype, &p, w->cfg.alpha, mode,
+                                       w->cfg.fused_nblocks, w->nonfinite, (void*)w->compute);
+    });
+  } else {
+    unsigned long long s = 0;
+    rc = issue(w, K_FUSED, w->compute, [&] {
+      return lasgd_comm_fused_round(w->comm, cur, w->cfg.algo, w->x, g, w->m, w->delta, &p, w->cfg.alpha, mode,
+                                    w->cfg.fused_nblocks, w->nonfinite, (void*)w->compute, &s);
+    });
+    if (!rc) w->seq = s;
+  }
+  if (rc) return rc;
+  w->mom_started = w->m != nullptr;
+  w->local_clock++;
+  close_round_bookkeeping(w, w->tau + 1);
+  return 1;
+}
+
+extern "C" int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* delta, void* snap0, void* snap1,
+                                   size_t n, int dtype, const lasgd_worker_config* cfg, void* compute_stream,
+                                   void* side_stream, unsigned long long* nonfinite, lasgd_worker** out) {
+  if (!out || !cfg || !x) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (cfg->sync_period < 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "sync_period must be >= 1");
+  if (!(cfg->alpha > 0.0 && cfg->alpha <= 1.0)) return fail(LASGD_ERR_INVALID_ARGUMENT, "alpha must be in (0, 1]");
+  if (cfg->mode != 0 && cfg->mode != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "mode must be 0 (pull) or 1 (delta)");
+  if (cfg->mode == 1 && !delta) return fail(LASGD_ERR_INVALID_ARGUMENT, "delta mode needs the delta buffer");
+  if (cfg->pipeline != 0 && cfg->pipeline != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "pipeline must be 0 or 1");
+  if (cfg->pipeline == 1 && cfg->adaptive)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "the fused pipeline implements the deterministic schedule only");
+  if (cfg->momentum != 0.0 && !m) return fail(LASGD_ERR_INVALID_ARGUMENT, "momentum needs m");
+  lasgd_worker* w = new lasgd_worker();
+  w->comm = comm;
+  w->x = x;
+  w->m = m;
+  w->delta = delta;
+  w->n = n;
+  w->dtype = dtype;
+  w->cfg = *cfg;
+  if (w->cfg.tau_max < 1) w->cfg.tau_max = w->cfg.sync_period;
+  w->compute = reinterpret_cast<cudaStream_t>(compute_stream);
+  w->side = reinterpret_cast<cudaStream_t>(side_stream);
+  w->nonfinite = nonfinite;
+  if (comm) {
+    int wr = 0;
+    if ((wr = lasgd_comm_info(comm, &w->rank, &w->world, &w->xbar)) != 0) {
+      delete w;
+      return wr;
+    }
+    if (lasgd_comm_buffer(comm, 0, &w->snap[0]) || lasgd_comm_buffer(comm, 1, &w->snap[1])) {
+      delete w;
+      return LASGD_ERR_INVALID_ARGUMENT;
+    }
+  } else {
+    if (!snap0 || !snap1) {
+      delete w;
+      return fail(LASGD_ERR_INVALID_ARGUMENT, "without a communicator two snapshot buffers are required");
+    }
+    w->snap[0] = snap0;
+    w->snap[1] = snap1;
+  }
+  cudaError_t e = cudaEventCreateWithFlags(&w->ev_snap, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    delete w;
+    return cuda_fail(e, "cudaEventCreate");
+  }
+  // Algorithm 1 lines 1-5: snapshot = x0, submit round 0 (overlap pipeline)
+  int rc = issue(w, K_SNAPSHOT, w->compute,
+                 [&] { return lasgd_snapshot(w->snap[0], w->x, w->n, w->dtype, (void*)w->compute); });
+  if (!rc && w->world > 1 && w->cfg.sync && w->cfg.pipeline == 0) rc = submit_allreduce(w, 0);
+  if (rc) {
+    lasgd_worker_destroy(w);
+    return rc;
+  }
+  *out = w;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_worker_step(lasgd_worker* w, const void* g, double lr) {
+  if (!w || !g) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  if (w->cfg.pipeline == 1 && w->cfg.sync && w->tau + 1 == w->cfg.sync_period) return fused_step(w, g, lr);
+  lasgd_sgd_params p = sgd_params(w, lr);
+  int rc = issue(w, K_SGD, w->compute, [&] {
+    return lasgd_sgd_step(w->x, g, w->m, w->delta, w->n, w->dtype, &p, w->nonfinite, (void*)w->compute);
+  });
+  if (rc) return rc;
+  w->mom_started = w->m != nullptr;
+  w->delta_fresh = false;
+  w->tau++;
+  w->local_clock++;
+  if (!w->cfg.sync) return 0;
+  if (w->cfg.adaptive) {
+    if (w->cfg.max_host_lead > 0) {
+      if (w->lead.empty()) {
+        w->lead.resize(w->cfg.max_host_lead);
+        for (auto& ev : w->lead) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      }
+      cudaEvent_t& slot = w->lead[w->lead_pos];
+      if (w->lead_count >= w->cfg.max_host_lead) cudaEventSynchronize(slot);
+      cudaEventRecord(slot, w->compute);
+      w->lead_pos = (w->lead_pos + 1) % w->lead.size();
+      w->lead_count++;
+    }
+    int done = 1;
+    if (w->world > 1) {
+      done = lasgd_comm_query(w->comm, w->seq);
+      if (done < 0) return done;
+    }
+    if (done == 1 || w->tau >= w->cfg.tau_max) {
+      rc = close_round(w);
+      return rc ? rc : 1;
+    }
+    return 0;
+  }
+  if (w->tau == w->cfg.sync_period) {
+    rc = close_round(w);
+    return rc ? rc : 1;
+  }
+  return 0;
+}
+
+extern "C" int lasgd_worker_drain(lasgd_worker* w) {
+  if (!w) return fail(LASGD_ERR_INVALID_ARGUMENT, "null worker");
+  if (w->world > 1 && w->seq && w->cfg.pipeline == 0) return lasgd_comm_stream_wait(w->comm, w->seq, (void*)w->compute);
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_worker_get_state(lasgd_worker* w, lasgd_worker_state* s) {
+  if (!w || !s) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  s->tau_i = w->tau;
+  s->snap_idx = w->snap_idx;
+  s->local_clock = w->local_clock;
+  s->global_clock = w->global_clock;
+  s->seq = w->seq;
+  s->momentum_started = w->mom_started;
+  s->delta_fresh = w->delta_fresh;
+  for (int k = 0; k < LASGD_KERNEL_KINDS; ++k) s->launches[k] = w->launches[k];
+  for (int t = 0; t < LASGD_TAU_HIST; ++t) s->tau_hist[t] = w->tau_hist[t];
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_worker_set_timing(lasgd_worker* w, int on) {
+  if (!w) return fail(LASGD_ERR_INVALID_ARGUMENT, "null worker");
+  w->timed = on != 0;
+  return LASGD_OK;
+}
+
+// Durations (ms) of the timed launches of `kind` since the last reset, oldest first.
+// The caller synchronises first.  Returns the number written.
+extern "C" int lasgd_worker_timings(lasgd_worker* w, int kind, float* out, int max) {
+  if (!w || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  int k = 0;
+  for (const auto& r : w->recs) {
+    if (r.kind != kind) continue;
+    if (k >= max) break;
+    float ms = 0.f;
+    LASGD_CUDA_TRY(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    out[k++] = ms;
+  }
+  return k;
+}
+
+extern "C" int lasgd_worker_reset_stats(lasgd_worker* w) {
+  if (!w) return fail(LASGD_ERR_INVALID_ARGUMENT, "null worker");
+  for (auto& r : w->recs) {
+    w->pool.push_back(r.e0);
+    w->pool.push_back(r.e1);
+  }
+  w->recs.clear();
+  memset(w->launches, 0, sizeof(w->launches));
+  memset(w->tau_hist, 0, sizeof(w->tau_hist));
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_worker_destroy(lasgd_worker* w) {
+  if (!w) return LASGD_OK;
+  cudaStreamSynchronize(w->compute);
+  if (w->side) cudaStreamSynchronize(w->side);
+  for (auto& r : w->recs) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  for (auto e : w->pool) cudaEventDestroy(e);
+  for (auto e : w->lead) cudaEventDestroy(e);
+  if (w->ev_snap) cudaEventDestroy(w->ev_snap);
+  delete w;
+  return LASGD_OK;
+}

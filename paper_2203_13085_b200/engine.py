@@ -2,40 +2,83 @@
 
 This is Algorithm 1 (optimizer.py:181-207) driven by real
 asynchrony instead of the reference's caller-supplied ``collective_complete``
-flag:
+flag.  The protocol itself runs natively (``lasgd_worker_*`` in
+csrc/lasgd_worker.cu): one ctypes call per local step issues every launch of
+that step, so the host keeps well ahead of the GPU.
 
 * compute stream (high priority): forward/backward (PyTorch), then K5 — the
   fused local step on the flat buffer — every minibatch;
-* at a round boundary: the compute stream waits for the previous round's mean
-  (event), applies the fused pull / finalize that also writes the next
-  snapshot slot (K4+K1), and hands the snapshot to the side stream;
-* side stream (low priority, bounded CTA budget): the NVLink P2P mean
-  all-reduce (K2/K3 with K6 flags) overlaps the next minibatches.
+* ``pipeline="overlap"``: at a round boundary the compute stream waits for the
+  previous round's mean (event), applies the fused pull / finalize that also
+  writes the next snapshot slot (K4+K1) and hands the snapshot to the side
+  stream (low priority, bounded CTA budget), where the NVLink P2P mean
+  all-reduce (K2/K3 with K6 flags) overlaps the next minibatches;
+* ``pipeline="fused"`` (deterministic only): the boundary step is ONE kernel
+  (K7) that applies the local step, reads every peer's snapshot over NVLink,
+  forms the ring-order mean, pulls and writes the next snapshot — bit-identical
+  results, HBM and NVLink streamed concurrently.
 
-Round boundaries are either deterministic (exactly ``sync_period`` local steps
-per round — the parity schedule) or adaptive (finalize as soon as the
-host-mapped completion flag says the mean landed, or block the compute stream
-when ``tau_max`` steps have been taken — the paper's dynamic rate, Table 3).
-
-``pipeline="fused"`` (deterministic only) replaces the boundary step's
-K5 -> (mean lands) -> K4 -> K2/K3 chain by ONE kernel (K7) that applies the local
-step, reads every peer's snapshot over NVLink, forms the ring-order mean, pulls and
-writes the next snapshot in the same pass — bit-identical results, HBM and NVLink
-streamed concurrently.  ``pipeline="overlap"`` (default) keeps the mean on the side
-stream so it overlaps the next minibatches' forward/backward.
+Round boundaries are deterministic (exactly ``sync_period`` local steps per
+round — the parity schedule) or adaptive (finalize as soon as the host-mapped
+completion flag says the mean landed, or make the compute stream wait when
+``tau_max`` steps have been taken — the paper's dynamic rate, Table 3).
 """
 
 from __future__ import annotations
 
 import collections
+import ctypes
 from typing import Optional
 
 import torch
 
 from . import _native as N
 from . import kernels as K
-from .optimizer import NodeState, SgdConfig
+from .optimizer import SgdConfig, _FiniteMonitor
 from .problems import LrSchedule, lr_at
+
+
+class WorkerState:
+    """NodeState-shaped view (optimizer.py:79-104) of the native worker."""
+
+    def __init__(self, worker: "LASGDWorker", x, snapshots, delta, momentum_buf, finite):
+        self._w = worker
+        self.rank = worker.rank
+        self.x_local = x
+        self.snapshots = snapshots
+        self.delta = delta
+        self.momentum_buf = momentum_buf
+        self._finite = finite
+
+    def _s(self):
+        return self._w._native_state()
+
+    @property
+    def tau_i(self) -> int:
+        return self._s().tau_i
+
+    @property
+    def snap_idx(self) -> int:
+        return self._s().snap_idx
+
+    @property
+    def local_clock(self) -> int:
+        return self._s().local_clock
+
+    @property
+    def global_clock(self) -> int:
+        return self._s().global_clock
+
+    @property
+    def x_snapshot(self) -> torch.Tensor:
+        return self.snapshots[self.snap_idx]
+
+    @property
+    def nonfinite_counter(self):
+        return self._finite.counter
+
+    def check_finite(self) -> None:
+        self._finite.check(self.x_local.numel())
 
 
 class LASGDWorker:
@@ -44,185 +87,120 @@ class LASGDWorker:
                  lr: Optional[float] = None, adaptive: bool = False, tau_max: Optional[int] = None,
                  algo: int = N.ALGO_AUTO, compute_stream: Optional[torch.cuda.Stream] = None, sync: bool = True,
                  timed: bool = False, check_finite: str = "lazy", max_host_lead: int = 2,
-                 pipeline: str = "overlap", fused_nblocks: int = 0):
+                 pipeline: str = "overlap", fused_nblocks: int = 0, check_every: int = 16):
         if (schedule is None) == (lr is None):
             raise ValueError("give exactly one of schedule / lr")
-        if sync_period < 1:
-            raise ValueError("sync_period must be >= 1")
-        if not 0.0 < alpha <= 1.0:
-            raise ValueError("alpha must be in (0, 1]")
         if mode not in ("pull", "delta"):
             raise ValueError("mode must be 'pull' or 'delta'")
         if pipeline not in ("overlap", "fused"):
             raise ValueError("pipeline must be 'overlap' or 'fused'")
-        if pipeline == "fused" and adaptive:
-            raise ValueError("the fused pipeline implements the deterministic schedule only")
-        self.pipeline = pipeline
-        self.fused_nblocks = fused_nblocks
+        if check_finite not in ("lazy", "eager", "off"):
+            raise ValueError("check_finite must be 'lazy', 'eager' or 'off'")
+        sgd = sgd or SgdConfig()
+        sgd.validate()
+        K._check(x, g)
         self.comm = comm
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
         self.k = sync_period
-        self.alpha = alpha
-        self.mode = mode
         self.schedule, self.lr = schedule, lr
-        self.adaptive = adaptive
-        self.tau_max = tau_max if tau_max is not None else sync_period
-        self.algo = algo
-        self.sync = sync
+        self.pipeline = pipeline
         self.timed = timed
         self.g = g
         self.compute = compute_stream if compute_stream is not None else torch.cuda.current_stream(x.device)
+        self._local_clock = 0
+        self._rounds = 0
+        self._check_mode = check_finite
+        self._check_every = max(1, check_every)
         snaps = comm.snapshots if comm is not None else [torch.empty_like(x), torch.empty_like(x)]
         delta = torch.zeros_like(x) if mode == "delta" else None
-        self.state = NodeState(self.rank, x, snaps, delta, sgd=sgd, check_finite=check_finite)
+        mbuf = torch.empty_like(x) if sgd.momentum != 0 else None
+        finite = _FiniteMonitor(x.device)
+        self.state = WorkerState(self, x, snaps, delta, mbuf, finite)
         self.xbar = comm.xbar if comm is not None else None
-        self.seq = 0
-        self.launches = collections.Counter()
-        self.records = []  # (name, start_event, end_event)
-        self.tau_hist = collections.Counter()
-        self._lead = collections.deque()
-        self._max_lead = max_host_lead
-        with torch.cuda.stream(self.compute):
-            self._launch("snapshot", self.compute, lambda: K.snapshot(self.state.snapshots[0], x))
-            if self.sync and self.world > 1 and pipeline == "overlap":
-                self._submit(0)
-
-    # ------------------------------------------------------------------ helpers
-    def _launch(self, name: str, stream, fn) -> None:
-        if self.timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            fn()
-            e1.record(stream)
-            self.records.append((name, e0, e1))
-        else:
-            fn()
-        self.launches[name] += 1
-
-    def _submit(self, slot: int) -> None:
-        self.comm.stream.wait_stream(self.compute)
-        box = {}
-        self._launch("allreduce", self.comm.stream, lambda: box.setdefault("s", self.comm.allreduce(slot, self.algo)))
-        self.seq = box["s"]
-
-    def current_lr(self) -> float:
-        return self.lr if self.schedule is None else lr_at(self.schedule, self.state.local_clock)
+        cfg = N.WorkerConfig(sync_period, float(alpha), 1 if mode == "delta" else 0, 1 if pipeline == "fused" else 0,
+                             int(algo), int(fused_nblocks), float(sgd.momentum), float(sgd.dampening),
+                             float(sgd.weight_decay), int(sgd.nesterov), int(bool(sync)), int(bool(adaptive)),
+                             int(tau_max or 0), int(max_host_lead))
+        side = comm.stream if comm is not None else None
+        h = ctypes.c_void_p()
+        ptr = K._ptr
+        N.check(N.lib().lasgd_worker_create(
+            comm._h if comm is not None else None, ptr(x), ptr(mbuf), ptr(delta),
+            None if comm is not None else ptr(snaps[0]), None if comm is not None else ptr(snaps[1]),
+            x.numel(), K.dtype_code(x), ctypes.byref(cfg), ctypes.c_void_p(self.compute.cuda_stream),
+            ctypes.c_void_p(side.cuda_stream) if side is not None else None,
+            None if check_finite == "off" else ptr(finite.counter), ctypes.byref(h)), "lasgd_worker_create")
+        self._h = h
+        self._keep = (x, g, snaps, delta, mbuf, finite)  # buffers the native worker points into
+        if timed:
+            N.check(N.lib().lasgd_worker_set_timing(self._h, 1))
 
     # ------------------------------------------------------------------ protocol
+    def current_lr(self) -> float:
+        return self.lr if self.schedule is None else lr_at(self.schedule, self._local_clock)
+
     def step(self) -> bool:
-        """One local step from the gradient already in ``g`` (call on the compute
-        stream after backward).  Returns True if this step closed a round."""
-        st = self.state
-        c = st.sgd
-        lr = self.current_lr()
-        if self.pipeline == "fused" and self.sync and st.tau_i + 1 == self.k:
-            self._fused_round(lr)
-            return True
-        self._launch("sgd_step", self.compute, lambda: K.sgd_step(
-            st.x_local, self.g, lr, m=st.momentum_buf, delta=st.delta, momentum=c.momentum, dampening=c.dampening,
-            weight_decay=c.weight_decay, nesterov=c.nesterov, first_step=not st._momentum_started,
-            delta_reset=st._delta_fresh, nonfinite=st.nonfinite_counter, stream=self.compute))
-        st._momentum_started = st.momentum_buf is not None
-        st._delta_fresh = False
-        st.tau_i += 1
-        st.local_clock += 1
-        if not self.sync:
-            return False
-        if self.adaptive:
-            self._throttle()
-            done = self.world == 1 or self.comm.query(self.seq) == 1
-            if done or st.tau_i >= self.tau_max:
-                self._round()
-                return True
-            return False
-        if st.tau_i == self.k:
-            self._round()
+        """One local step from the gradient in ``self.g`` (call on the compute stream
+        after backward).  Returns True if this step closed a round."""
+        rc = N.lib().lasgd_worker_step(self._h, self.g.data_ptr(), self.current_lr())
+        if rc < 0:
+            N.check(rc, "lasgd_worker_step")
+        self._local_clock += 1
+        if self._check_mode == "eager":
+            self.state.check_finite()
+        if rc == 1:
+            self._rounds += 1
+            if self._check_mode == "lazy" and self._rounds % self._check_every == 0:
+                with torch.cuda.stream(self.compute):
+                    self.state._finite.poll(self.state.x_local.numel())
             return True
         return False
 
-    def _fused_round(self, lr: float) -> None:
-        st = self.state
-        c = st.sgd
-        cur, nxt = st.snap_idx, 1 - st.snap_idx
-        mode = 1 if (self.mode == "delta" and self.alpha == 1.0) else 0
-        kw = dict(momentum=c.momentum, dampening=c.dampening, weight_decay=c.weight_decay, nesterov=c.nesterov,
-                  first_step=not st._momentum_started, delta_reset=st._delta_fresh, alpha=self.alpha, mode=mode,
-                  nonfinite=st.nonfinite_counter)
-        self.tau_hist[st.tau_i + 1] += 1
-        if self.world == 1:
-            # P == 1 (optimizer.py:168-169): local step + snapshot in one pass, no mean
-            self._launch("fused_round", self.compute, lambda: K.fused_round_virtual(
-                [st.x_local], [self.g], [st.snapshots[cur]], [st.snapshots[nxt]], lr,
-                ms=None if st.momentum_buf is None else [st.momentum_buf],
-                deltas=None if st.delta is None else [st.delta], nblocks=self.fused_nblocks, stream=self.compute,
-                **kw))
-        else:
-            box = {}
-            self._launch("fused_round", self.compute, lambda: box.setdefault("s", self.comm.fused_round(
-                cur, st.x_local, self.g, lr, m=st.momentum_buf, delta=st.delta, algo=self.algo,
-                nblocks=self.fused_nblocks,
-                stream=self.compute, **kw)))
-            self.seq = box["s"]
-        st._momentum_started = st.momentum_buf is not None
-        st._delta_fresh = st.delta is not None
-        st.snap_idx = nxt
-        st.tau_i = 0
-        st.local_clock += 1
-        st.global_clock += 1
-        if st.check_mode == "lazy":
-            with torch.cuda.stream(self.compute):
-                st._finite.poll(st.x_local.numel())
-
-    def _throttle(self) -> None:
-        ev = torch.cuda.Event()
-        ev.record(self.compute)
-        self._lead.append(ev)
-        while len(self._lead) > self._max_lead:
-            self._lead.popleft().synchronize()
-
-    def _round(self) -> None:
-        st = self.state
-        nxt = 1 - st.snap_idx
-        x = st.x_local
-        self.tau_hist[st.tau_i] += 1
-        if self.world == 1:
-            # optimizer.py:168-169: P == 1 keeps the live model; only the snapshot moves
-            self._launch("snapshot", self.compute, lambda: K.snapshot(st.snapshots[nxt], x, stream=self.compute))
-        else:
-            self.comm.stream_wait(self.seq, self.compute)
-            if self.mode == "delta" and self.alpha == 1.0:
-                self._launch("finalize", self.compute, lambda: K.finalize(
-                    x, self.xbar, st.delta, snap_next=st.snapshots[nxt], nonfinite=st.nonfinite_counter,
-                    stream=self.compute))
-            else:
-                cur = st.snapshots[st.snap_idx]
-                self._launch("pull", self.compute, lambda: K.elastic_pull(
-                    x, cur, self.xbar, self.alpha, snap_next=st.snapshots[nxt], nonfinite=st.nonfinite_counter,
-                    stream=self.compute))
-        st.snap_idx = nxt
-        st._delta_fresh = st.delta is not None
-        st.tau_i = 0
-        st.global_clock += 1
-        if st.check_mode == "lazy":
-            with torch.cuda.stream(self.compute):
-                st._finite.poll(x.numel())
-        if self.world > 1:
-            self._submit(nxt)
-
     def drain(self) -> None:
         """Order the compute stream after the in-flight all-reduce."""
-        if self.world > 1 and self.seq and self.pipeline == "overlap":
-            self.comm.stream_wait(self.seq, self.compute)
+        N.check(N.lib().lasgd_worker_drain(self._h), "lasgd_worker_drain")
 
-    # ------------------------------------------------------------------ measurement
+    # ------------------------------------------------------------------ state / measurement
+    def _native_state(self) -> N.WorkerState:
+        s = N.WorkerState()
+        N.check(N.lib().lasgd_worker_get_state(self._h, ctypes.byref(s)))
+        return s
+
+    @property
+    def seq(self) -> int:
+        return self._native_state().seq
+
+    @property
+    def launches(self) -> collections.Counter:
+        s = self._native_state()
+        return collections.Counter({k: s.launches[i] for i, k in enumerate(N.KERNEL_KINDS) if s.launches[i]})
+
+    @property
+    def tau_hist(self) -> collections.Counter:
+        s = self._native_state()
+        return collections.Counter({t: s.tau_hist[t] for t in range(N.TAU_HIST) if s.tau_hist[t]})
+
     def kernel_times(self) -> dict:
-        """Per-kernel list of durations (ms) of the timed launches (after a sync)."""
-        out = collections.defaultdict(list)
-        for name, e0, e1 in self.records:
-            out[name].append(e0.elapsed_time(e1))
-        return dict(out)
+        """Per-kernel durations (ms) of the timed launches (call after a sync)."""
+        out = {}
+        for i, name in enumerate(N.KERNEL_KINDS):
+            buf = (ctypes.c_float * 65536)()
+            k = N.check(N.lib().lasgd_worker_timings(self._h, i, buf, 65536))
+            if k:
+                out[name] = list(buf[:k])
+        return out
 
     def reset_records(self) -> None:
-        self.records.clear()
-        self.launches.clear()
+        N.check(N.lib().lasgd_worker_reset_stats(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.lib().lasgd_worker_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

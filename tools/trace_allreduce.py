@@ -39,6 +39,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes-mb", default="16,102.228128,1024")
     ap.add_argument("--nblocks", default="64,128")
+    ap.add_argument("--fused", action="store_true", help="trace the fused round kernel (K7) instead of K2/K3")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -50,16 +51,26 @@ def main():
         comm = L.P2PCommunicator(n, timeout_s=60.0)
         comm.snapshots[0].normal_()
         comm.snapshots[1].normal_()
+        xs, gs, ms = (torch.randn(n, device=dev) for _ in range(3))
+        slot = [0]
+
+        def launch(algo, nb):
+            if not a.fused:
+                return comm.allreduce(slot[0], algo, stream=s)
+            r = comm.fused_round(slot[0], xs, gs, 0.01, m=ms, momentum=0.9, weight_decay=1e-4, nesterov=True,
+                                 algo=algo, nblocks=nb, stream=s)
+            slot[0] ^= 1
+            return r
         for nb in [int(v) for v in a.nblocks.split(",")]:
             comm.set_nblocks(nb)
             for algo in (N.ALGO_ONESHOT, N.ALGO_TWOSHOT):
                 with torch.cuda.stream(s):
                     for i in range(4):
-                        comm.allreduce(i % 2, algo, stream=s)
+                        launch(algo, nb)
                     torch.cuda.synchronize()
                     dist.barrier()
                     comm.set_trace(True)
-                    comm.allreduce(0, algo, stream=s)
+                    launch(algo, nb)
                     torch.cuda.synchronize()
                     comm.set_trace(False)
                 tr = comm.read_trace()
