@@ -60,6 +60,7 @@ struct CommArgs {
   unsigned long long seq;
   unsigned long long* nonfinite;
   unsigned long long* trace;  // optional per-CTA timeline: [b][0..3] = start, entry passed, mid passed, end
+  unsigned long long* tile_ctr;  // one-shot work queue of this launch (nullptr: static slices)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer();
@@ -175,6 +176,7 @@ __device__ void publish_done(const CommArgs& a) {
     const unsigned prev = atomicAdd(&a.done_ctr[slot], 1u);
     if (prev == (unsigned)a.nblocks - 1u) {
       a.done_ctr[slot] = 0u;
+      if (a.tile_ctr) *a.tile_ctr = 0ull;  // every CTA has left its tile loop
       __threadfence_system();
       st_release_sys64(a.done_seq, a.seq);
     }
@@ -209,6 +211,38 @@ __device__ __forceinline__ void chunk_slice(size_t cs, size_t ce, int nb, int b,
   p1 = as / W + p1;
 }
 
+// Work distribution of the one-shot kernels over packs [0, npack): with a launch work
+// queue (P2P launches) CTAs take tiles of TILE_ITERS*U*blockDim packs from an atomic
+// counter, the next index fetched while the current tile streams, so fast CTAs absorb
+// the tail; otherwise (virtual ranks) CTA b takes the b-th even slice.  Every CTA has
+// passed its entry barrier before it takes a tile, so the double-buffer argument is
+// unchanged (it only needs every CTA to wait for its peers' same-index CTA).
+constexpr int kTileIters = 2;
+
+template <int U, typename F>
+__device__ __forceinline__ void for_tiles(const CommArgs& a, int b, size_t npack, F&& range) {
+  if (a.tile_ctr == nullptr) {
+    size_t p0, p1;
+    split(npack, a.nblocks, b, p0, p1);
+    range(p0, p1);
+    return;
+  }
+  __shared__ unsigned long long s_next;
+  const size_t tile = (size_t)kTileIters * U * blockDim.x;
+  const unsigned long long ntiles = (npack + tile - 1) / tile;
+  if (threadIdx.x == 0) s_next = atomicAdd(a.tile_ctr, 1ull);
+  __syncthreads();
+  unsigned long long t = s_next;
+  while (t < ntiles) {
+    __syncthreads();  // everyone has read s_next
+    if (threadIdx.x == 0) s_next = atomicAdd(a.tile_ctr, 1ull);  // prefetch the next index
+    const size_t p0 = (size_t)t * tile;
+    range(p0, p0 + tile < npack ? p0 + tile : npack);
+    __syncthreads();
+    t = s_next;
+  }
+}
+
 // ------------------------------------------------------------------ one-shot (K2)
 template <typename T, int P, bool VIRTUAL, int U>
 __global__ void __launch_bounds__(256, 2) k_oneshot(CommArgs a) {
@@ -229,8 +263,7 @@ __global__ void __launch_bounds__(256, 2) k_oneshot(CommArgs a) {
 #pragma unroll
     for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
     T* out = reinterpret_cast<T*>(a.xbar[rank]);
-    size_t p0, p1;
-    split(n / W, a.nblocks, b, p0, p1);
+    auto range = [&](size_t p0, size_t p1) {
     for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
       Pack<T> v[U][P];
 #pragma unroll
@@ -261,6 +294,8 @@ __global__ void __launch_bounds__(256, 2) k_oneshot(CommArgs a) {
         }
       }
     }
+    };
+    for_tiles<U>(a, b, n / W, range);
     if (b == a.nblocks - 1) {  // scalar tail n % W
       for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
         T lane[P];
@@ -447,8 +482,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_round(CommArgs a, FusedRound<T
       bad += bb;
       return xv;
     };
-    size_t p0, p1;
-    split(n / W, a.nblocks, b, p0, p1);
+    auto range = [&](size_t p0, size_t p1) {
     for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
       Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U][P];
 #pragma unroll
@@ -487,6 +521,8 @@ __global__ void __launch_bounds__(256, 2) k_fused_round(CommArgs a, FusedRound<T
         }
       }
     }
+    };
+    for_tiles<U>(a, b, n / W, range);
     if (b == a.nblocks - 1) {  // scalar tail n % W
       for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
         T lane[P];
@@ -819,7 +855,8 @@ extern "C" int lasgd_fused_round_virtual(int P, int algo, void* const* x, const 
   if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   if (algo == LASGD_ALGO_TWOSHOT && !xbars) return fail(LASGD_ERR_INVALID_ARGUMENT, "two-shot needs per-rank mean buffers");
   if (n == 0) return LASGD_OK;
-  if (nblocks <= 0) nblocks = 2 * num_sms();
+  // P == 1 (local step + snapshot) needs ~60 registers: 4 CTAs per SM; otherwise 2
+  if (nblocks <= 0) nblocks = (P == 1 ? 4 : 2) * num_sms();
   CommArgs a;
   memset(&a, 0, sizeof(a));
   for (int q = 0; q < P; ++q) {
@@ -867,6 +904,7 @@ struct lasgd_comm {
   unsigned long long* done_host = nullptr;
   unsigned long long* done_dev = nullptr;
   unsigned int* done_ctr = nullptr;
+  unsigned long long* tile_ctr = nullptr;  // [kDoneSlots] one-shot work queues
   unsigned long long* trace_buf = nullptr;  // [kMaxB][4] globaltimer stamps of the last traced launch
   bool trace_on = false;
   unsigned long long seq = 0;  // launches issued
@@ -926,6 +964,8 @@ extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int 
     e = cudaHostGetDevicePointer((void**)&c->status_dev, c->status_host, 0);
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->done_ctr, kDoneSlots * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->tile_ctr, kDoneSlots * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->tile_ctr, 0, kDoneSlots * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->done_ctr, 0, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMalloc(&c->trace_buf, (size_t)kMaxB * 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->trace_buf, 0, (size_t)kMaxB * 4 * sizeof(unsigned long long));
@@ -1055,6 +1095,7 @@ static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned lo
   }
   a.status = c->status_dev;
   a.done_ctr = c->done_ctr;
+  a.tile_ctr = c->tile_ctr + (s % kDoneSlots);
   a.done_seq = c->done_dev;
   a.seq = s;
   a.nonfinite = nullptr;
@@ -1191,6 +1232,7 @@ extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
     if (r != c->rank && c->peer_base[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
   for (int i = 0; i < c->nev; ++i) cudaEventDestroy(c->ev[i]);
   if (c->done_ctr) cudaFree(c->done_ctr);
+  if (c->tile_ctr) cudaFree(c->tile_ctr);
   if (c->trace_buf) cudaFree(c->trace_buf);
   if (c->status_host) cudaFreeHost(c->status_host);
   if (c->base) cudaFree(c->base);
