@@ -34,7 +34,7 @@ namespace lasgd {
 
 constexpr int kMaxR = LASGD_MAX_RANKS;
 constexpr int kMaxB = LASGD_MAX_BLOCKS;  // flag slots per phase and rank
-constexpr int kPhases = 2;
+constexpr int kPhases = 3;  // 0 entry (per CTA), 1 mid (per CTA), 2 rank-level mid
 constexpr size_t kPadBytes = (size_t)kPhases * kMaxB * kMaxR * sizeof(uint32_t);
 constexpr int kDoneSlots = 64;
 constexpr int kEvents = 64;
@@ -60,7 +60,8 @@ struct CommArgs {
   unsigned long long seq;
   unsigned long long* nonfinite;
   unsigned long long* trace;  // optional per-CTA timeline: [b][0..3] = start, entry passed, mid passed, end
-  unsigned long long* tile_ctr;  // one-shot work queue of this launch (nullptr: static slices)
+  unsigned long long* tile_ctr;  // two work queues of this launch (nullptr: static slices)
+  unsigned int* mid_ctr;         // CTAs of this rank past the reduce-scatter (rank-level barrier)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer();
@@ -176,7 +177,7 @@ __device__ void publish_done(const CommArgs& a) {
     const unsigned prev = atomicAdd(&a.done_ctr[slot], 1u);
     if (prev == (unsigned)a.nblocks - 1u) {
       a.done_ctr[slot] = 0u;
-      if (a.tile_ctr) *a.tile_ctr = 0ull;  // every CTA has left its tile loop
+      if (a.tile_ctr) a.tile_ctr[0] = a.tile_ctr[1] = 0ull;  // every CTA has left its tile loops
       __threadfence_system();
       st_release_sys64(a.done_seq, a.seq);
     }
@@ -192,25 +193,6 @@ __device__ __forceinline__ void split(size_t npack, int nb, int b, size_t& p0, s
   if (p1 > npack) p1 = npack;
 }
 
-// Slice b of chunk [cs, ce): 16-byte-aligned body split over CTAs, the unaligned
-// head goes to CTA 0 and the tail to the last CTA (identical on every rank).
-template <typename T>
-__device__ __forceinline__ void chunk_slice(size_t cs, size_t ce, int nb, int b, size_t& h0, size_t& h1, size_t& p0,
-                                            size_t& p1, size_t& t0, size_t& t1) {
-  constexpr int W = Pack<T>::W;
-  size_t as = (cs + W - 1) / W * W, ae = ce / W * W;
-  if (as > ae || ae - as < (size_t)W) {  // tiny chunk: all scalar on CTA 0
-    h0 = cs; h1 = (b == 0) ? ce : cs;
-    p0 = p1 = 0; t0 = t1 = 0;
-    return;
-  }
-  h0 = cs; h1 = (b == 0) ? as : cs;
-  t0 = ae; t1 = (b == nb - 1) ? ce : ae;
-  split((ae - as) / W, nb, b, p0, p1);
-  p0 = as / W + p0;
-  p1 = as / W + p1;
-}
-
 // Work distribution of the one-shot kernels over packs [0, npack): with a launch work
 // queue (P2P launches) CTAs take tiles of TILE_ITERS*U*blockDim packs from an atomic
 // counter, the next index fetched while the current tile streams, so fast CTAs absorb
@@ -219,28 +201,87 @@ __device__ __forceinline__ void chunk_slice(size_t cs, size_t ce, int nb, int b,
 // unchanged (it only needs every CTA to wait for its peers' same-index CTA).
 constexpr int kTileIters = 2;
 
-template <int U, typename F>
-__device__ __forceinline__ void for_tiles(const CommArgs& a, int b, size_t npack, F&& range) {
-  if (a.tile_ctr == nullptr) {
+// Tiles of `tile` packs over [base, base + npack): from the atomic queue `ctr` when
+// given (next index prefetched while the current tile streams), else a contiguous
+// even slice per CTA.
+template <typename F>
+__device__ __forceinline__ void tile_loop(unsigned long long* ctr, int b, int nblocks, size_t base, size_t npack,
+                                          size_t tile, F&& range) {
+  if (npack == 0) return;
+  if (ctr == nullptr) {
     size_t p0, p1;
-    split(npack, a.nblocks, b, p0, p1);
-    range(p0, p1);
+    split(npack, nblocks, b, p0, p1);
+    if (p0 < p1) range(base + p0, base + p1);
     return;
   }
   __shared__ unsigned long long s_next;
-  const size_t tile = (size_t)kTileIters * U * blockDim.x;
   const unsigned long long ntiles = (npack + tile - 1) / tile;
-  if (threadIdx.x == 0) s_next = atomicAdd(a.tile_ctr, 1ull);
+  __syncthreads();
+  if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);
   __syncthreads();
   unsigned long long t = s_next;
   while (t < ntiles) {
     __syncthreads();  // everyone has read s_next
-    if (threadIdx.x == 0) s_next = atomicAdd(a.tile_ctr, 1ull);  // prefetch the next index
+    if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);  // prefetch the next index
     const size_t p0 = (size_t)t * tile;
-    range(p0, p0 + tile < npack ? p0 + tile : npack);
+    range(base + p0, base + (p0 + tile < npack ? p0 + tile : npack));
     __syncthreads();
     t = s_next;
   }
+}
+
+template <int U, typename F>
+__device__ __forceinline__ void for_tiles(const CommArgs& a, int b, size_t npack, F&& range) {
+  tile_loop(a.tile_ctr, b, a.nblocks, 0, npack, (size_t)kTileIters * U * blockDim.x, range);
+}
+
+// Rank-level barrier between the two phases of the two-shot kernels: every CTA of this
+// rank counts itself in; the last one signals every peer (after every CTA's
+// __threadfence_system, so all reduce-scatter stores are visible system-wide); then
+// all CTAs wait for every peer's signal.  Requires all CTAs co-resident: the P2P
+// two-shot kernels are launched cooperatively.
+template <int P>
+__device__ bool rank_barrier(const CommArgs& a, int b, int rank) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned prev = atomicAdd(a.mid_ctr, 1u);
+    s_last = prev == (unsigned)a.nblocks - 1u;
+    if (s_last) *a.mid_ctr = 0u;  // every CTA of this launch has counted itself in
+  }
+  __syncthreads();
+  const size_t slot = (size_t)2 * kMaxB * kMaxR;
+  if (s_last && threadIdx.x < P && a.skip_signal_phase != 1) {
+    __threadfence_system();
+    st_release_sys(a.pad[threadIdx.x] + slot + rank, a.epoch);
+  }
+  int ok = 1;
+  if (threadIdx.x < P) {
+    const int q = threadIdx.x;
+    const uint32_t* f = a.pad[rank] + slot + q;
+    const unsigned long long t0 = globaltimer();
+    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+      if ((long long)(globaltimer() - t0) > a.timeout_ns) {
+        report_failure(a, ERR_TIMEOUT, q, 1, b, rank);
+        ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  return __syncthreads_and(ok) != 0;
+}
+
+// Aligned body of chunk c in packs, [cp0, cp1), plus its unaligned head/tail elements.
+template <typename T, int P>
+__device__ __forceinline__ void chunk_packs(size_t n, int c, size_t& cs, size_t& ce, size_t& cp0, size_t& cp1) {
+  constexpr int W = Pack<T>::W;
+  cs = chunk_bound(n, P, c);
+  ce = chunk_bound(n, P, c + 1);
+  cp0 = (cs + W - 1) / W;
+  cp1 = ce / W;
+  if (cp1 < cp0) cp1 = cp0;
 }
 
 // ------------------------------------------------------------------ one-shot (K2)
@@ -321,6 +362,66 @@ __device__ __forceinline__ T ordered_sum(const T* const (&src)[P], int rank, siz
   return rot_sum<T, P>(v, rank);
 }
 
+// Reduce-scatter of this rank's chunk (ring order x_rank, x_rank+1, ..., x_rank-1)
+// into its xbar buffer: aligned packs from work queue 0, head/tail elements on CTA 0.
+template <typename T, int P, int U>
+__device__ __forceinline__ unsigned reduce_own_chunk(const CommArgs& a, int b, int rank, unsigned long long* q0) {
+  constexpr int W = Pack<T>::W;
+  const size_t n = a.n;
+  unsigned bad = 0;
+  T* own = reinterpret_cast<T*>(a.xbar[rank]);
+  const T* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
+  size_t cs, ce, cp0, cp1;
+  chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
+  auto range = [&](size_t p0, size_t p1) {
+    for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+      Pack<T> v[U][P];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t pu = p + (size_t)u * blockDim.x;
+        if (pu < p1) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t pu = p + (size_t)u * blockDim.x;
+        if (pu < p1) {
+          Pack<T> o;
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            T lane[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+            o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+            bad += !finite(o.v[k]);
+          }
+          st_plain(own + pu * W, o);
+        }
+      }
+    }
+  };
+  tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, range);
+  if (b == 0) {  // unaligned head / tail of the chunk (and tiny chunks)
+    const size_t hs = cs, he = cp0 * W < ce ? cp0 * W : ce;
+    const size_t ts = cp1 * W > hs ? (cp1 * W > he ? cp1 * W : he) : he;
+    for (size_t j = hs + threadIdx.x; j < he; j += blockDim.x) {
+      T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+      own[j] = r;
+      bad += !finite(r);
+    }
+    for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) {
+      T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+      own[j] = r;
+      bad += !finite(r);
+    }
+  }
+  return bad;
+}
+
 template <typename T, int P, bool VIRTUAL, int U, int UAG>
 __global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
   constexpr int W = Pack<T>::W;
@@ -330,83 +431,57 @@ __global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
   bool ok = true;
   unsigned bad = 0;
   T* out = reinterpret_cast<T*>(a.xbar[rank]);
+  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
+  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
   trace_mark(a, b, 0);
   if (a.phases & 1) {
     if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
     trace_mark(a, b, 1);
-    if (ok) {
-      // reduce-scatter: this rank owns chunk `rank` and sums it in ring order
-      // x_rank, x_rank+1, ..., x_rank-1 (the order the reference ring produces).
-      const T* src[P];
-#pragma unroll
-      for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
-      size_t h0, h1, p0, p1, t0, t1;
-      chunk_slice<T>(chunk_bound(n, P, rank), chunk_bound(n, P, rank + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
-      for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-        Pack<T> v[U][P];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const size_t pu = p + (size_t)u * blockDim.x;
-          if (pu < p1) {
-#pragma unroll
-            for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const size_t pu = p + (size_t)u * blockDim.x;
-          if (pu < p1) {
-            Pack<T> o;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-              T lane[P];
-#pragma unroll
-              for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
-              o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
-              bad += !finite(o.v[k]);
-            }
-            st_plain(out + pu * W, o);
-          }
-        }
-      }
-      for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) {
-        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
-        out[j] = r;
-        bad += !finite(r);
-      }
-      for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) {
-        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
-        out[j] = r;
-        bad += !finite(r);
-      }
-    }
+    if (ok) bad += reduce_own_chunk<T, P, U>(a, b, rank, q0);
   }
   if (a.phases & 2) {
-    if (!VIRTUAL && ok) ok = cta_barrier<P>(a, 1, b, rank);
+    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
     trace_mark(a, b, 2);
     if (ok) {
-      // all-gather: pull slice b of every other rank's reduced chunk.
-#pragma unroll 1
-      for (int d = 1; d < P; ++d) {
-        const int q = (rank + d) % P;
-        const T* peer = reinterpret_cast<const T*>(a.xbar[q]);
-        size_t h0, h1, p0, p1, t0, t1;
-        chunk_slice<T>(chunk_bound(n, P, q), chunk_bound(n, P, q + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
+      // all-gather: every pack outside the own chunk comes from its owner's xbar
+      size_t bnd[P + 1];
+#pragma unroll
+      for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
+      auto range = [&](size_t p0, size_t p1) {
         for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)UAG * blockDim.x) {
           Pack<T> v[UAG];
+          int own[UAG];
 #pragma unroll
           for (int u = 0; u < UAG; ++u) {
             const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) v[u] = ld_cg(peer + pu * W);
+            own[u] = -1;
+            if (pu < p1) {
+              const int c0 = chunk_of<P>(pu * W, bnd), c1 = chunk_of<P>(pu * W + W - 1, bnd);
+              own[u] = c0 == c1 ? c0 : P;  // P marks a pack straddling two chunks
+              if (c0 == c1 && c0 != rank) v[u] = ld_cg(reinterpret_cast<const T*>(a.xbar[c0]) + pu * W);
+            }
           }
 #pragma unroll
           for (int u = 0; u < UAG; ++u) {
             const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) st_stream(out + pu * W, v[u]);
+            if (own[u] >= 0 && own[u] < P && own[u] != rank) {
+              st_stream(out + pu * W, v[u]);
+            } else if (own[u] == P) {
+              for (int k = 0; k < W; ++k) {
+                const size_t j = pu * W + k;
+                const int c = chunk_of<P>(j, bnd);
+                if (c != rank) out[j] = reinterpret_cast<const T*>(a.xbar[c])[j];
+              }
+            }
           }
         }
-        for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) out[j] = peer[j];
-        for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) out[j] = peer[j];
+      };
+      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * UAG * blockDim.x, range);
+      if (b == a.nblocks - 1) {
+        for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
+          const int c = chunk_of<P>(j, bnd);
+          if (c != rank) out[j] = reinterpret_cast<const T*>(a.xbar[c])[j];
+        }
       }
     }
   }
@@ -542,12 +617,12 @@ __global__ void __launch_bounds__(256, 2) k_fused_round(CommArgs a, FusedRound<T
   if (!VIRTUAL) publish_done(a);
 }
 
-// Two-shot form of K7 for larger P: (1) reduce-scatter of this rank's chunk slice into
-// its xbar buffer (ring order, same as K3), (2) per-CTA mid barrier, (3) for every chunk
-// q, slice b: local step + pull with chunk q's mean read straight from its owner's
-// xbar over NVLink (own chunk: local), next snapshot.  NVLink in-bytes 2(P-1)/P*B; xbar
-// is written only for the own chunk.  Phase bits as in k_twoshot (virtual ranks run
-// phase 1 and phase 2 as two launches).
+// Two-shot form of K7 for larger P: (1) reduce-scatter of this rank's chunk into its
+// xbar buffer (ring order, same as K3), (2) rank-level mid barrier, (3) over every
+// pack: local step + pull with the pack's mean read straight from its owner's xbar
+// (NVLink unless the pack is in the own chunk), next snapshot.  NVLink in-bytes
+// 2(P-1)/P*B; xbar is written only for the own chunk.  Both phases take tiles from
+// work queues.  Virtual ranks run phase 1 and phase 2 as two launches.
 template <typename T, int P, bool VIRTUAL, int U>
 __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound<T> f) {
   constexpr int W = Pack<T>::W;
@@ -557,58 +632,16 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
   const size_t n = a.n;
   bool ok = true;
   unsigned bad = 0;
-  T* own_xbar = reinterpret_cast<T*>(a.xbar[rank]);
+  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
+  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
   trace_mark(a, b, 0);
   if (a.phases & 1) {
     if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
     trace_mark(a, b, 1);
-    if (ok) {
-      const T* src[P];
-#pragma unroll
-      for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
-      size_t h0, h1, p0, p1, t0, t1;
-      chunk_slice<T>(chunk_bound(n, P, rank), chunk_bound(n, P, rank + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
-      for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-        Pack<T> v[U][P];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const size_t pu = p + (size_t)u * blockDim.x;
-          if (pu < p1) {
-#pragma unroll
-            for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const size_t pu = p + (size_t)u * blockDim.x;
-          if (pu < p1) {
-            Pack<T> o;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-              T lane[P];
-#pragma unroll
-              for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
-              o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
-              bad += !finite(o.v[k]);
-            }
-            st_plain(own_xbar + pu * W, o);
-          }
-        }
-      }
-      for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) {
-        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
-        own_xbar[j] = r;
-        bad += !finite(r);
-      }
-      for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) {
-        T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
-        own_xbar[j] = r;
-        bad += !finite(r);
-      }
-    }
+    if (ok) bad += reduce_own_chunk<T, P, U>(a, b, rank, q0);
   }
   if (a.phases & 2) {
-    if (!VIRTUAL && ok) ok = cta_barrier<P>(a, 1, b, rank);
+    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
     trace_mark(a, b, 2);
     if (ok) {
       T* const x = f.x[vr];
@@ -619,6 +652,9 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
       const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
       const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
       const bool store_d = f.c.use_delta && f.mode == 0;
+      size_t bnd[P + 1];
+#pragma unroll
+      for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
       auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
         unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
         if (f.mode == 0) {
@@ -629,20 +665,20 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
         }
         bad += bb;
       };
-#pragma unroll 1
-      for (int d = 0; d < P; ++d) {
-        const int q = (rank + d) % P;
-        const T* zq = reinterpret_cast<const T*>(a.xbar[q]);  // owner's reduced chunk (NVLink unless q == rank)
-        size_t h0, h1, p0, p1, t0, t1;
-        chunk_slice<T>(chunk_bound(n, P, q), chunk_bound(n, P, q + 1), a.nblocks, b, h0, h1, p0, p1, t0, t1);
+      auto mean_at = [&](size_t j) { return reinterpret_cast<const T*>(a.xbar[chunk_of<P>(j, bnd)])[j]; };
+      auto range = [&](size_t p0, size_t p1) {
         for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
           Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
+          int own[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const size_t pu = p + (size_t)u * blockDim.x;
+            own[u] = -1;
             if (pu < p1) {
               const size_t j = pu * W;
-              vz[u] = ld_cg(zq + j);
+              const int c0 = chunk_of<P>(j, bnd), c1 = chunk_of<P>(j + W - 1, bnd);
+              own[u] = c0 == c1 ? c0 : P;
+              if (c0 == c1) vz[u] = ld_cg(reinterpret_cast<const T*>(a.xbar[c0]) + j);
               vx[u] = ld_stream(x + j);
               vg[u] = ld_stream(g + j);
               if (load_m) vm[u] = ld_stream(m + j);
@@ -653,8 +689,12 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) {
+            if (own[u] >= 0) {
               const size_t j = pu * W;
+              if (own[u] == P) {
+#pragma unroll
+                for (int k = 0; k < W; ++k) vz[u].v[k] = mean_at(j + k);
+              }
 #pragma unroll
               for (int k = 0; k < W; ++k) element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
               st_stream(x + j, vx[u]);
@@ -664,16 +704,17 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
             }
           }
         }
-        auto scalar = [&](size_t j) {
+      };
+      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * U * blockDim.x, range);
+      if (b == a.nblocks - 1) {  // scalar tail n % W
+        for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), zq[j]);
+          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), mean_at(j));
           x[j] = xv;
           if (f.c.use_mom) m[j] = mv;
           if (store_d) dl[j] = dv;
           sn[j] = xv;
-        };
-        for (size_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) scalar(j);
-        for (size_t j = t0 + threadIdx.x; j < t1; j += blockDim.x) scalar(j);
+        }
       }
     }
   }
@@ -682,16 +723,47 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
   if (!VIRTUAL) publish_done(a);
 }
 
+// Launch `kernel` normally, or cooperatively (all CTAs co-resident, required by the
+// rank-level barrier of the P2P two-shot kernels).  A cooperative grid is clamped to
+// what fits on the device — every rank computes the same clamp on the same GPU type,
+// so the per-CTA flag slots still line up.
+template <typename... Args>
+int launch_kernel(bool coop, void (*kernel)(Args...), dim3 grid, int threads, cudaStream_t s, Args... args) {
+  if (!coop) {
+    kernel<<<grid, threads, 0, s>>>(args...);
+    LASGD_CUDA_TRY(cudaGetLastError());
+    return LASGD_OK;
+  }
+  void* kargs[] = {(void*)&args...};
+  LASGD_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kernel, grid, dim3(threads), kargs, 0, s));
+  return LASGD_OK;
+}
+
+template <typename... Args>
+int coop_capacity(void (*kernel)(Args...), int threads) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  return per_sm * num_sms();
+}
+
 template <typename T, bool VIRTUAL>
 int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s,
                  int algo = LASGD_ALGO_ONESHOT) {
+  static_assert(sizeof(CommArgs) + sizeof(FusedRound<T>) < 4000, "kernel parameters");
 #define LASGD_FCASE(PP)                                                                             \
   case PP:                                                                                          \
-    if (algo == LASGD_ALGO_TWOSHOT && PP > 1)                                                       \
-      k_fused_twoshot<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)><<<grid, threads, 0, s>>>(a, f);           \
-    else                                                                                            \
-      k_fused_round<T, PP, VIRTUAL, (PP <= 2 ? 2 : 1)><<<grid, threads, 0, s>>>(a, f);             \
-    break;
+    if (algo == LASGD_ALGO_TWOSHOT && PP > 1) {                                                     \
+      auto kern = k_fused_twoshot<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)>;                               \
+      CommArgs aa = a;                                                                              \
+      if (!VIRTUAL) {                                                                               \
+        const int cap = coop_capacity(kern, threads);                                               \
+        if ((int)grid.x > cap) grid.x = cap;                                                        \
+        aa.nblocks = grid.x;                                                                        \
+      }                                                                                             \
+      return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                \
+    }                                                                                               \
+    return launch_kernel(false, k_fused_round<T, PP, VIRTUAL, (PP <= 2 ? 2 : 1)>, grid, threads, s, \
+                         a, f);
   switch (P) {
     LASGD_FCASE(1)
     LASGD_FCASE(2)
@@ -747,16 +819,25 @@ int check_fused_args(int nr, void* const* x, const void* const* g, void* const* 
 // ------------------------------------------------------------------ dispatch
 template <int P>
 constexpr int unroll_for() { return P <= 2 ? 8 : (P <= 4 ? 4 : 2); }
+template <int P>
+constexpr int oneshot_unroll() { return P <= 2 ? 4 : (P <= 4 ? 2 : 1); }  // <= 128 regs, no spills
 
 template <typename T, bool VIRTUAL>
 int launch_allreduce(int algo, int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
 #define LASGD_CASE(PP)                                                                                    \
   case PP:                                                                                                \
-    if (algo == LASGD_ALGO_ONESHOT)                                                                       \
-      k_oneshot<T, PP, VIRTUAL, unroll_for<PP>()><<<grid, threads, 0, s>>>(a);                            \
-    else                                                                                                  \
-      k_twoshot<T, PP, VIRTUAL, unroll_for<PP>(), 8><<<grid, threads, 0, s>>>(a);                         \
-    break;
+    if (algo == LASGD_ALGO_ONESHOT) return launch_kernel(false, k_oneshot<T, PP, VIRTUAL, oneshot_unroll<PP>()>, \
+                                                         grid, threads, s, a);                            \
+    {                                                                                                     \
+      auto kern = k_twoshot<T, PP, VIRTUAL, unroll_for<PP>(), 8>;                                         \
+      CommArgs aa = a;                                                                                    \
+      if (!VIRTUAL) {                                                                                     \
+        const int cap = coop_capacity(kern, threads);                                                     \
+        if ((int)grid.x > cap) grid.x = cap;                                                              \
+        aa.nblocks = grid.x;                                                                              \
+      }                                                                                                   \
+      return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa);                                         \
+    }
   switch (P) {
     LASGD_CASE(1)
     LASGD_CASE(2)
@@ -904,7 +985,8 @@ struct lasgd_comm {
   unsigned long long* done_host = nullptr;
   unsigned long long* done_dev = nullptr;
   unsigned int* done_ctr = nullptr;
-  unsigned long long* tile_ctr = nullptr;  // [kDoneSlots] one-shot work queues
+  unsigned long long* tile_ctr = nullptr;  // [kDoneSlots][2] work queues
+  unsigned int* mid_ctr = nullptr;         // [kDoneSlots] rank-level barrier counters
   unsigned long long* trace_buf = nullptr;  // [kMaxB][4] globaltimer stamps of the last traced launch
   bool trace_on = false;
   unsigned long long seq = 0;  // launches issued
@@ -964,8 +1046,10 @@ extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int 
     e = cudaHostGetDevicePointer((void**)&c->status_dev, c->status_host, 0);
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->done_ctr, kDoneSlots * sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMalloc(&c->tile_ctr, kDoneSlots * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(c->tile_ctr, 0, kDoneSlots * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->tile_ctr, 2 * kDoneSlots * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->tile_ctr, 0, 2 * kDoneSlots * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->mid_ctr, kDoneSlots * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->mid_ctr, 0, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->done_ctr, 0, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMalloc(&c->trace_buf, (size_t)kMaxB * 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->trace_buf, 0, (size_t)kMaxB * 4 * sizeof(unsigned long long));
@@ -1095,7 +1179,8 @@ static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned lo
   }
   a.status = c->status_dev;
   a.done_ctr = c->done_ctr;
-  a.tile_ctr = c->tile_ctr + (s % kDoneSlots);
+  a.tile_ctr = c->tile_ctr + 2 * (s % kDoneSlots);
+  a.mid_ctr = c->mid_ctr + (s % kDoneSlots);
   a.done_seq = c->done_dev;
   a.seq = s;
   a.nonfinite = nullptr;
@@ -1233,6 +1318,7 @@ extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
   for (int i = 0; i < c->nev; ++i) cudaEventDestroy(c->ev[i]);
   if (c->done_ctr) cudaFree(c->done_ctr);
   if (c->tile_ctr) cudaFree(c->tile_ctr);
+  if (c->mid_ctr) cudaFree(c->mid_ctr);
   if (c->trace_buf) cudaFree(c->trace_buf);
   if (c->status_host) cudaFreeHost(c->status_host);
   if (c->base) cudaFree(c->base);
