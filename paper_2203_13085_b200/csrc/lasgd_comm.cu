@@ -204,14 +204,29 @@ constexpr int kTileIters = 2;
 // Tiles of `tile` packs over [base, base + npack): from the atomic queue `ctr` when
 // given (next index prefetched while the current tile streams), else a contiguous
 // even slice per CTA.
+// `rot` rotates the order in which the packs are visited (logical pack l maps to
+// (l + rot) mod npack): the two-shot all-gather starts every rank at a different
+// owner's chunk so no owner serves all readers at once.
 template <typename F>
 __device__ __forceinline__ void tile_loop(unsigned long long* ctr, int b, int nblocks, size_t base, size_t npack,
-                                          size_t tile, F&& range) {
+                                          size_t tile, F&& range, size_t rot = 0) {
   if (npack == 0) return;
+  auto visit = [&](size_t l0, size_t l1) {
+    if (l0 >= l1) return;
+    size_t a0 = l0 + rot;
+    if (a0 >= npack) a0 -= npack;
+    const size_t len = l1 - l0;
+    if (a0 + len <= npack) {
+      range(base + a0, base + a0 + len);
+    } else {
+      range(base + a0, base + npack);
+      range(base, base + a0 + len - npack);
+    }
+  };
   if (ctr == nullptr) {
     size_t p0, p1;
     split(npack, nblocks, b, p0, p1);
-    if (p0 < p1) range(base + p0, base + p1);
+    visit(p0, p1);
     return;
   }
   __shared__ unsigned long long s_next;
@@ -224,7 +239,7 @@ __device__ __forceinline__ void tile_loop(unsigned long long* ctr, int b, int nb
     __syncthreads();  // everyone has read s_next
     if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);  // prefetch the next index
     const size_t p0 = (size_t)t * tile;
-    range(base + p0, base + (p0 + tile < npack ? p0 + tile : npack));
+    visit(p0, p0 + tile < npack ? p0 + tile : npack);
     __syncthreads();
     t = s_next;
   }
@@ -476,7 +491,8 @@ __global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
           }
         }
       };
-      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * UAG * blockDim.x, range);
+      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * UAG * blockDim.x, range,
+                chunk_bound(n, P, (rank + 1) % P) / W);
       if (b == a.nblocks - 1) {
         for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
           const int c = chunk_of<P>(j, bnd);
@@ -705,7 +721,8 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
           }
         }
       };
-      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * U * blockDim.x, range);
+      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * U * blockDim.x, range,
+                chunk_bound(n, P, (rank + 1) % P) / W);
       if (b == a.nblocks - 1) {  // scalar tail n % W
         for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
