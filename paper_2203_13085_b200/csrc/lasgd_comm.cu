@@ -377,6 +377,69 @@ __device__ __forceinline__ T ordered_sum(const T* const (&src)[P], int rank, siz
   return rot_sum<T, P>(v, rank);
 }
 
+// Visit tiles 0..ntiles-1 from the atomic queue `ctr` (next index prefetched), or
+// statically strided over the CTAs when there is no queue (virtual ranks).
+template <typename V>
+__device__ __forceinline__ void queue_loop(unsigned long long* ctr, int b, int nblocks, unsigned long long ntiles,
+                                           V&& visit) {
+  if (ctr == nullptr) {
+    for (unsigned long long t = b; t < ntiles; t += nblocks) visit(t);
+    return;
+  }
+  __shared__ unsigned long long s_next;
+  __syncthreads();
+  if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);
+  __syncthreads();
+  unsigned long long t = s_next;
+  while (t < ntiles) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);
+    visit(t);
+    __syncthreads();
+    t = s_next;
+  }
+}
+
+// Phase-2 work of the two-shot kernels: the aligned body of every chunk c (minus the
+// own chunk when skip_own) in tiles interleaved across chunks and rotated per rank —
+// tile t is the (t / P)-th tile of chunk (rank + 1 + t) % P — so at any moment the
+// CTAs are spread over every owner (NVLink) and over the own chunk (HBM only), and
+// no owner serves all readers at once.  CTA 0 then does the unaligned head/tail
+// elements of every chunk (at most 2W-2 per chunk boundary).
+template <typename T, int P, typename FB, typename FS>
+__device__ __forceinline__ void chunk_tiles(unsigned long long* ctr, int b, int nblocks, size_t n, int rank,
+                                            bool skip_own, size_t tile, FB&& body, FS&& scalar) {
+  constexpr int W = Pack<T>::W;
+  size_t tmax = 0;
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    size_t cs, ce, cp0, cp1;
+    chunk_packs<T, P>(n, c, cs, ce, cp0, cp1);
+    const size_t tc = (cp1 - cp0 + tile - 1) / tile;
+    tmax = tc > tmax ? tc : tmax;
+  }
+  queue_loop(ctr, b, nblocks, (unsigned long long)tmax * P, [&](unsigned long long t) {
+    const int c = (rank + 1 + (int)(t % P)) % P;
+    if (skip_own && c == rank) return;
+    size_t cs, ce, cp0, cp1;
+    chunk_packs<T, P>(n, c, cs, ce, cp0, cp1);
+    const size_t a0 = cp0 + (size_t)(t / P) * tile;
+    if (a0 >= cp1) return;
+    body(c, a0, a0 + tile < cp1 ? a0 + tile : cp1);
+  });
+  if (b == 0) {
+    for (int c = 0; c < P; ++c) {
+      if (skip_own && c == rank) continue;
+      size_t cs, ce, cp0, cp1;
+      chunk_packs<T, P>(n, c, cs, ce, cp0, cp1);
+      const size_t he = cp0 * W < ce ? cp0 * W : ce;
+      const size_t ts = cp1 * W > he ? cp1 * W : he;
+      for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(c, j);
+      for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(c, j);
+    }
+  }
+}
+
 // Reduce-scatter of this rank's chunk (ring order x_rank, x_rank+1, ..., x_rank-1)
 // into its xbar buffer: aligned packs from work queue 0, head/tail elements on CTA 0.
 template <typename T, int P, int U>
@@ -459,46 +522,24 @@ __global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
     trace_mark(a, b, 2);
     if (ok) {
       // all-gather: every pack outside the own chunk comes from its owner's xbar
-      size_t bnd[P + 1];
+      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * UAG * blockDim.x,
+        [&](int c, size_t p0, size_t p1) {
+          const T* zc = reinterpret_cast<const T*>(a.xbar[c]);
+          for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)UAG * blockDim.x) {
+            Pack<T> v[UAG];
 #pragma unroll
-      for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
-      auto range = [&](size_t p0, size_t p1) {
-        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)UAG * blockDim.x) {
-          Pack<T> v[UAG];
-          int own[UAG];
+            for (int u = 0; u < UAG; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) v[u] = ld_cg(zc + pu * W);
+            }
 #pragma unroll
-          for (int u = 0; u < UAG; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            own[u] = -1;
-            if (pu < p1) {
-              const int c0 = chunk_of<P>(pu * W, bnd), c1 = chunk_of<P>(pu * W + W - 1, bnd);
-              own[u] = c0 == c1 ? c0 : P;  // P marks a pack straddling two chunks
-              if (c0 == c1 && c0 != rank) v[u] = ld_cg(reinterpret_cast<const T*>(a.xbar[c0]) + pu * W);
+            for (int u = 0; u < UAG; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) st_stream(out + pu * W, v[u]);
             }
           }
-#pragma unroll
-          for (int u = 0; u < UAG; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (own[u] >= 0 && own[u] < P && own[u] != rank) {
-              st_stream(out + pu * W, v[u]);
-            } else if (own[u] == P) {
-              for (int k = 0; k < W; ++k) {
-                const size_t j = pu * W + k;
-                const int c = chunk_of<P>(j, bnd);
-                if (c != rank) out[j] = reinterpret_cast<const T*>(a.xbar[c])[j];
-              }
-            }
-          }
-        }
-      };
-      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * UAG * blockDim.x, range,
-                chunk_bound(n, P, (rank + 1) % P) / W);
-      if (b == a.nblocks - 1) {
-        for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
-          const int c = chunk_of<P>(j, bnd);
-          if (c != rank) out[j] = reinterpret_cast<const T*>(a.xbar[c])[j];
-        }
-      }
+        },
+        [&](int c, size_t j) { out[j] = reinterpret_cast<const T*>(a.xbar[c])[j]; });
     }
   }
   report_nonfinite(a.nonfinite, bad);
@@ -668,9 +709,6 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
       const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
       const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
       const bool store_d = f.c.use_delta && f.mode == 0;
-      size_t bnd[P + 1];
-#pragma unroll
-      for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
       auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
         unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
         if (f.mode == 0) {
@@ -681,58 +719,48 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
         }
         bad += bb;
       };
-      auto mean_at = [&](size_t j) { return reinterpret_cast<const T*>(a.xbar[chunk_of<P>(j, bnd)])[j]; };
-      auto range = [&](size_t p0, size_t p1) {
-        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-          Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
-          int own[U];
+      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, false, (size_t)kTileIters * U * blockDim.x,
+        [&](int c, size_t p0, size_t p1) {
+          const T* zc = reinterpret_cast<const T*>(a.xbar[c]);  // owner's reduced chunk (NVLink unless c == rank)
+          for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+            Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            own[u] = -1;
-            if (pu < p1) {
-              const size_t j = pu * W;
-              const int c0 = chunk_of<P>(j, bnd), c1 = chunk_of<P>(j + W - 1, bnd);
-              own[u] = c0 == c1 ? c0 : P;
-              if (c0 == c1) vz[u] = ld_cg(reinterpret_cast<const T*>(a.xbar[c0]) + j);
-              vx[u] = ld_stream(x + j);
-              vg[u] = ld_stream(g + j);
-              if (load_m) vm[u] = ld_stream(m + j);
-              if (load_d) vd[u] = ld_stream(dl + j);
-              if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (own[u] >= 0) {
-              const size_t j = pu * W;
-              if (own[u] == P) {
-#pragma unroll
-                for (int k = 0; k < W; ++k) vz[u].v[k] = mean_at(j + k);
+            for (int u = 0; u < U; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) {
+                const size_t j = pu * W;
+                vz[u] = ld_cg(zc + j);
+                vx[u] = ld_stream(x + j);
+                vg[u] = ld_stream(g + j);
+                if (load_m) vm[u] = ld_stream(m + j);
+                if (load_d) vd[u] = ld_stream(dl + j);
+                if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
               }
+            }
 #pragma unroll
-              for (int k = 0; k < W; ++k) element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
-              st_stream(x + j, vx[u]);
-              if (f.c.use_mom) st_stream(m + j, vm[u]);
-              if (store_d) st_stream(dl + j, vd[u]);
-              st_stream(sn + j, vx[u]);
+            for (int u = 0; u < U; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) {
+                const size_t j = pu * W;
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                  element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
+                st_stream(x + j, vx[u]);
+                if (f.c.use_mom) st_stream(m + j, vm[u]);
+                if (store_d) st_stream(dl + j, vd[u]);
+                st_stream(sn + j, vx[u]);
+              }
             }
           }
-        }
-      };
-      tile_loop(q1, b, a.nblocks, 0, n / W, (size_t)kTileIters * U * blockDim.x, range,
-                chunk_bound(n, P, (rank + 1) % P) / W);
-      if (b == a.nblocks - 1) {  // scalar tail n % W
-        for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
+        },
+        [&](int c, size_t j) {
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), mean_at(j));
+          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), reinterpret_cast<const T*>(a.xbar[c])[j]);
           x[j] = xv;
           if (f.c.use_mom) m[j] = mv;
           if (store_d) dl[j] = dv;
           sn[j] = xv;
-        }
-      }
+        });
     }
   }
   report_nonfinite(a.nonfinite, bad);
