@@ -3,17 +3,20 @@
 
 Workload (BASELINE.json configs[2], the metric's config): ResNet-50 LASGD,
 batch 256 per GPU, parameters in one contiguous fp32 flat buffer of
-n = 25,557,032 (torchvision resnet50).  A "step" is one pass of the hot path
-over one minibatch's synthetic gradient: the fused local SGD step (K5,
-Nesterov momentum 0.9, weight decay 1e-4 — PAPER.md:229) and, every
-`sync_period` steps, the round boundary: wait for the previous mean, fused
-elastic pull + next snapshot (K4+K1), NVLink P2P mean all-reduce on the
-low-priority side stream (K2/K3, overlapping the next steps).  images/s =
-images whose gradients the sync path consumed per second over all ranks.
+n = 25,557,032 (torchvision resnet50); `--model resnet18|mobilenet_v2` selects
+the other BASELINE configs.  A "step" is one pass of the hot path over one
+minibatch's synthetic gradient under the deterministic schedule (sync period 1,
+the paper's tau_max = 1): the local step (Nesterov momentum 0.9, weight decay
+1e-4 — PAPER.md:229) and the round boundary — mean of every rank's snapshot
+over NVLink, elastic pull, next snapshot.  Default `--pipeline fused`: one K7
+kernel per boundary step; `--pipeline overlap`: K5, then K4 with the K2/K3
+all-reduce on a low-priority side stream.  images/s = images whose gradients
+the sync path consumed per second over all ranks.
 
-Also reported (not the headline): the real ResNet-50 training step
-(forward/backward in PyTorch, bf16 autocast, channels_last) with LASGD and
-with sync disabled (the no-sync ceiling) -> exposed sync ms/step.
+Also reported (not the headline): the real training step (forward/backward in
+PyTorch, bf16 autocast, channels_last) with the sync path under each pipeline,
+adaptive completion (tau histogram), and sync disabled (the no-sync ceiling) ->
+exposed sync ms/step.
 
 `--impl reference` times the reference's own CPU algorithm (f64, delta
 bookkeeping, ring-order mean; the C restatement in oracle/, all host threads,
@@ -35,7 +38,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ResNet-50 LASGD images/sec at 1/2/4/8 B200; exposed sync ms/step; sync GB/s vs roofline"
-R50_PARAMS = 25_557_032  # sum of torchvision resnet50() parameter numels (161 tensors)
+# BASELINE.json configs: ResNet-50 / ImageNet 224 (the metric's config), ResNet-18 / CIFAR 32 (10 classes),
+# MobileNetV2 / ImageNet 224.  params = torchvision parameter counts (flat fp32 buffer length).
+MODELS = {
+    "resnet50": {"params": 25_557_032, "image": 224, "classes": 1000, "ctor": "resnet50"},
+    "resnet18": {"params": 11_181_642, "image": 32, "classes": 10, "ctor": "resnet18"},
+    "mobilenet_v2": {"params": 3_504_872, "image": 224, "classes": 1000, "ctor": "mobilenet_v2"},
+}
 NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction, /opt/skills/guides/B200_PROFILING.md
 HBM_FALLBACK_GBS = 6650.0
 
@@ -47,6 +56,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--model", choices=sorted(MODELS), default="resnet50")
     ap.add_argument("--sync-period", type=int, default=1)
     ap.add_argument("--alpha", type=float, default=1.0)
     ap.add_argument("--algo", choices=["auto", "oneshot", "twoshot"], default="auto")
@@ -64,8 +74,8 @@ def parse():
 
 def config_dict(args, world):
     return {
-        "workload": "resnet50-lasgd-sync",
-        "params": R50_PARAMS,
+        "workload": f"{args.model}-lasgd-sync",
+        "params": MODELS[args.model]["params"],
         "batch_per_gpu": args.batch,
         "sync_period": args.sync_period,
         "alpha": args.alpha,
@@ -244,11 +254,13 @@ def run_reference(args, rank, world):
         return 0
     threads = os.cpu_count() or 1
     P = world
-    dt, n = cpu_reference_run(R50_PARAMS, P, args.sync_period, max(1, args.steps), max(1, args.warmup), threads)
-    scale = n / R50_PARAMS  # elementwise work is linear in n: full-size step time = dt / scale
+    full = MODELS[args.model]["params"]
+    dt, n = cpu_reference_run(full, P, args.sync_period, max(1, args.steps), max(1, args.warmup), threads)
+    scale = n / full  # elementwise work is linear in n: full-size step time = dt / scale
     value = P * args.batch / (dt / scale)
     sample = (f"reference algorithm (f64, delta bookkeeping, ring-order mean, {P} workers in-process) on "
-              f"{n} of {R50_PARAMS} parameters per step, scaled linearly to the full vector; "
+              f"{n} of {full} parameters per step, scaled linearly to the full vector; "
+              "the reference has no momentum, so its local step is the plain sgd_local_step; "
               f"{args.steps} timed steps after {args.warmup} warm-up; host: {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
@@ -302,7 +314,7 @@ def main():
         return float(t.item())
 
     algo_code = {"auto": N.ALGO_AUTO, "oneshot": N.ALGO_ONESHOT, "twoshot": N.ALGO_TWOSHOT}[args.algo]
-    n = R50_PARAMS
+    n = MODELS[args.model]["params"]
     sgd = L.SgdConfig(0.9, 0.0, 1e-4, True)
     lr = 0.1
     comm = L.P2PCommunicator(n, nblocks=args.nblocks, timeout_s=60.0) if world > 1 else None
@@ -491,11 +503,11 @@ def main():
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        dt, ns = cpu_reference_run(R50_PARAMS, 1, args.sync_period, 10, 2, threads, target_step_s=0.5)
-        scale = ns / R50_PARAMS
+        dt, ns = cpu_reference_run(n, 1, args.sync_period, 10, 2, threads, target_step_s=0.5)
+        scale = ns / n
         cpu_base = {"value": args.batch / (dt / scale), "unit": "images/s", "cores": threads, "kind": "port",
                     "sample": f"reference algorithm (f64 C port of oracle/, 1 worker, sgd_local_step + finalize) on "
-                              f"{ns} of {R50_PARAMS} parameters, 10 steps, scaled linearly; host {cpu_model()}"}
+                              f"{ns} of {n} parameters, 10 steps, scaled linearly; host {cpu_model()}"}
 
     if rank == 0:
         line = {
@@ -523,15 +535,19 @@ def main():
 
 
 def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barrier, max_over_ranks):
+    """Real training step (forward/backward in PyTorch, bf16 autocast, channels_last) with
+    the sync path under each schedule, and with sync disabled (the no-sync ceiling)."""
     import torch
     import torchvision
 
     import paper_2203_13085_b200 as L
 
+    spec = MODELS[args.model]
     torch.backends.cudnn.benchmark = True
-    model = torchvision.models.resnet50().to(dev).to(memory_format=torch.channels_last)
+    model = getattr(torchvision.models, spec["ctor"])(num_classes=spec["classes"]).to(dev)
+    model = model.to(memory_format=torch.channels_last)
     flat = L.FlatParams(model, channels_last=True)
-    assert flat.numel == R50_PARAMS
+    assert flat.numel == spec["params"], (flat.numel, spec["params"])
     if comm is not None:
         # identical x0 on every rank (Algorithm 1 line 1)
         import torch.distributed as dist
@@ -539,15 +555,16 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         dist.broadcast(flat.x, 0)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    images = torch.randn(args.batch, 3, 224, 224, device=dev, generator=gen).to(memory_format=torch.channels_last)
-    labels = torch.randint(0, 1000, (args.batch,), device=dev, generator=gen)
+    hw = spec["image"]
+    images = torch.randn(args.batch, 3, hw, hw, device=dev, generator=gen).to(memory_format=torch.channels_last)
+    labels = torch.randint(0, spec["classes"], (args.batch,), device=dev, generator=gen)
     lossf = torch.nn.CrossEntropyLoss()
 
-    def train(sync, steps, warm):
+    def train(steps, warm, **wkw):
         with torch.cuda.stream(compute):
             w = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=args.sync_period, alpha=args.alpha, mode="pull",
-                              sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute, sync=sync,
-                              pipeline=args.pipeline, fused_nblocks=args.fused_nblocks)
+                              sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
+                              fused_nblocks=args.fused_nblocks, **wkw)
 
             def one():
                 flat.zero_grad()
@@ -561,6 +578,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
             w.drain()
         torch.cuda.synchronize()
         barrier()
+        w.reset_records()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(compute):
             a.record(compute)
@@ -569,17 +587,29 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
             w.drain()
             b.record(compute)
         torch.cuda.synchronize()
-        return max_over_ranks(a.elapsed_time(b)) / steps
+        ms = max_over_ranks(a.elapsed_time(b)) / steps
+        hist = dict(w.tau_hist)
+        w.close()
+        return ms, hist
 
-    t_sync = train(True, args.train_steps, args.train_warmup)
-    t_nosync = train(False, args.train_steps, args.train_warmup)
-    return {
-        "model": "resnet50 (torchvision, random init)", "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params",
-        "steps": args.train_steps, "images_per_s_lasgd": world * args.batch / (t_sync / 1e3),
-        "images_per_s_nosync": world * args.batch / (t_nosync / 1e3), "ms_per_step_lasgd": t_sync,
-        "ms_per_step_nosync": t_nosync, "exposed_sync_ms_per_step": t_sync - t_nosync,
-        "exposed_sync_frac": (t_sync - t_nosync) / t_sync,
-    }
+    out = {"model": f"{spec['ctor']} (torchvision, random init, {hw}x{hw}, {spec['classes']} classes)",
+           "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params", "steps": args.train_steps}
+    t_nosync, _ = train(args.train_steps, args.train_warmup, sync=False)
+    runs = {"fused": dict(pipeline="fused"), "overlap": dict(pipeline="overlap"),
+            "overlap_adaptive": dict(pipeline="overlap", adaptive=True, tau_max=5)}
+    for name, kw in runs.items():
+        t, hist = train(args.train_steps, args.train_warmup, **kw)
+        out[name] = {"images_per_s": world * args.batch / (t / 1e3), "ms_per_step": t,
+                     "exposed_sync_ms_per_step": t - t_nosync, "exposed_sync_frac": (t - t_nosync) / t}
+        if kw.get("adaptive"):
+            out[name]["tau_histogram"] = {str(k): v for k, v in sorted(hist.items())}
+    out["nosync"] = {"images_per_s": world * args.batch / (t_nosync / 1e3), "ms_per_step": t_nosync}
+    main = out[args.pipeline]
+    out["images_per_s_lasgd"] = main["images_per_s"]
+    out["images_per_s_nosync"] = out["nosync"]["images_per_s"]
+    out["exposed_sync_ms_per_step"] = main["exposed_sync_ms_per_step"]
+    out["exposed_sync_frac"] = main["exposed_sync_frac"]
+    return out
 
 
 if __name__ == "__main__":
