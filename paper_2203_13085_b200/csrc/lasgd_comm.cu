@@ -572,7 +572,7 @@ struct FusedRound {
 };
 
 template <typename T, int P, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(256, 2) k_fused_round(CommArgs a, FusedRound<T> f) {
+__global__ void __launch_bounds__(256, (P == 1 ? 4 : 2)) k_fused_round(CommArgs a, FusedRound<T> f) {
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int vr = VIRTUAL ? (int)blockIdx.y : 0;
