@@ -30,20 +30,22 @@ from .flat import FlatParams  # noqa: E402
 from .optimizer import (  # noqa: E402
     HyperParamError,
     HyperParams,
+    ModelDivergenceError,
     NodeState,
     SgdConfig,
     TickAction,
     lasgd_finalize_round,
     lasgd_node_tick,
     sgd_local_step,
+    sync_allreduce_sgd_round,
 )
 from .params import ChunkSpec, as_device_vector, blend, partition_chunks, require_same_dim  # noqa: E402
 from .problems import LrSchedule, lr_at  # noqa: E402
 
 __all__ = [
     "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
-    "DimensionMismatchError", "FlatParams", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule",
+    "DimensionMismatchError", "FlatParams", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "ModelDivergenceError",
     "NodeState", "NonFiniteError", "P2PCommunicator", "SgdConfig", "Status", "TickAction", "TransportFault",
     "all_reduce_average", "as_device_vector", "blend", "bytes_per_node", "lasgd_finalize_round", "lasgd_node_tick",
-    "lr_at", "partition_chunks", "poll", "require_same_dim", "ring_schedule", "sgd_local_step",
+    "lr_at", "partition_chunks", "poll", "require_same_dim", "ring_schedule", "sgd_local_step", "sync_allreduce_sgd_round",
 ]

@@ -105,6 +105,8 @@ class LASGDWorker:
         self.k = sync_period
         self.schedule, self.lr = schedule, lr
         self.pipeline = pipeline
+        self.adaptive = adaptive
+        self.algo = algo
         self.timed = timed
         self.g = g
         self.compute = compute_stream if compute_stream is not None else torch.cuda.current_stream(x.device)
@@ -157,9 +159,30 @@ class LASGDWorker:
             return True
         return False
 
-    def drain(self) -> None:
-        """Order the compute stream after the in-flight all-reduce."""
+    def drain(self, group=None) -> None:
+        """Order the compute stream after the in-flight all-reduce.
+
+        Adaptive mode: ranks close rounds on their own clock, so at the end of a run
+        one rank may have launched more all-reduces than another, and its last launch
+        would wait for a peer launch that never comes.  The launch counts are
+        exchanged over torch.distributed and lagging ranks contribute their current
+        snapshot to the missing rounds (exactly what a node that keeps running would
+        submit), so every launched collective completes."""
         N.check(N.lib().lasgd_worker_drain(self._h), "lasgd_worker_drain")
+        if not (self.adaptive and self.world > 1):
+            return
+        import torch.distributed as dist
+
+        st = self._native_state()
+        counts = [None] * self.world
+        dist.all_gather_object(counts, int(st.seq), group=group)
+        extra = max(counts) - int(st.seq)
+        seq = 0
+        if extra > 0:
+            self.comm.stream.wait_stream(self.compute)
+            for _ in range(extra):
+                seq = self.comm.allreduce(st.snap_idx, self.algo)
+            self.comm.stream_wait(seq, self.compute)
 
     # ------------------------------------------------------------------ state / measurement
     def _native_state(self) -> N.WorkerState:

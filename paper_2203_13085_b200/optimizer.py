@@ -264,6 +264,37 @@ def lasgd_finalize_round(state: NodeState, z, num_nodes: int,
     return state
 
 
+class ModelDivergenceError(RuntimeError):
+    """optimizer.py:210-211: synchronous replicas stopped being bit-identical."""
+
+
+def sync_allreduce_sgd_round(states, grads, eta: float, transport=None, round_id: int = 0) -> torch.Tensor:
+    """optimizer.py:214-242 (SGD-AR baseline): average the gradients with the same
+    ring-order mean all-reduce, apply x = x + (-eta)*mean_g on every replica and move
+    its snapshot.  Replicas on one device (loopback) are checked bit for bit first;
+    with a per-process P2P transport each process passes its own single state."""
+    from .collective import all_reduce_average
+
+    if len(states) != len(grads):
+        raise ValueError("need one gradient per node")
+    ref = states[0].x_local
+    for st in states[1:]:
+        if not torch.equal(st.x_local.view(torch.int32 if ref.dtype == torch.float32 else torch.int64),
+                           ref.view(torch.int32 if ref.dtype == torch.float32 else torch.int64)):
+            raise ModelDivergenceError(f"node {st.rank} model differs from node {states[0].rank}")
+    handle = all_reduce_average(grads, transport=transport, round_id=round_id)
+    mean_g = handle.result_async()
+    for st in states:
+        K.sgd_step(st.x_local, mean_g, eta, nonfinite=st.nonfinite_counter)
+        nxt = 1 - st.snap_idx
+        K.snapshot(st.snapshots[nxt], st.x_local)
+        st.snap_idx = nxt
+        st.local_clock += 1
+        st.global_clock += 1
+        st._after_op(boundary=True)
+    return mean_g
+
+
 def lasgd_node_tick(state: NodeState, grad_fn: Callable, schedule: LrSchedule, collective_complete: bool,
                     z, tau_max: int, num_nodes: int,
                     submit: Optional[Callable[[torch.Tensor], CollectiveHandle]] = None, *,

@@ -261,5 +261,29 @@ def main():
     print("golden fixtures written to", HERE)
 
 
+def gen_sgd_ar(n=1001, P=3, rounds=5, seed=31):
+    """sync_allreduce_sgd_round (optimizer.py:214-242) with fixed gradients (reference)."""
+    rng = np.random.default_rng(seed)
+    x0 = rng.standard_normal(n)
+    grads = rng.standard_normal((rounds, P, n))
+    etas = np.array([0.1, 0.05, 0.2, 0.01, 0.07])[:rounds]
+    states = [O.NodeState.fresh(r, PR.ParamVector(x0)) for r in range(P)]
+    hist, means = [], []
+    for t in range(rounds):
+        mg = O.sync_allreduce_sgd_round(states, [PR.ParamVector(g) for g in grads[t]], float(etas[t]), round_id=t)
+        means.append(mg.data)
+        hist.append(states[0].x_local.data.copy())
+    return {"x0": x0, "grads": grads, "etas": etas, "x_hist": np.stack(hist), "mean_hist": np.stack(means)}
+
+
+def main_sgd_ar():
+    np.savez_compressed(os.path.join(HERE, "sgd_ar.npz"), **gen_sgd_ar())
+    print("sgd_ar fixture written")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "sgd_ar":
+        main_sgd_ar()
+    else:
+        main()
+        main_sgd_ar()

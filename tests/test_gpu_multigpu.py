@@ -114,6 +114,23 @@ def _w_worker_loop(rank, world, port):
         torch.cuda.synchronize()
         assert _same_bits(x.cpu().numpy(), xs[rank]), pipe
         dist.barrier()
+    # adaptive completion: ranks close rounds on their own clock (rank 1 is slowed down);
+    # drain() must equalise the launch counts so every collective completes
+    for tau_max in (1, 3):
+        x = torch.from_numpy(x0.copy()).cuda()
+        w = L.LASGDWorker(x, g, comm=comm, sync_period=tau_max, lr=0.05, mode="pull", adaptive=True,
+                          tau_max=tau_max)
+        for t in range(12):
+            if rank == 1:
+                torch.cuda._sleep(2_000_000)
+            g.copy_(torch.from_numpy(grads[t % steps, rank]))
+            w.step()
+        w.drain()
+        torch.cuda.synchronize()
+        hist = dict(w.tau_hist)
+        assert all(1 <= k <= tau_max for k in hist), hist
+        assert np.isfinite(x.cpu().numpy()).all()
+        dist.barrier()
     comm.close()
     dist.destroy_process_group()
 
