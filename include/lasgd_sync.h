@@ -214,6 +214,8 @@ typedef struct {
   int adaptive;        /* 1: close a round as soon as the mean landed (overlap pipeline only)    */
   int tau_max;         /* adaptive budget (optimizer.py:141-144); <= 0: sync_period              */
   int max_host_lead;   /* adaptive: host may run at most this many steps ahead of the GPU        */
+  int max_host_wait_us; /* adaptive: cap on one run-ahead wait (<= 0: 250 ms); a stream stalled on
+                           a peer's future launch must not block the host                        */
 } lasgd_worker_config;
 
 typedef struct {

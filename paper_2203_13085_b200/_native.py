@@ -93,6 +93,7 @@ class WorkerConfig(ctypes.Structure):
         ("adaptive", ctypes.c_int),
         ("tau_max", ctypes.c_int),
         ("max_host_lead", ctypes.c_int),
+        ("max_host_wait_us", ctypes.c_int),
     ]
 
 

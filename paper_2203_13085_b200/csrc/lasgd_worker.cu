@@ -14,6 +14,7 @@
 //   compute stream waits on the event; the host never blocks except for the optional
 //   run-ahead throttle that bounds how far the host's view runs ahead of the GPU).
 #include <string.h>
+#include <time.h>
 
 #include <vector>
 
@@ -263,7 +264,20 @@ extern "C" int lasgd_worker_step(lasgd_worker* w, const void* g, double lr) {
         for (auto& ev : w->lead) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
       }
       cudaEvent_t& slot = w->lead[w->lead_pos];
-      if (w->lead_count >= w->cfg.max_host_lead) cudaEventSynchronize(slot);
+      if (w->lead_count >= w->cfg.max_host_lead) {
+        // Bounded wait: if the compute stream is stalled on a peer's next launch (a
+        // rank that closed more rounds than its peers, e.g. at the end of a run), an
+        // unbounded host wait would deadlock against the peer's drain.
+        struct timespec t0, t;
+        clock_gettime(CLOCK_MONOTONIC, &t0);
+        const double cap = w->cfg.max_host_wait_us > 0 ? w->cfg.max_host_wait_us * 1e-6 : 0.25;
+        while (cudaEventQuery(slot) == cudaErrorNotReady) {
+          clock_gettime(CLOCK_MONOTONIC, &t);
+          if ((t.tv_sec - t0.tv_sec) + 1e-9 * (t.tv_nsec - t0.tv_nsec) > cap) break;
+          struct timespec ns = {0, 20000};
+          nanosleep(&ns, nullptr);
+        }
+      }
       cudaEventRecord(slot, w->compute);
       w->lead_pos = (w->lead_pos + 1) % w->lead.size();
       w->lead_count++;

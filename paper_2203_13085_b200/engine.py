@@ -87,7 +87,8 @@ class LASGDWorker:
                  lr: Optional[float] = None, adaptive: bool = False, tau_max: Optional[int] = None,
                  algo: int = N.ALGO_AUTO, compute_stream: Optional[torch.cuda.Stream] = None, sync: bool = True,
                  timed: bool = False, check_finite: str = "lazy", max_host_lead: int = 2,
-                 pipeline: str = "overlap", fused_nblocks: int = 0, check_every: int = 16):
+                 pipeline: str = "overlap", fused_nblocks: int = 0, check_every: int = 16,
+                 max_host_wait_us: int = 250_000):
         if (schedule is None) == (lr is None):
             raise ValueError("give exactly one of schedule / lr")
         if mode not in ("pull", "delta"):
@@ -123,7 +124,7 @@ class LASGDWorker:
         cfg = N.WorkerConfig(sync_period, float(alpha), 1 if mode == "delta" else 0, 1 if pipeline == "fused" else 0,
                              int(algo), int(fused_nblocks), float(sgd.momentum), float(sgd.dampening),
                              float(sgd.weight_decay), int(sgd.nesterov), int(bool(sync)), int(bool(adaptive)),
-                             int(tau_max or 0), int(max_host_lead))
+                             int(tau_max or 0), int(max_host_lead), int(max_host_wait_us))
         side = comm.stream if comm is not None else None
         h = ctypes.c_void_p()
         ptr = K._ptr
