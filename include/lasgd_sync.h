@@ -191,6 +191,12 @@ int lasgd_comm_set_trace(lasgd_comm* c, int on);
 int lasgd_comm_read_trace(lasgd_comm* c, unsigned long long* out, int max_ctas);
 int lasgd_comm_destroy(lasgd_comm* c);
 
+/* Highest launch sequence number any peer has started (from the entry flags peers
+ * wrote into this rank's signal pad); used to drain adaptive runs without a host
+ * collective.  Never waits behind the caller's streams. */
+int lasgd_comm_peer_max_seq(lasgd_comm* c, unsigned long long* out);
+/* Number of launches this rank has issued on the communicator (its current sequence number). */
+int lasgd_comm_launches(lasgd_comm* c, unsigned long long* out);
 /* rank, world size and the mean buffer of a communicator (any pointer may be NULL). */
 int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar);
 

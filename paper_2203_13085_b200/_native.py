@@ -149,6 +149,8 @@ SIGNATURES = {
     "lasgd_comm_read_trace": (_I, [_P, _P, _I]),
     "lasgd_comm_destroy": (_I, [_P]),
     "lasgd_comm_info": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_P)]),
+    "lasgd_comm_peer_max_seq": (_I, [_P, _ULLP]),
+    "lasgd_comm_launches": (_I, [_P, _ULLP]),
     "lasgd_worker_create": (_I, [_P, _P, _P, _P, _P, _P, _SZ, _I, ctypes.POINTER(WorkerConfig), _P, _P, _P,
                                  ctypes.POINTER(_P)]),
     "lasgd_worker_step": (_I, [_P, _P, _D]),

@@ -366,6 +366,18 @@ class P2PCommunicator:
                 "lasgd_comm_fused_round")
         return seq.value
 
+    def launches(self) -> int:
+        """Sequence number of this rank's latest launch."""
+        v = ctypes.c_ulonglong()
+        N.check(N.lib().lasgd_comm_launches(self._h, ctypes.byref(v)))
+        return v.value
+
+    def peer_max_seq(self) -> int:
+        """Highest launch any peer has started (from its entry flags in our pad)."""
+        v = ctypes.c_ulonglong()
+        N.check(N.lib().lasgd_comm_peer_max_seq(self._h, ctypes.byref(v)), "peer_max_seq")
+        return v.value
+
     def query(self, seq: int) -> int:
         return N.check(N.lib().lasgd_comm_query(self._h, seq), "all-reduce")
 

@@ -1155,6 +1155,33 @@ extern "C" int lasgd_comm_resolve_algo(lasgd_comm* c, int algo) {
   return resolve_algo(algo, c->world, c->n * c->elem);
 }
 
+// Highest launch sequence number any peer has started, read from the entry flags the
+// peers' CTAs wrote into this rank's signal pad.  Uses a private non-blocking stream,
+// so it never waits behind the caller's (possibly stalled) streams.
+extern "C" int lasgd_comm_peer_max_seq(lasgd_comm* c, unsigned long long* out) {
+  if (!c || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard g(c->device);
+  const size_t words = (size_t)kMaxB * kMaxR;  // phase-0 region
+  static thread_local uint32_t* host = nullptr;
+  static thread_local cudaStream_t s = nullptr;
+  if (!host) LASGD_CUDA_TRY(cudaHostAlloc((void**)&host, words * sizeof(uint32_t), cudaHostAllocDefault));
+  if (!s) LASGD_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  LASGD_CUDA_TRY(cudaMemcpyAsync(host, c->base, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  LASGD_CUDA_TRY(cudaStreamSynchronize(s));
+  uint32_t best = 0;
+  for (int b = 0; b < kMaxB; ++b)
+    for (int q = 0; q < c->world; ++q)
+      if (q != c->rank && host[(size_t)b * kMaxR + q] > best) best = host[(size_t)b * kMaxR + q];
+  *out = best;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_launches(lasgd_comm* c, unsigned long long* out) {
+  if (!c || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  *out = c->seq;
+  return LASGD_OK;
+}
+
 extern "C" int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   if (rank) *rank = c->rank;

@@ -172,18 +172,39 @@ class LASGDWorker:
         N.check(N.lib().lasgd_worker_drain(self._h), "lasgd_worker_drain")
         if not (self.adaptive and self.world > 1):
             return
+        import time
+
         import torch.distributed as dist
 
-        st = self._native_state()
-        counts = [None] * self.world
-        dist.all_gather_object(counts, int(st.seq), group=group)
-        extra = max(counts) - int(st.seq)
-        seq = 0
-        if extra > 0:
-            self.comm.stream.wait_stream(self.compute)
+        comm = self.comm
+        slot = self._native_state().snap_idx
+
+        def pad_to(target: int) -> None:
+            extra = target - comm.launches()
+            if extra <= 0:
+                return
+            comm.stream.wait_stream(self.compute)  # the padding reads the current snapshot slot
             for _ in range(extra):
-                seq = self.comm.allreduce(st.snap_idx, self.algo)
-            self.comm.stream_wait(seq, self.compute)
+                comm.allreduce(slot, self.algo)
+
+        # A peer that launched more rounds may be stalled (device waiting on our missing
+        # launch, host possibly blocked behind it), so never block on a host collective
+        # here: pad to what the peers' entry flags show while an asynchronous MAX of the
+        # launch counts completes, then pad to the agreed maximum.
+        side = torch.cuda.Stream(device=self.state.x_local.device)
+        backend = dist.get_backend(group)
+        with torch.cuda.stream(side):
+            t = torch.tensor([comm.launches()], dtype=torch.int64,
+                             device=self.state.x_local.device if backend == "nccl" else "cpu")
+            work = dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group, async_op=True)
+            while not work.is_completed():
+                pad_to(comm.peer_max_seq())
+                time.sleep(1e-3)
+            work.wait()
+        pad_to(int(t.item()))
+        last = comm.launches()
+        if last:
+            comm.stream_wait(last, self.compute)
 
     # ------------------------------------------------------------------ state / measurement
     def _native_state(self) -> N.WorkerState:
