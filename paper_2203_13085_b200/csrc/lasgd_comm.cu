@@ -691,35 +691,103 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
   unsigned bad = 0;
   unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
   unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
+  T* const x = f.x[vr];
+  const T* const g = f.g[vr];
+  T* const m = f.m[vr];
+  T* const dl = f.delta[vr];
+  T* const sn = f.snap_next[vr];
+  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
+  const bool store_d = f.c.use_delta && f.mode == 0;
+  auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
+    unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+    if (f.mode == 0) {
+      bb += pull_elem(f.neg_alpha, xv, sv, zb);
+    } else {
+      xv = add_rn(zb, dv);
+      bb += !finite(xv);
+    }
+    bad += bb;
+  };
   trace_mark(a, b, 0);
   if (a.phases & 1) {
     if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
     trace_mark(a, b, 1);
-    if (ok) bad += reduce_own_chunk<T, P, U>(a, b, rank, q0);
+    if (ok) {
+      // Own chunk, complete in this phase: its mean is formed here (ring order, stored
+      // for the peers' phase 2) and the local step + pull applied right away — the own
+      // snapshot is one of the P sources already in registers.
+      T* own = reinterpret_cast<T*>(a.xbar[rank]);
+      const T* src[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
+      size_t cs, ce, cp0, cp1;
+      chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
+      tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> v[U][P], vx[U], vg[U], vm[U], vd[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+#pragma unroll
+              for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + j);
+              vx[u] = ld_stream(x + j);
+              vg[u] = ld_stream(g + j);
+              if (load_m) vm[u] = ld_stream(m + j);
+              if (load_d) vd[u] = ld_stream(dl + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+              Pack<T> z;
+#pragma unroll
+              for (int k = 0; k < W; ++k) {
+                T lane[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+                T sv = lane[0];
+#pragma unroll
+                for (int q = 1; q < P; ++q) sv = (q == rank) ? lane[q] : sv;
+                z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], sv, z.v[k]);
+              }
+              st_plain(own + j, z);
+              st_stream(x + j, vx[u]);
+              if (f.c.use_mom) st_stream(m + j, vm[u]);
+              if (store_d) st_stream(dl + j, vd[u]);
+              st_stream(sn + j, vx[u]);
+            }
+          }
+        }
+      });
+      if (b == 0) {  // unaligned head / tail elements of the own chunk
+        const size_t he = cp0 * W < ce ? cp0 * W : ce;
+        const size_t ts = cp1 * W > he ? cp1 * W : he;
+        auto scalar = [&](size_t j) {
+          const T zb = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+          own[j] = zb;
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, snap_own[j], zb);
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+        };
+        for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
+        for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
+      }
+    }
   }
   if (a.phases & 2) {
     if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
     trace_mark(a, b, 2);
     if (ok) {
-      T* const x = f.x[vr];
-      const T* const g = f.g[vr];
-      T* const m = f.m[vr];
-      T* const dl = f.delta[vr];
-      T* const sn = f.snap_next[vr];
-      const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
-      const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-      const bool store_d = f.c.use_delta && f.mode == 0;
-      auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
-        unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
-        if (f.mode == 0) {
-          bb += pull_elem(f.neg_alpha, xv, sv, zb);
-        } else {
-          xv = add_rn(zb, dv);
-          bb += !finite(xv);
-        }
-        bad += bb;
-      };
-      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, false, (size_t)kTileIters * U * blockDim.x,
+      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
         [&](int c, size_t p0, size_t p1) {
           const T* zc = reinterpret_cast<const T*>(a.xbar[c]);  // owner's reduced chunk (NVLink unless c == rank)
           for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
