@@ -572,7 +572,7 @@ struct FusedRound {
 };
 
 template <typename T, int P, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(256, (P == 1 ? 4 : 2)) k_fused_round(CommArgs a, FusedRound<T> f) {
+__global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs a, FusedRound<T> f) {
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int vr = VIRTUAL ? (int)blockIdx.y : 0;
@@ -1049,8 +1049,8 @@ extern "C" int lasgd_fused_round_virtual(int P, int algo, void* const* x, const 
   if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   if (algo == LASGD_ALGO_TWOSHOT && !xbars) return fail(LASGD_ERR_INVALID_ARGUMENT, "two-shot needs per-rank mean buffers");
   if (n == 0) return LASGD_OK;
-  // P == 1 (local step + snapshot) needs ~60 registers: 4 CTAs per SM; otherwise 2
-  if (nblocks <= 0) nblocks = (P == 1 ? 4 : 2) * num_sms();
+  // P == 1 (local step + snapshot) fits 3 CTAs per SM (<= 85 registers); otherwise 2
+  if (nblocks <= 0) nblocks = (P == 1 ? 3 : 2) * num_sms();
   CommArgs a;
   memset(&a, 0, sizeof(a));
   for (int q = 0; q < P; ++q) {
