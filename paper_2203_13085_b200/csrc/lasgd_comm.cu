@@ -1045,7 +1045,10 @@ extern "C" int lasgd_fused_round_virtual(int P, int algo, void* const* x, const 
   if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
   int rc = check_fused_args(P, x, g, m, delta, snap_next, sgd, alpha, mode);
   if (rc) return rc;
-  algo = P == 1 ? LASGD_ALGO_ONESHOT : resolve_algo(algo, P, n * elem_bytes(dtype));
+  if (P == 1)  // no peers: the streaming local step with the snapshot store fused in
+    return sgd_step_snapshot(dtype, x[0], g[0], m ? m[0] : nullptr, delta ? delta[0] : nullptr, snap_next[0], n, sgd,
+                             nonfinite, stream);
+  algo = resolve_algo(algo, P, n * elem_bytes(dtype));
   if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   if (algo == LASGD_ALGO_TWOSHOT && !xbars) return fail(LASGD_ERR_INVALID_ARGUMENT, "two-shot needs per-rank mean buffers");
   if (n == 0) return LASGD_OK;

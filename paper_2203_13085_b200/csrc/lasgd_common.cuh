@@ -22,6 +22,10 @@ int cuda_fail(cudaError_t e, const char* what);
 
 int num_sms();  // SM count of the current device (cached per device)
 
+// K5 with the next snapshot written in the same pass (lasgd_elementwise.cu).
+int sgd_step_snapshot(int dtype, void* x, const void* g, void* m, void* delta, void* snap, size_t n,
+                      const lasgd_sgd_params* p, unsigned long long* nf, void* s);
+
 // ---------------------------------------------------------------- arithmetic
 // Separately rounded ops (the reference's numpy never contracts a*b+c).
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }

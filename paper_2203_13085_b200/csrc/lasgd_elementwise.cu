@@ -130,6 +130,7 @@ struct SgdOp {
   const T* g;
   T* m;
   T* delta;
+  T* snap;  // optional: also write the updated x here (K7 at P = 1: local step + next snapshot)
   SgdCoef<T> c;
   static constexpr int U = 2;
   struct Loaded { Pack<T> x, g, m, d; };
@@ -147,6 +148,7 @@ struct SgdOp {
     st_stream(x + j, L.x);
     if (c.use_mom) st_stream(m + j, L.m);
     if (c.use_delta) st_stream(delta + j, L.d);
+    if (snap) st_stream(snap + j, L.x);
     return bad;
   }
   __device__ __forceinline__ unsigned scalar(size_t j) const {
@@ -155,6 +157,7 @@ struct SgdOp {
     x[j] = xv;
     if (c.use_mom) m[j] = mv;
     if (c.use_delta) delta[j] = dv;
+    if (snap) snap[j] = xv;
     return bad;
   }
 };
@@ -240,15 +243,26 @@ int copy_t(void* dst, const void* src, size_t n, void* s) {
 
 template <typename T>
 int sgd_t(void* x, const void* g, void* m, void* delta, size_t n, const lasgd_sgd_params* p,
-          unsigned long long* nf, void* s) {
+          unsigned long long* nf, void* s, void* snap = nullptr) {
   SgdOp<T> op;
   op.x = (T*)x;
   op.g = (const T*)g;
   op.m = (T*)m;
   op.delta = (T*)delta;
+  op.snap = (T*)snap;
   op.c = make_sgd_coef<T>(p, delta != nullptr);
-  bool al = aligned16(x) && aligned16(g) && (!op.c.use_mom || aligned16(m)) && (!op.c.use_delta || aligned16(delta));
+  bool al = aligned16(x) && aligned16(g) && (!op.c.use_mom || aligned16(m)) && (!op.c.use_delta || aligned16(delta)) &&
+            (!snap || aligned16(snap));
   return launch<T>(op, n, al, nf, s);
+}
+
+// K7 at P = 1 (no peers, no mean, no pull — optimizer.py:168-169): the local step with
+// the next snapshot written in the same streaming pass (6B instead of K5 5B + K1 2B).
+int sgd_step_snapshot(int dtype, void* x, const void* g, void* m, void* delta, void* snap, size_t n,
+                      const lasgd_sgd_params* p, unsigned long long* nf, void* s) {
+  if (dtype == LASGD_F32) return sgd_t<float>(x, g, m, delta, n, p, nf, s, snap);
+  if (dtype == LASGD_F64) return sgd_t<double>(x, g, m, delta, n, p, nf, s, snap);
+  return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
 }
 
 template <typename T>
