@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--model", choices=sorted(MODELS), default="resnet50")
     ap.add_argument("--sync-period", type=int, default=1)
     ap.add_argument("--alpha", type=float, default=1.0)
-    ap.add_argument("--algo", choices=["auto", "oneshot", "twoshot"], default="auto")
+    ap.add_argument("--algo", choices=["auto", "oneshot", "twoshot", "push"], default="auto",
+                    help="all-reduce / fused-round algorithm (push: K8, fused pipeline only)")
     ap.add_argument("--nblocks", type=int, default=128)
     ap.add_argument("--pipeline", choices=["overlap", "fused"], default="fused",
                     help="overlap: K5 | K4 | K2/K3 on a side stream; fused: one K7 pass per round boundary")
@@ -154,7 +155,10 @@ def kernel_bytes(name, n, world, comm, algo_code, sgd_momentum=True):
     if name == "fused_round":
         hbm = (7 if world > 1 else 6) * B  # read x,g,m(,own snap); write x,m,next snap
         nvl = (world - 1) * B  # one-shot: every peer's whole snapshot over NVLink
-        if world > 1 and comm.resolve_algo(algo_code) == 2:  # two-shot: RS in + AG in, own chunk mean via HBM
+        if world > 1 and algo_code == 3:  # push: 2(P-1)/P*B out as stores; staged reads + landing writes in HBM
+            nvl = comm.bytes_per_node(2)
+            hbm += 2 * nvl
+        elif world > 1 and comm.resolve_algo(algo_code) == 2:  # two-shot: RS in + AG in, own chunk mean via HBM
             nvl = comm.bytes_per_node(2)
             hbm += 2 * B // world
         if nvl / NVLINK_PEAK_GBS > hbm / peaks()[0]:
@@ -313,7 +317,8 @@ def main():
         dist.all_reduce(t)
         return float(t.item())
 
-    algo_code = {"auto": N.ALGO_AUTO, "oneshot": N.ALGO_ONESHOT, "twoshot": N.ALGO_TWOSHOT}[args.algo]
+    algo_code = {"auto": N.ALGO_AUTO, "oneshot": N.ALGO_ONESHOT, "twoshot": N.ALGO_TWOSHOT,
+                 "push": N.ALGO_PUSH}[args.algo]
     n = MODELS[args.model]["params"]
     sgd = L.SgdConfig(0.9, 0.0, 1e-4, True)
     lr = 0.1

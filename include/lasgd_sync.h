@@ -51,6 +51,7 @@ extern "C" {
 #define LASGD_ALGO_AUTO 0
 #define LASGD_ALGO_ONESHOT 1
 #define LASGD_ALGO_TWOSHOT 2
+#define LASGD_ALGO_PUSH 3 /* fused round only: owners reduce locally staged chunks, results pushed */
 
 #define LASGD_MAX_RANKS 8
 #define LASGD_MAX_BLOCKS 512
@@ -116,6 +117,17 @@ int lasgd_finalize(void* x, void* snap_next, const void* z, const void* delta, s
  * Results are bit-identical to the reference ring order. */
 int lasgd_mean_virtual(void* const* outs, int n_out, const void* const* srcs, int P, size_t n, int dtype,
                        int algo, int nblocks, unsigned long long* nonfinite, void* stream);
+
+/* K8 (push round) over P virtual ranks on ONE device — test path.  snaps = every
+ * rank's current snapshot (parity `cur`), stages = every rank's staging area of
+ * 2 * P * lasgd_push_stage_elems(n, P, dtype) elements; init = 1 stages the current
+ * snapshots first (the communicator does this on its first push round). */
+int lasgd_fused_push_virtual(int P, void* const* x, const void* const* g, void* const* m, void* const* delta,
+                             const void* const* snaps, void* const* snap_next, void* const* xbars,
+                             void* const* stages, int cur, int init, size_t n, int dtype,
+                             const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+                             unsigned long long* nonfinite, void* stream);
+size_t lasgd_push_stage_elems(size_t n, int P, int dtype);
 
 /* ---- multi-GPU communicator (NVLink P2P through NVSwitch) -------------- */
 
@@ -195,6 +207,9 @@ int lasgd_comm_destroy(lasgd_comm* c);
  * wrote into this rank's signal pad); used to drain adaptive runs without a host
  * collective.  Never waits behind the caller's streams. */
 int lasgd_comm_peer_max_seq(lasgd_comm* c, unsigned long long* out);
+/* The caller rewrote a snapshot slot outside the push round: the next push round
+ * re-stages the current snapshot first. */
+int lasgd_comm_invalidate_staging(lasgd_comm* c);
 /* Number of launches this rank has issued on the communicator (its current sequence number). */
 int lasgd_comm_launches(lasgd_comm* c, unsigned long long* out);
 /* rank, world size and the mean buffer of a communicator (any pointer may be NULL). */

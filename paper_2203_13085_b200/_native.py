@@ -30,6 +30,7 @@ F64 = 1
 ALGO_AUTO = 0
 ALGO_ONESHOT = 1
 ALGO_TWOSHOT = 2
+ALGO_PUSH = 3
 MAX_RANKS = 8
 MAX_BLOCKS = 512
 IPC_HANDLE_BYTES = 64
@@ -151,6 +152,10 @@ SIGNATURES = {
     "lasgd_comm_info": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_P)]),
     "lasgd_comm_peer_max_seq": (_I, [_P, _ULLP]),
     "lasgd_comm_launches": (_I, [_P, _ULLP]),
+    "lasgd_comm_invalidate_staging": (_I, [_P]),
+    "lasgd_fused_push_virtual": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _SZ, _I, ctypes.POINTER(SgdParams),
+                                      _D, _I, _I, _P, _P]),
+    "lasgd_push_stage_elems": (_SZ, [_SZ, _I, _I]),
     "lasgd_worker_create": (_I, [_P, _P, _P, _P, _P, _P, _SZ, _I, ctypes.POINTER(WorkerConfig), _P, _P, _P,
                                  ctypes.POINTER(_P)]),
     "lasgd_worker_step": (_I, [_P, _P, _D]),

@@ -62,6 +62,12 @@ struct CommArgs {
   unsigned long long* trace;  // optional per-CTA timeline: [b][0..3] = start, entry passed, mid passed, end
   unsigned long long* tile_ctr;  // two work queues of this launch (nullptr: static slices)
   unsigned int* mid_ctr;         // CTAs of this rank past the reduce-scatter (rank-level barrier)
+  unsigned int* end_ctr;         // CTAs of this rank done pushing (push round, rank-level end signal)
+  // push round (K8): per-rank staging regions and round bookkeeping
+  char* stage[kMaxR];            // owner o's staging: [parity][source rank][stage_elems]
+  size_t stage_elems;
+  int cur;                       // snapshot slot / staging parity read this round
+  uint32_t prev_push;            // launch whose end signals certify the staged contributions
 };
 
 __device__ __forceinline__ unsigned long long globaltimer();
@@ -250,33 +256,38 @@ __device__ __forceinline__ void for_tiles(const CommArgs& a, int b, size_t npack
   tile_loop(a.tile_ctr, b, a.nblocks, 0, npack, (size_t)kTileIters * U * blockDim.x, range);
 }
 
-// Rank-level barrier between the two phases of the two-shot kernels: every CTA of this
-// rank counts itself in; the last one signals every peer (after every CTA's
-// __threadfence_system, so all reduce-scatter stores are visible system-wide); then
-// all CTAs wait for every peer's signal.  Requires all CTAs co-resident: the P2P
-// two-shot kernels are launched cooperatively.
+// Rank-level signal of kind k (0 = mid: reduce-scatter / mean pushes done, 1 = end:
+// next-snapshot chunks pushed to their owners): every CTA counts itself in (after a
+// __threadfence_system, so its stores — remote ones included — are visible system
+// wide); the last CTA of the rank writes `epoch` into slot [k][rank] of every peer.
 template <int P>
-__device__ bool rank_barrier(const CommArgs& a, int b, int rank) {
+__device__ void rank_signal(const CommArgs& a, int kind, unsigned* ctr, int rank) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    const unsigned prev = atomicAdd(a.mid_ctr, 1u);
+    const unsigned prev = atomicAdd(ctr, 1u);
     s_last = prev == (unsigned)a.nblocks - 1u;
-    if (s_last) *a.mid_ctr = 0u;  // every CTA of this launch has counted itself in
+    if (s_last) *ctr = 0u;  // every CTA of this launch has counted itself in
   }
   __syncthreads();
-  const size_t slot = (size_t)2 * kMaxB * kMaxR;
-  if (s_last && threadIdx.x < P && a.skip_signal_phase != 1) {
+  const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)kind * kMaxR;
+  if (s_last && threadIdx.x < P && !(kind == 0 && a.skip_signal_phase == 1)) {
     __threadfence_system();
     st_release_sys(a.pad[threadIdx.x] + slot + rank, a.epoch);
   }
+}
+
+// Wait until every rank has signalled kind k with an epoch >= `epoch`.
+template <int P>
+__device__ bool rank_wait(const CommArgs& a, int kind, uint32_t epoch, int b, int rank) {
+  const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)kind * kMaxR;
   int ok = 1;
   if (threadIdx.x < P) {
     const int q = threadIdx.x;
     const uint32_t* f = a.pad[rank] + slot + q;
     const unsigned long long t0 = globaltimer();
-    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+    while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
       if ((long long)(globaltimer() - t0) > a.timeout_ns) {
         report_failure(a, ERR_TIMEOUT, q, 1, b, rank);
         ok = 0;
@@ -286,6 +297,14 @@ __device__ bool rank_barrier(const CommArgs& a, int b, int rank) {
     }
   }
   return __syncthreads_and(ok) != 0;
+}
+
+// Rank-level barrier between the two phases of the two-shot kernels.  Requires all
+// CTAs co-resident: the P2P two-shot kernels are launched cooperatively.
+template <int P>
+__device__ bool rank_barrier(const CommArgs& a, int b, int rank) {
+  rank_signal<P>(a, 0, a.mid_ctr, rank);
+  return rank_wait<P>(a, 0, a.epoch, b, rank);
 }
 
 // Aligned body of chunk c in packs, [cp0, cp1), plus its unaligned head/tail elements.
@@ -929,6 +948,216 @@ int check_fused_args(int nr, void* const* x, const void* const* g, void* const* 
   return LASGD_OK;
 }
 
+// ------------------------------------------------------------------ push round (K8)
+// The fused round with the data movement done by remote STORES from the producer.
+// Chunk c is owned by rank c.  Every rank keeps, in its IPC region, a staging area
+// stage[parity][source][chunk] for the contributions to its own chunk.
+//   init (phase bit 4): push chunk c of the current snapshot to owner c's staging.
+//   phase A (bit 1): wait for every rank's end signal of the previous push launch
+//     (staged contributions complete; peers finished their previous round); the owner
+//     forms the ring-order mean of its chunk from local staging + its own snapshot,
+//     applies the local step + pull to its own chunk, and pushes the mean to every
+//     peer's xbar.
+//   rank-level mid barrier (all means pushed).
+//   phase B (bit 2): every other chunk: local step + pull with the mean in the local
+//     xbar, next snapshot written locally and pushed to the owner's staging (other
+//     parity); then the rank-level end signal.
+// Per rank and round: NVLink out 2(P-1)/P*B as posted writes, all reads local.  Same
+// element functions and summation order as K7, so results are bit-identical.
+template <typename T>
+__device__ __forceinline__ T* stage_ptr(const CommArgs& a, int owner, int parity, int src, int P) {
+  return reinterpret_cast<T*>(a.stage[owner]) + ((size_t)parity * P + src) * a.stage_elems;
+}
+
+template <typename T, int P, bool VIRTUAL, int U>
+__global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T> f) {
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
+  const int b = blockIdx.x;
+  const size_t n = a.n;
+  const int cur = a.cur, nxt = 1 - a.cur;
+  bool ok = true;
+  unsigned bad = 0;
+  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
+  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
+  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  trace_mark(a, b, 0);
+  // offset of element j of chunk c inside a staging slot (keeps 16-byte alignment)
+  auto soff = [&](int c, size_t j) { return j - chunk_bound(n, P, c) / W * W; };
+  if (a.phases & 4) {
+    // initial contributions: chunk c of the current snapshot -> owner c, parity cur
+    chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
+      [&](int c, size_t p0, size_t p1) {
+        T* dst = stage_ptr<T>(a, c, cur, rank, P);
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) v[u] = ld_stream(snap_own + pu * W);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) st_plain(dst + soff(c, pu * W), v[u]);
+          }
+        }
+      },
+      [&](int c, size_t j) { stage_ptr<T>(a, c, cur, rank, P)[soff(c, j)] = snap_own[j]; });
+    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+  }
+  T* const x = f.x[vr];
+  const T* const g = f.g[vr];
+  T* const m = f.m[vr];
+  T* const dl = f.delta[vr];
+  T* const sn = f.snap_next[vr];
+  const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
+  const bool store_d = f.c.use_delta && f.mode == 0;
+  auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
+    unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+    if (f.mode == 0) {
+      bb += pull_elem(f.neg_alpha, xv, sv, zb);
+    } else {
+      xv = add_rn(zb, dv);
+      bb += !finite(xv);
+    }
+    bad += bb;
+  };
+  if (a.phases & 1) {
+    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
+    trace_mark(a, b, 1);
+    if (ok) {
+      const T* src[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) src[q] = q == rank ? snap_own : stage_ptr<T>(a, rank, cur, q, P);
+      size_t cs, ce, cp0, cp1;
+      chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
+      const size_t base = cs / W * W;  // staging offset origin of the own chunk
+      tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> v[U][P], vx[U], vg[U], vm[U], vd[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+#pragma unroll
+              for (int q = 0; q < P; ++q) v[u][q] = ld_stream(src[q] + (q == rank ? j : j - base));
+              vx[u] = ld_stream(x + j);
+              vg[u] = ld_stream(g + j);
+              if (load_m) vm[u] = ld_stream(m + j);
+              if (load_d) vd[u] = ld_stream(dl + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+              Pack<T> z;
+#pragma unroll
+              for (int k = 0; k < W; ++k) {
+                T lane[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+                T sv = lane[0];
+#pragma unroll
+                for (int q = 1; q < P; ++q) sv = (q == rank) ? lane[q] : sv;
+                z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], sv, z.v[k]);
+              }
+#pragma unroll
+              for (int q = 0; q < P; ++q)
+                if (q != rank) st_plain(reinterpret_cast<T*>(a.xbar[q]) + j, z);  // the mean to every peer
+              st_stream(x + j, vx[u]);
+              if (f.c.use_mom) st_stream(m + j, vm[u]);
+              if (store_d) st_stream(dl + j, vd[u]);
+              st_stream(sn + j, vx[u]);
+            }
+          }
+        }
+      });
+      if (b == 0) {  // unaligned head / tail elements of the own chunk
+        const size_t he = cp0 * W < ce ? cp0 * W : ce;
+        const size_t ts = cp1 * W > he ? cp1 * W : he;
+        auto scalar = [&](size_t j) {
+          T lane[P];
+#pragma unroll
+          for (int q = 0; q < P; ++q) lane[q] = src[q][q == rank ? j : j - base];
+          const T zb = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+            if (q != rank) reinterpret_cast<T*>(a.xbar[q])[j] = zb;
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, snap_own[j], zb);
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+        };
+        for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
+        for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
+      }
+    }
+  }
+  if (a.phases & 2) {
+    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
+    trace_mark(a, b, 2);
+    if (ok) {
+      const T* zl = reinterpret_cast<const T*>(a.xbar[rank]);  // means pushed by their owners
+      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
+        [&](int c, size_t p0, size_t p1) {
+          T* dst = stage_ptr<T>(a, c, nxt, rank, P);
+          for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+            Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) {
+                const size_t j = pu * W;
+                vz[u] = ld_stream(zl + j);
+                vx[u] = ld_stream(x + j);
+                vg[u] = ld_stream(g + j);
+                if (load_m) vm[u] = ld_stream(m + j);
+                if (load_d) vd[u] = ld_stream(dl + j);
+                if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) {
+                const size_t j = pu * W;
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                  element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
+                st_plain(dst + soff(c, j), vx[u]);  // next-round contribution to owner c
+                st_stream(x + j, vx[u]);
+                if (f.c.use_mom) st_stream(m + j, vm[u]);
+                if (store_d) st_stream(dl + j, vd[u]);
+                st_stream(sn + j, vx[u]);
+              }
+            }
+          }
+        },
+        [&](int c, size_t j) {
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), zl[j]);
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+          stage_ptr<T>(a, c, nxt, rank, P)[soff(c, j)] = xv;
+        });
+      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
+  if (!VIRTUAL) publish_done(a);
+}
+
 // ------------------------------------------------------------------ dispatch
 template <int P>
 constexpr int unroll_for() { return P <= 2 ? 8 : (P <= 4 ? 4 : 2); }
@@ -965,6 +1194,40 @@ int launch_allreduce(int algo, int P, const CommArgs& a, dim3 grid, int threads,
 #undef LASGD_CASE
   LASGD_CUDA_TRY(cudaGetLastError());
   return LASGD_OK;
+}
+
+template <typename T, bool VIRTUAL>
+int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s) {
+#define LASGD_PCASE(PP)                                                                             \
+  case PP: {                                                                                        \
+    auto kern = k_push_round<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)>;                                    \
+    CommArgs aa = a;                                                                                \
+    if (!VIRTUAL) {                                                                                 \
+      const int cap = coop_capacity(kern, threads);                                                 \
+      if ((int)grid.x > cap) grid.x = cap;                                                          \
+      aa.nblocks = grid.x;                                                                          \
+    }                                                                                               \
+    return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                  \
+  }
+  switch (P) {
+    LASGD_PCASE(2)
+    LASGD_PCASE(3)
+    LASGD_PCASE(4)
+    LASGD_PCASE(5)
+    LASGD_PCASE(6)
+    LASGD_PCASE(7)
+    LASGD_PCASE(8)
+    default: return fail(LASGD_ERR_UNSUPPORTED, "push round needs 2 <= P <= %d, got %d", kMaxR, P);
+  }
+#undef LASGD_PCASE
+}
+
+size_t elem_bytes(int dtype);
+
+// Elements per staging slot: the largest chunk plus room for the 16-byte alignment shift.
+size_t push_stage_elems(size_t n, int P, int dtype) {
+  const size_t W = 16 / elem_bytes(dtype);
+  return (n + P - 1) / P + 2 * W;
 }
 
 int launch_any(int dtype, bool virt, int algo, int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
@@ -1083,6 +1346,53 @@ extern "C" int lasgd_fused_round_virtual(int P, int algo, void* const* x, const 
   return LASGD_OK;
 }
 
+extern "C" size_t lasgd_push_stage_elems(size_t n, int P, int dtype) { return push_stage_elems(n, P, dtype); }
+
+// K8 over P virtual ranks on one device: (init) staging launch, then phase A for every
+// rank, then phase B for every rank (stream order replaces the rank-level barriers).
+extern "C" int lasgd_fused_push_virtual(int P, void* const* x, const void* const* g, void* const* m,
+                                        void* const* delta, const void* const* snaps, void* const* snap_next,
+                                        void* const* xbars, void* const* stages, int cur, int init, size_t n,
+                                        int dtype, const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+                                        unsigned long long* nonfinite, void* stream) {
+  if (P < 2 || P > kMaxR) return fail(LASGD_ERR_UNSUPPORTED, "push round needs 2 <= P <= %d", kMaxR);
+  if (!x || !g || !snaps || !snap_next || !xbars || !stages) return fail(LASGD_ERR_INVALID_ARGUMENT, "null pointer array");
+  if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+  if (cur != 0 && cur != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "parity %d", cur);
+  int rc = check_fused_args(P, x, g, m, delta, snap_next, sgd, alpha, mode);
+  if (rc) return rc;
+  if (n == 0) return LASGD_OK;
+  if (nblocks <= 0) nblocks = 2 * num_sms();
+  CommArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < P; ++q) {
+    if (!snaps[q] || !xbars[q] || !stages[q] || !aligned16(snaps[q]) || !aligned16(xbars[q]) || !aligned16(stages[q]))
+      return fail(LASGD_ERR_INVALID_ARGUMENT, "rank %d buffers null or unaligned", q);
+    a.snap[q] = reinterpret_cast<const char*>(snaps[q]);
+    a.xbar[q] = reinterpret_cast<char*>(xbars[q]);
+    a.stage[q] = reinterpret_cast<char*>(stages[q]);
+  }
+  a.n = n;
+  a.nblocks = nblocks;
+  a.skip_signal_phase = -1;
+  a.stage_elems = push_stage_elems(n, P, dtype);
+  a.cur = cur;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int ph : {4, 1, 2}) {
+    if (ph == 4 && !init) continue;
+    a.phases = ph;
+    a.nonfinite = ph == 4 ? nullptr : nonfinite;
+    if (dtype == LASGD_F32)
+      rc = launch_push<float, true>(P, a, make_fused<float>(P, x, g, m, delta, snap_next, sgd, alpha, mode),
+                                    dim3(nblocks, P), 256, s);
+    else
+      rc = launch_push<double, true>(P, a, make_fused<double>(P, x, g, m, delta, snap_next, sgd, alpha, mode),
+                                     dim3(nblocks, P), 256, s);
+    if (rc) return rc;
+  }
+  return LASGD_OK;
+}
+
 // ====================================================================== communicator
 struct lasgd_comm {
   int rank = 0, world = 1, device = 0, dtype = LASGD_F32;
@@ -1092,7 +1402,10 @@ struct lasgd_comm {
   long long fault_seq = -1;
   int fault_phase = 0;
   char* base = nullptr;
-  size_t region_bytes = 0, off_snap[2] = {0, 0}, off_xbar = 0;
+  size_t region_bytes = 0, off_snap[2] = {0, 0}, off_xbar = 0, off_stage = 0, stage_elems = 0;
+  int push_slot = -1;            // staging parity that holds the current contributions (-1: none)
+  unsigned long long last_push = 0;  // launch whose end signals certify them
+  unsigned int* end_ctr = nullptr;   // [kDoneSlots] rank-level end-signal counters
   char* peer_base[kMaxR] = {nullptr};
   bool opened = false;
   bool poisoned = false;
@@ -1149,7 +1462,10 @@ extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int 
   c->off_snap[0] = round_up(kPadBytes, 4096);
   c->off_snap[1] = round_up(c->off_snap[0] + bytes, 4096);
   c->off_xbar = round_up(c->off_snap[1] + bytes, 4096);
-  c->region_bytes = round_up(c->off_xbar + bytes, (size_t)2 << 20);
+  // staging for the push round: [2 parities][world sources][stage_elems]
+  c->stage_elems = world > 1 ? push_stage_elems(n, world, dtype) : 0;
+  c->off_stage = round_up(c->off_xbar + bytes, 4096);
+  c->region_bytes = round_up(c->off_stage + 2 * (size_t)world * c->stage_elems * c->elem, (size_t)2 << 20);
   cudaError_t e = cudaMalloc(&c->base, c->region_bytes);
   if (e != cudaSuccess) {
     delete c;
@@ -1166,6 +1482,8 @@ extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int 
   if (e == cudaSuccess) e = cudaMemset(c->tile_ctr, 0, 2 * kDoneSlots * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->mid_ctr, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->mid_ctr, 0, kDoneSlots * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->end_ctr, kDoneSlots * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->end_ctr, 0, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->done_ctr, 0, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMalloc(&c->trace_buf, (size_t)kMaxB * 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->trace_buf, 0, (size_t)kMaxB * 4 * sizeof(unsigned long long));
@@ -1247,6 +1565,12 @@ extern "C" int lasgd_comm_peer_max_seq(lasgd_comm* c, unsigned long long* out) {
   return LASGD_OK;
 }
 
+extern "C" int lasgd_comm_invalidate_staging(lasgd_comm* c) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  c->push_slot = -1;
+  return LASGD_OK;
+}
+
 extern "C" int lasgd_comm_launches(lasgd_comm* c, unsigned long long* out) {
   if (!c || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
   *out = c->seq;
@@ -1324,6 +1648,10 @@ static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned lo
   a.done_ctr = c->done_ctr;
   a.tile_ctr = c->tile_ctr + 2 * (s % kDoneSlots);
   a.mid_ctr = c->mid_ctr + (s % kDoneSlots);
+  a.end_ctr = c->end_ctr + (s % kDoneSlots);
+  for (int r = 0; r < c->world; ++r) a.stage[r] = c->peer_base[r] + c->off_stage;
+  a.stage_elems = c->stage_elems;
+  a.cur = snap_slot;
   a.done_seq = c->done_dev;
   a.seq = s;
   a.nonfinite = nullptr;
@@ -1341,6 +1669,7 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
   int rc = prepare_launch(c, snap_slot, a, s);
   if (rc) return rc;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  c->push_slot = -1;  // the caller rewrote a snapshot slot: staged push contributions are stale
   rc = launch_any(c->dtype, false, algo, c->world, a, dim3(c->nblocks, 1), c->threads, cs);
   if (rc) return rc;
   LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
@@ -1352,8 +1681,10 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
                                       void* delta, const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                                       unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
-  algo = c->world == 1 ? LASGD_ALGO_ONESHOT : resolve_algo(algo, c->world, c->n * c->elem);
-  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
+  const bool push = algo == LASGD_ALGO_PUSH && c->world > 1;
+  if (!push) algo = c->world == 1 ? LASGD_ALGO_ONESHOT : resolve_algo(algo, c->world, c->n * c->elem);
+  if (!push && algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   void* xs[1] = {x};
   const void* gs[1] = {g};
   void* ms[1] = {m};
@@ -1370,11 +1701,43 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
   DeviceGuard dg(c->device);
   CommArgs a;
   unsigned long long s = 0;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (push) {
+    auto fl = make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode);
+    auto fd = make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode);
+    if (c->push_slot != snap_slot) {
+      // first push round (or after other use of the slots): stage the current snapshot's
+      // chunks at their owners (one extra launch, certified by its end signals)
+      rc = prepare_launch(c, snap_slot, a, s);
+      if (rc) return rc;
+      a.nblocks = nblocks;
+      a.phases = 4;
+      rc = c->dtype == LASGD_F32 ? launch_push<float, false>(c->world, a, fl, dim3(nblocks, 1), c->threads, cs)
+                                 : launch_push<double, false>(c->world, a, fd, dim3(nblocks, 1), c->threads, cs);
+      if (rc) return rc;
+      LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+      c->last_push = s;
+    }
+    rc = prepare_launch(c, snap_slot, a, s);
+    if (rc) return rc;
+    a.nblocks = nblocks;
+    a.nonfinite = nonfinite;
+    a.phases = 3;
+    a.prev_push = (uint32_t)c->last_push;
+    rc = c->dtype == LASGD_F32 ? launch_push<float, false>(c->world, a, fl, dim3(nblocks, 1), c->threads, cs)
+                               : launch_push<double, false>(c->world, a, fd, dim3(nblocks, 1), c->threads, cs);
+    if (rc) return rc;
+    c->last_push = s;
+    c->push_slot = 1 - snap_slot;
+    LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+    if (seq) *seq = s;
+    return LASGD_OK;
+  }
   rc = prepare_launch(c, snap_slot, a, s);
   if (rc) return rc;
   a.nblocks = nblocks;
   a.nonfinite = nonfinite;
-  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  c->push_slot = -1;  // this round writes the next snapshot without staging it
   if (c->dtype == LASGD_F32)
     rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, algo);
   else
@@ -1462,6 +1825,7 @@ extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
   if (c->done_ctr) cudaFree(c->done_ctr);
   if (c->tile_ctr) cudaFree(c->tile_ctr);
   if (c->mid_ctr) cudaFree(c->mid_ctr);
+  if (c->end_ctr) cudaFree(c->end_ctr);
   if (c->trace_buf) cudaFree(c->trace_buf);
   if (c->status_host) cudaFreeHost(c->status_host);
   if (c->base) cudaFree(c->base);

@@ -235,6 +235,7 @@ extern "C" int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* del
   // Algorithm 1 lines 1-5: snapshot = x0, submit round 0 (overlap pipeline)
   int rc = issue(w, K_SNAPSHOT, w->compute,
                  [&] { return lasgd_snapshot(w->snap[0], w->x, w->n, w->dtype, (void*)w->compute); });
+  if (!rc && comm) rc = lasgd_comm_invalidate_staging(comm);  // slot 0 rewritten: re-stage before a push round
   if (!rc && w->world > 1 && w->cfg.sync && w->cfg.pipeline == 0) rc = submit_allreduce(w, 0);
   if (rc) {
     lasgd_worker_destroy(w);

@@ -122,6 +122,30 @@ def fused_round_virtual(xs, gs, snaps, snap_nexts, lr: float, *, ms=None, deltas
             "fused_round_virtual")
 
 
+def push_stage_elems(n: int, P: int, dtype: torch.dtype = torch.float32) -> int:
+    return int(N.lib().lasgd_push_stage_elems(n, P, _DTYPES[dtype]))
+
+
+def fused_push_virtual(xs, gs, snaps, snap_nexts, xbars, stages, cur: int, init: bool, lr: float, *, ms=None,
+                       deltas=None, momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False, first_step=False,
+                       delta_reset=False, alpha: float = 1.0, mode: int = 0, nblocks: int = 0, nonfinite=None,
+                       stream=None) -> None:
+    """K8 (push round) for P ranks on one device; ``stages[r]`` holds
+    2 * P * push_stage_elems(n, P) elements."""
+    P = len(xs)
+    code, n = _check(*(list(xs) + list(gs) + list(snaps) + list(snap_nexts) + list(xbars) + list(ms or []) +
+                       list(deltas or [])))
+
+    def arr(ts):
+        return None if ts is None else (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
+
+    p = sgd_params(lr, momentum, dampening, weight_decay, nesterov, first_step, delta_reset)
+    N.check(N.lib().lasgd_fused_push_virtual(P, arr(xs), arr(gs), arr(ms), arr(deltas), arr(snaps), arr(snap_nexts),
+                                             arr(xbars), arr(stages), int(cur), int(bool(init)), n, code,
+                                             ctypes.byref(p), float(alpha), int(mode), int(nblocks), _ptr(nonfinite),
+                                             _stream(stream)), "fused_push_virtual")
+
+
 def mean_virtual(outs: Sequence[torch.Tensor], srcs: Sequence[torch.Tensor], algo: int = N.ALGO_ONESHOT,
                  nblocks: int = 0, nonfinite=None, stream=None) -> None:
     """Ring-order mean of P same-device contributions (collective.py:154-203)."""

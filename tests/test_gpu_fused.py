@@ -119,3 +119,53 @@ def test_fused_rejects_bad_arguments():
         K.fused_round_virtual([x], [x], [x], [x], 0.1, mode=1)  # finalize needs delta
     with pytest.raises(ValueError):
         K.fused_round_virtual([x], [x], [x], [x], 0.1, momentum=0.9)  # momentum needs m
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [7, 4099, 100_003])
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_push_round_multi_round_bit_exact(P, n, momentum):
+    """K8 over virtual ranks, 3 rounds (sync period 1): staging, parity flips and the
+    pushed means/contributions reproduce the oracle's deterministic loop bit for bit."""
+    rng = np.random.default_rng(P * 31 + n % 101)
+    steps = 3
+    x0 = rng.standard_normal(n).astype(np.float32)
+    grads = rng.standard_normal((steps, P, n)).astype(np.float32)
+    xs = [dev(x0.copy()) for _ in range(P)]
+    ms = [torch.zeros(n, device="cuda") for _ in range(P)] if momentum else None
+    snaps = [[dev(x0.copy()) for _ in range(P)], [torch.zeros(n, device="cuda") for _ in range(P)]]
+    xbars = [torch.zeros(n, device="cuda") for _ in range(P)]
+    se = K.push_stage_elems(n, P)
+    stages = [torch.full((2 * P * se,), float("nan"), device="cuda") for _ in range(P)]
+    cur = 0
+    for t in range(steps):
+        K.fused_push_virtual(xs, [dev(grads[t, r]) for r in range(P)], snaps[cur], snaps[1 - cur], xbars, stages, cur,
+                             t == 0, 0.05, ms=ms, momentum=momentum, weight_decay=1e-4 if momentum else 0.0,
+                             nesterov=bool(momentum), first_step=(t == 0), alpha=0.5, nblocks=5)
+        cur = 1 - cur
+    torch.cuda.synchronize()
+    cfg = O.SgdConfig(0.05, momentum, 0.0, 1e-4, True) if momentum else None
+    ref, _, _, _ = O.run_lasgd_pull(x0, grads, [0.05] * steps, P, 1, 0.5, sgd=cfg)
+    for r in range(P):
+        assert same_bits(xs[r].cpu().numpy(), ref[r]), (P, n, r)
+        assert same_bits(snaps[cur][r].cpu().numpy(), ref[r]), (P, n, r)
+
+
+def test_push_round_finalize_mode():
+    P, n = 3, 10_007
+    rng = np.random.default_rng(8)
+    x0 = rng.standard_normal(n).astype(np.float32)
+    grads = rng.standard_normal((2, P, n)).astype(np.float32)
+    xs = [dev(x0.copy()) for _ in range(P)]
+    ds = [torch.zeros(n, device="cuda") for _ in range(P)]
+    snaps = [[dev(x0.copy()) for _ in range(P)], [torch.zeros(n, device="cuda") for _ in range(P)]]
+    xbars = [torch.zeros(n, device="cuda") for _ in range(P)]
+    se = K.push_stage_elems(n, P)
+    stages = [torch.zeros(2 * P * se, device="cuda") for _ in range(P)]
+    for t in range(2):
+        K.fused_push_virtual(xs, [dev(grads[t, r]) for r in range(P)], snaps[t % 2], snaps[1 - t % 2], xbars, stages,
+                             t % 2, t == 0, 0.03, deltas=ds, delta_reset=(t > 0), mode=1)
+    torch.cuda.synchronize()
+    ref, _, _, _ = O.run_lasgd_delta(x0, grads, [0.03, 0.03], P, 1)
+    for r in range(P):
+        assert same_bits(xs[r].cpu().numpy(), ref[r])

@@ -80,7 +80,8 @@ def _w_worker_loop(rank, world, port):
     grads = np.stack([np.stack([_vec(100 * t + r, n) for r in range(world)]) for t in range(steps)])
     mom = L.SgdConfig(0.9, 0.0, 1e-4, True)
     cases = [(2, 1.0, None, "overlap", 1), (1, 0.5, mom, "overlap", 2), (3, 0.25, None, "overlap", 1),
-             (1, 1.0, mom, "fused", 1), (2, 0.5, None, "fused", 1), (1, 0.5, mom, "fused", 2), (3, 1.0, None, "fused", 2)]
+             (1, 1.0, mom, "fused", 1), (2, 0.5, None, "fused", 1), (1, 0.5, mom, "fused", 2), (3, 1.0, None, "fused", 2),
+             (1, 0.5, mom, "fused", 3), (2, 1.0, None, "fused", 3)]
     for k, alpha, sgd, pipe, algo in cases:
         comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
         x = torch.from_numpy(x0.copy()).cuda()
@@ -104,7 +105,7 @@ def _w_worker_loop(rank, world, port):
     x = torch.from_numpy(x0.copy()).cuda()
     g = torch.empty_like(x)
     xs, _, _, _ = O.run_lasgd_delta(x0, grads, np.full(steps, 0.05), world, 2)
-    for pipe, algo in (("overlap", 2), ("fused", 1), ("fused", 2)):
+    for pipe, algo in (("overlap", 2), ("fused", 1), ("fused", 2), ("fused", 3)):
         x = torch.from_numpy(x0.copy()).cuda()
         w = L.LASGDWorker(x, g, comm=comm, sync_period=2, lr=0.05, mode="delta", pipeline=pipe, algo=algo)
         for t in range(steps):

@@ -1,0 +1,75 @@
+// All-to-all NVLink probe on P GPUs (one process, peer access): every GPU moves S bytes
+// to/from each of its P-1 peers at the same time, with SM loads (pull) or SM stores (push).
+// Reports the per-GPU inbound (pull) / outbound (push) bandwidth.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o a2a_probe a2a_probe.cu
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+struct Ptrs { const uint4* src[8]; uint4* dst[8]; };
+
+// CTA b works for peer (b % (P-1)); pull: dst[local] <- src[peer]; push: dst[peer] <- src[local]
+__global__ void k_a2a(Ptrs p, int npeers, size_t n16) {
+  const int peer = blockIdx.x % npeers;
+  const int cta = blockIdx.x / npeers, nct = gridDim.x / npeers;
+  const uint4* s = p.src[peer];
+  uint4* d = p.dst[peer];
+  size_t i = (size_t)cta * blockDim.x + threadIdx.x, st = (size_t)nct * blockDim.x;
+  for (; i + 3 * st < n16; i += 4 * st) {
+    uint4 v0 = __ldcg(s + i), v1 = __ldcg(s + i + st), v2 = __ldcg(s + i + 2 * st), v3 = __ldcg(s + i + 3 * st);
+    __stcg(d + i, v0); __stcg(d + i + st, v1); __stcg(d + i + 2 * st, v2); __stcg(d + i + 3 * st, v3);
+  }
+  for (; i < n16; i += st) __stcg(d + i, __ldcg(s + i));
+}
+
+int main() {
+  int P = 0;
+  cudaGetDeviceCount(&P);
+  if (P < 2) { printf("need >= 2 GPUs\n"); return 0; }
+  const size_t S = (size_t)256 << 20;  // bytes per peer pair
+  char* in[8]; char* out[8];
+  cudaStream_t st[8]; cudaEvent_t e0[8], e1[8];
+  for (int d = 0; d < P; ++d) {
+    CK(cudaSetDevice(d));
+    for (int q = 0; q < P; ++q) if (q != d) CK(cudaDeviceEnablePeerAccess(q, 0));
+    CK(cudaMalloc(&in[d], S * P));
+    CK(cudaMalloc(&out[d], S * P));
+    CK(cudaMemset(in[d], 1, S * P));
+    CK(cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0[d])); CK(cudaEventCreate(&e1[d]));
+  }
+  for (int mode = 0; mode < 2; ++mode) {
+    for (int ctas : {148, 296}) {
+      float best = 1e9;
+      for (int rep = 0; rep < 4; ++rep) {
+        for (int d = 0; d < P; ++d) {
+          Ptrs p;
+          int k = 0;
+          for (int q = 0; q < P; ++q) {
+            if (q == d) continue;
+            if (mode == 0) { p.src[k] = (const uint4*)(in[q] + S * d); p.dst[k] = (uint4*)(out[d] + S * q); }
+            else { p.src[k] = (const uint4*)(in[d] + S * q); p.dst[k] = (uint4*)(out[q] + S * d); }
+            ++k;
+          }
+          CK(cudaSetDevice(d));
+          CK(cudaEventRecord(e0[d], st[d]));
+          k_a2a<<<ctas / (P - 1) * (P - 1), 512, 0, st[d]>>>(p, P - 1, S / 16);
+          CK(cudaEventRecord(e1[d], st[d]));
+        }
+        float ms = 0;
+        for (int d = 0; d < P; ++d) {
+          CK(cudaSetDevice(d));
+          CK(cudaEventSynchronize(e1[d]));
+          float t; CK(cudaEventElapsedTime(&t, e0[d], e1[d]));
+          ms = t > ms ? t : ms;
+        }
+        if (rep && ms < best) best = ms;
+      }
+      printf("{\"P\": %d, \"mode\": \"%s\", \"ctas\": %d, \"GBps_per_gpu\": %.1f}\n", P, mode ? "push_stores" : "pull_loads",
+             ctas, (double)S * (P - 1) / (best * 1e-3) / 1e9);
+      fflush(stdout);
+    }
+  }
+  return 0;
+}
