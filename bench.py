@@ -450,7 +450,7 @@ def main():
             barrier()
 
             def ar():
-                seq = comm.allreduce(0, algo_code, stream=compute)
+                seq = comm.allreduce(0, algo_code if algo_code != N.ALGO_PUSH else N.ALGO_AUTO, stream=compute)
                 return seq
 
             iso["allreduce"] = timeit(ar, reps=10)

@@ -1227,7 +1227,8 @@ size_t elem_bytes(int dtype);
 // Elements per staging slot: the largest chunk plus room for the 16-byte alignment shift.
 size_t push_stage_elems(size_t n, int P, int dtype) {
   const size_t W = 16 / elem_bytes(dtype);
-  return (n + P - 1) / P + 2 * W;
+  const size_t e = (n + P - 1) / P + 2 * W;
+  return (e + 63) / 64 * 64;  // every slot starts 16-byte (in fact 256-byte) aligned
 }
 
 int launch_any(int dtype, bool virt, int algo, int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
