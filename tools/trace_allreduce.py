@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--sizes-mb", default="16,102.228128,1024")
     ap.add_argument("--nblocks", default="64,128")
     ap.add_argument("--fused", action="store_true", help="trace the fused round kernel (K7) instead of K2/K3")
+    ap.add_argument("--algos", default="1,2", help="1 one-shot, 2 two-shot, 3 push (fused only)")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -63,7 +64,7 @@ def main():
             return r
         for nb in [int(v) for v in a.nblocks.split(",")]:
             comm.set_nblocks(nb)
-            for algo in (N.ALGO_ONESHOT, N.ALGO_TWOSHOT):
+            for algo in [int(v) for v in a.algos.split(",")]:
                 with torch.cuda.stream(s):
                     for i in range(4):
                         launch(algo, nb)
