@@ -73,7 +73,7 @@ def parse():
     return ap.parse_args()
 
 
-def config_dict(args, world):
+def config_dict(args, world, fused_algo=None):
     return {
         "workload": f"{args.model}-lasgd-sync",
         "params": MODELS[args.model]["params"],
@@ -82,6 +82,7 @@ def config_dict(args, world):
         "alpha": args.alpha,
         "local_step": "sgd momentum=0.9 nesterov weight_decay=1e-4 lr=0.1",
         "allreduce": args.algo,
+        "fused_round_algo": fused_algo,
         "pipeline": args.pipeline,
         "sm_budget_ctas": args.nblocks,
         "parallelism": f"dp{world}",
@@ -155,10 +156,11 @@ def kernel_bytes(name, n, world, comm, algo_code, sgd_momentum=True):
     if name == "fused_round":
         hbm = (7 if world > 1 else 6) * B  # read x,g,m(,own snap); write x,m,next snap
         nvl = (world - 1) * B  # one-shot: every peer's whole snapshot over NVLink
-        if world > 1 and algo_code == 3:  # push: 2(P-1)/P*B out as stores; staged reads + landing writes in HBM
+        fa = comm.resolve_fused_algo(algo_code) if world > 1 else 1
+        if fa == 3:  # push: 2(P-1)/P*B out as stores; staged reads + landing writes in HBM
             nvl = comm.bytes_per_node(2)
             hbm += 2 * nvl
-        elif world > 1 and comm.resolve_algo(algo_code) == 2:  # two-shot: RS in + AG in, own chunk mean via HBM
+        elif fa == 2:  # two-shot: RS in + AG in, own chunk mean via HBM
             nvl = comm.bytes_per_node(2)
             hbm += 2 * B // world
         if nvl / NVLINK_PEAK_GBS > hbm / peaks()[0]:
@@ -354,11 +356,14 @@ def main():
     w.reset_records()
     with torch.cuda.stream(compute):
         e0.record(compute)
+        h0 = time.perf_counter()
         run_sync_path(w, args.steps, lambda t: grads[t % 2])
+        host_issue_ms = (time.perf_counter() - h0) * 1e3
         w.drain()
         e1.record(compute)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1))
+    host_issue_ms = max_over_ranks(host_issue_ms)
     launches = sum(w.launches.values())
     barrier()
 
@@ -517,9 +522,11 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "host_issue_ms_per_step": host_issue_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": config_dict(args, world),
+            "config": config_dict(args, world, {1: "oneshot", 2: "twoshot", 3: "push"}.get(
+                comm.resolve_fused_algo(algo_code) if comm is not None else 1)),
             "roofline": roofline,
             "cpu_baseline": cpu_base,
             "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,

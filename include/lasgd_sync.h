@@ -169,7 +169,11 @@ int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, u
  * lasgd_finalize under the same schedule; launched on `stream` with `nblocks` CTAs
  * (<= 0: the communicator's budget), `algo` one-shot (every peer's whole snapshot) or
  * two-shot (reduce-scatter of the own chunk, per-CTA mid barrier, then the pull reads
- * each chunk's mean from its owner); a launch like lasgd_comm_allreduce (same
+ * each chunk's mean from its owner) or PUSH (K8: each owner reduces contributions
+ * staged in its own HBM by the previous round and pushes the chunk mean to every
+ * peer; the next snapshot's chunks are pushed to their owners; the first push round
+ * after any other use of the slots adds one staging launch); AUTO = see
+ * lasgd_comm_resolve_fused_algo.  A launch like lasgd_comm_allreduce (same
  * sequence numbers, query / wait / stream_wait apply). */
 int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, void* x, const void* g, void* m, void* delta,
                            const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
@@ -193,6 +197,9 @@ int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len);
 /* NVLink bytes this rank's peers read from it in one launch (collective.py:206-226 analogue). */
 unsigned long long lasgd_comm_bytes_per_node(lasgd_comm* c, int algo);
 int lasgd_comm_resolve_algo(lasgd_comm* c, int algo);
+/* The algorithm lasgd_comm_fused_round runs for `algo`: AUTO resolves to one-shot where
+ * the all-reduce would be one-shot and to PUSH where it would be two-shot. */
+int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo);
 /* Change the SM budget (CTAs per launch) for subsequent launches; every rank must
  * make the same call between the same two launches. */
 int lasgd_comm_set_nblocks(lasgd_comm* c, int nblocks);

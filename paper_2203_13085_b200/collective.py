@@ -395,6 +395,10 @@ class P2PCommunicator:
     def resolve_algo(self, algo: int = N.ALGO_AUTO) -> int:
         return N.lib().lasgd_comm_resolve_algo(self._h, algo)
 
+    def resolve_fused_algo(self, algo: int = N.ALGO_AUTO) -> int:
+        """Algorithm fused_round runs for `algo` (AUTO -> one-shot or push)."""
+        return N.lib().lasgd_comm_resolve_fused_algo(self._h, algo)
+
     def set_nblocks(self, nblocks: int) -> None:
         """SM budget of later launches (collective: every rank must call it identically)."""
         N.check(N.lib().lasgd_comm_set_nblocks(self._h, int(nblocks)), "set_nblocks")

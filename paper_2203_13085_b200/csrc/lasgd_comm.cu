@@ -28,6 +28,10 @@
 #include <string.h>
 #include <time.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "lasgd_common.cuh"
 
 namespace lasgd {
@@ -873,9 +877,22 @@ int launch_kernel(bool coop, void (*kernel)(Args...), dim3 grid, int threads, cu
 
 template <typename... Args>
 int coop_capacity(void (*kernel)(Args...), int threads) {
+  // cached per (kernel, threads): an occupancy query per launch costs host time every step
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), threads);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
-  return per_sm * num_sms();
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int cap = per_sm * num_sms();
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = cap;
+  return cap;
 }
 
 template <typename T, bool VIRTUAL>
@@ -1252,6 +1269,16 @@ int resolve_algo(int algo, int P, size_t bytes) {
   return bytes <= cutoff ? LASGD_ALGO_ONESHOT : LASGD_ALGO_TWOSHOT;
 }
 
+// Fused round (K7/K8): where the all-reduce would be two-shot, the push round moves
+// the same NVLink bytes with stores only and no entry wait on peers' snapshots
+// (measured ~3% faster per round at P=4, profiles/bench_r01_push_*.json).
+int resolve_fused_algo(int algo, int P, size_t bytes) {
+  if (P <= 1) return LASGD_ALGO_ONESHOT;
+  if (algo != LASGD_ALGO_AUTO) return algo;
+  const int a = resolve_algo(algo, P, bytes);
+  return a == LASGD_ALGO_TWOSHOT ? LASGD_ALGO_PUSH : a;
+}
+
 }  // namespace lasgd
 
 using namespace lasgd;
@@ -1545,6 +1572,11 @@ extern "C" int lasgd_comm_resolve_algo(lasgd_comm* c, int algo) {
   return resolve_algo(algo, c->world, c->n * c->elem);
 }
 
+extern "C" int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  return resolve_fused_algo(algo, c->world, c->n * c->elem);
+}
+
 // Highest launch sequence number any peer has started, read from the entry flags the
 // peers' CTAs wrote into this rank's signal pad.  Uses a private non-blocking stream,
 // so it never waits behind the caller's (possibly stalled) streams.
@@ -1682,8 +1714,8 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
                                       void* delta, const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                                       unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
-  const bool push = algo == LASGD_ALGO_PUSH && c->world > 1;
-  if (!push) algo = c->world == 1 ? LASGD_ALGO_ONESHOT : resolve_algo(algo, c->world, c->n * c->elem);
+  algo = resolve_fused_algo(algo, c->world, c->n * c->elem);
+  const bool push = algo == LASGD_ALGO_PUSH;
   if (!push && algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT)
     return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   void* xs[1] = {x};
