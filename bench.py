@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--pipeline", choices=["overlap", "fused"], default="fused",
                     help="overlap: K5 | K4 | K2/K3 on a side stream; fused: one K7 pass per round boundary")
     ap.add_argument("--fused-nblocks", type=int, default=0, help="CTAs of the fused kernel (0 = 2 per SM)")
-    ap.add_argument("--train-steps", type=int, default=10)
+    ap.add_argument("--train-steps", type=int, default=30)
     ap.add_argument("--train-warmup", type=int, default=4)
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -604,6 +604,45 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         w.close()
         return ms, hist
 
+    def train_sgd_ar(steps, warm, nccl):
+        import torch.distributed as dist
+
+        from paper_2203_13085_b200 import kernels as K
+
+        with torch.cuda.stream(compute):
+            if nccl:
+                flat.bind_grads(own_g)
+                m = torch.empty_like(flat.x)
+                clock = [0]
+
+                def update():
+                    dist.all_reduce(flat.g, op=dist.ReduceOp.AVG)
+                    K.sgd_step(flat.x, flat.g, lr, m=m, momentum=sgd.momentum, weight_decay=sgd.weight_decay,
+                               nesterov=sgd.nesterov, first_step=clock[0] == 0, stream=compute)
+                    clock[0] += 1
+            else:
+                update = L.SGDARWorker(flat.x, comm=comm, sgd=sgd, lr=lr, compute_stream=compute, flat=flat).step
+
+            def one():
+                flat.zero_grad()
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    loss = lossf(model(images), labels)
+                loss.backward()
+                update()
+
+            for _ in range(warm):
+                one()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(compute):
+            a.record(compute)
+            for _ in range(steps):
+                one()
+            b.record(compute)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b)) / steps
+
     out = {"model": f"{spec['ctor']} (torchvision, random init, {hw}x{hw}, {spec['classes']} classes)",
            "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params", "steps": args.train_steps}
     t_nosync, _ = train(args.train_steps, args.train_warmup, sync=False)
@@ -616,6 +655,15 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         if kw.get("adaptive"):
             out[name]["tau_histogram"] = {str(k): v for k, v in sorted(hist.items())}
     out["nosync"] = {"images_per_s": world * args.batch / (t_nosync / 1e3), "ms_per_step": t_nosync}
+    if comm is not None:
+        # SGD-AR (optimizer.py:214-242): gradient mean every step, on the same P2P
+        # all-reduce (grads written by backward into the registered slots) and on NCCL
+        own_g = flat.g
+        for name in ("sgd_ar", "sgd_ar_nccl"):
+            t = train_sgd_ar(args.train_steps, args.train_warmup, name == "sgd_ar_nccl")
+            out[name] = {"images_per_s": world * args.batch / (t / 1e3), "ms_per_step": t,
+                         "exposed_sync_ms_per_step": t - t_nosync, "exposed_sync_frac": (t - t_nosync) / t}
+        flat.bind_grads(own_g)
     main = out[args.pipeline]
     out["images_per_s_lasgd"] = main["images_per_s"]
     out["images_per_s_nosync"] = out["nosync"]["images_per_s"]

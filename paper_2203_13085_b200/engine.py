@@ -249,3 +249,73 @@ class LASGDWorker:
             self.close()
         except Exception:
             pass
+
+
+class SGDARWorker:
+    """SGD-AR baseline (optimizer.py:214-242, ``sync_allreduce_sgd_round``) per process.
+
+    Backward writes the gradient straight into one of the communicator's registered
+    snapshot slots (``grad_buffer``), ``step()`` then launches the NVLink mean
+    all-reduce of the gradients (K2/K3, the reference ring's per-chunk order, so the
+    mean and therefore every replica's model stay bit-identical) and K5 with the mean
+    gradient, both on the compute stream: the synchronous data-parallel step LASGD is
+    compared against (Table 4).
+
+    The slots alternate per step: peers may still be reading this step's slot while
+    this rank runs the next backward; the slot is rewritten two steps later, after the
+    next all-reduce's entry barrier has proved every peer finished this one.  Pass
+    ``flat`` (FlatParams) to have ``.grad`` rebound to the current slot automatically."""
+
+    def __init__(self, x: torch.Tensor, *, comm=None, sgd: Optional[SgdConfig] = None,
+                 schedule: Optional[LrSchedule] = None, lr: Optional[float] = None, algo: int = N.ALGO_AUTO,
+                 compute_stream: Optional[torch.cuda.Stream] = None, flat=None):
+        if (schedule is None) == (lr is None):
+            raise ValueError("give exactly one of schedule / lr")
+        if algo == N.ALGO_PUSH:
+            raise ValueError("the push algorithm exists only as a fused LASGD round")
+        self.sgd = sgd or SgdConfig()
+        self.sgd.validate()
+        K._check(x)
+        self.x, self.comm, self.algo = x, comm, algo
+        self.schedule, self.lr = schedule, lr
+        self.compute = compute_stream if compute_stream is not None else torch.cuda.current_stream(x.device)
+        if comm is not None and (comm.n != x.numel() or comm.dtype != x.dtype):
+            raise ValueError("communicator buffers do not match x")
+        self._bufs = comm.snapshots if comm is not None else [torch.zeros_like(x)]
+        self._slot = 0
+        self.flat = flat
+        self.m = torch.empty_like(x) if self.sgd.momentum != 0 else None
+        self._finite = _FiniteMonitor(x.device)
+        self.local_clock = 0
+        self.launches = collections.Counter()
+        if flat is not None:
+            flat.bind_grads(self.grad_buffer)
+
+    @property
+    def grad_buffer(self) -> torch.Tensor:
+        """Where the next backward must write its gradient."""
+        return self._bufs[self._slot]
+
+    def current_lr(self) -> float:
+        return self.lr if self.schedule is None else lr_at(self.schedule, self.local_clock)
+
+    def step(self) -> None:
+        """Mean of every rank's ``grad_buffer`` then ``x = K5(x, mean)`` (call on the
+        compute stream after backward; every rank must call it the same number of times)."""
+        g = self.grad_buffer
+        if self.comm is not None:
+            self.comm.allreduce(self._slot, self.algo, stream=self.compute)
+            self.launches["allreduce"] += 1
+            g = self.comm.xbar
+            self._slot ^= 1
+        s = self.sgd
+        K.sgd_step(self.x, g, self.current_lr(), m=self.m, momentum=s.momentum, dampening=s.dampening,
+                   weight_decay=s.weight_decay, nesterov=s.nesterov, first_step=self.local_clock == 0,
+                   nonfinite=self._finite.counter, stream=self.compute)
+        self.launches["sgd_step"] += 1
+        self.local_clock += 1
+        if self.flat is not None and self.comm is not None:
+            self.flat.bind_grads(self.grad_buffer)
+
+    def check_finite(self) -> None:
+        self._finite.check(self.x.numel())

@@ -26,6 +26,7 @@ class FlatParams:
         self.x = torch.empty(self.numel, dtype=dtype, device=device)
         self.g = torch.zeros(self.numel, dtype=dtype, device=device)
         self.params = params
+        self.channels_last = channels_last
         self.offsets = []
         off = 0
         with torch.no_grad():
@@ -48,6 +49,15 @@ class FlatParams:
             o, i, h, w = shape
             return flat.view(o, h, w, i).permute(0, 3, 1, 2)  # NHWC storage, NCHW shape
         return flat.view(shape)
+
+    def bind_grads(self, buf: torch.Tensor) -> None:
+        """Point every ``.grad`` into ``buf`` (e.g. a communicator's registered slot, so
+        backward writes the all-reduce input in place)."""
+        if buf.dtype != self.x.dtype or buf.numel() != self.numel or not buf.is_contiguous():
+            raise ValueError("gradient buffer must be a contiguous vector like x")
+        for p, off in zip(self.params, self.offsets):
+            p.grad = self._view(buf, off, p.shape, self.channels_last)
+        self.g = buf
 
     def zero_grad(self) -> None:
         """One memset over the flat gradient buffer (grads stay attached as views)."""

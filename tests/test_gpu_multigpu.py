@@ -141,6 +141,56 @@ def _w_worker_loop(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_sgd_ar(rank, world, port):
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+
+    _init(rank, world, port)
+    n, steps = 65_541, 7
+    x0 = _vec(3, n)
+    grads = np.stack([np.stack([_vec(500 * t + r, n) for r in range(world)]) for t in range(steps)])
+    etas = np.array([0.1, 0.05, 0.2, 0.01, 0.07, 0.03, 0.11])
+    for sgd in (None, L.SgdConfig(0.9, 0.0, 1e-4, True)):
+        for algo in (1, 2):
+            comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
+            x = torch.from_numpy(x0.copy()).cuda()
+            compute = torch.cuda.Stream()
+            with torch.cuda.stream(compute):
+                w = L.SGDARWorker(x, comm=comm, sgd=sgd, lr=1.0, algo=algo, compute_stream=compute)
+                for t in range(steps):
+                    w.lr = float(etas[t])
+                    w.grad_buffer.copy_(torch.from_numpy(grads[t, rank]))
+                    w.step()
+            torch.cuda.synchronize()
+            cfg = None if sgd is None else O.SgdConfig(1.0, sgd.momentum, sgd.dampening, sgd.weight_decay,
+                                                       sgd.nesterov)
+            ref, _ = O.run_sgd_ar(x0, grads, etas, world, sgd=cfg)
+            assert _same_bits(x.cpu().numpy(), ref), (sgd, algo, rank)
+            dist.barrier()
+            comm.close()
+    # gradients written by backward straight into the registered slots (FlatParams rebinding)
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(torch.nn.Linear(32, 16), torch.nn.Tanh(), torch.nn.Linear(16, 1)).cuda()
+    flat = L.FlatParams(model)
+    comm = L.P2PCommunicator(flat.numel, nblocks=8, timeout_s=20.0)
+    w = L.SGDARWorker(flat.x, comm=comm, lr=0.05, flat=flat)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(10 + rank)
+    for _ in range(5):
+        flat.zero_grad()
+        model(torch.randn(8, 32, device="cuda", generator=gen)).square().mean().backward()
+        w.step()
+    torch.cuda.synchronize()
+    xs = [torch.empty_like(flat.x) for _ in range(world)]
+    dist.all_gather_object(xs, flat.x.cpu())
+    assert all(torch.equal(xs[0], v) for v in xs), "SGD-AR replicas diverged"
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def _w_fault(rank, world, port):
     import torch.distributed as dist
 
@@ -182,6 +232,11 @@ def test_p2p_allreduce_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_worker_round_protocol_bit_exact():
     _spawn(_w_worker_loop)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_sgd_ar_worker_bit_exact():
+    _spawn(_w_sgd_ar)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")

@@ -88,6 +88,18 @@ def test_pull_loop_bit_exact_f64(golden_pulls):
             assert np.array_equal(np.stack(hist[t]), c["xs_hist"][t]), (tag, t)
 
 
+def test_sgd_ar_loop_bit_exact_f64():
+    """run_sgd_ar vs the reference's sync_allreduce_sgd_round (tests/golden/sgd_ar.npz)."""
+    import os
+
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "sgd_ar.npz")))
+    P = g["grads"].shape[1]
+    for t in range(1, len(g["etas"]) + 1):
+        x, means = O.run_sgd_ar(g["x0"], g["grads"][:t], g["etas"][:t], P)
+        assert np.array_equal(x, g["x_hist"][t - 1]), t
+        assert np.array_equal(means[-1], g["mean_hist"][t - 1]), t
+
+
 def test_alpha1_pull_close_to_reference_finalize(golden_loops):
     """x - (snap - z) vs z + delta: equal up to rounding."""
     for tag, c in loop_cases(golden_loops, "abe"):
