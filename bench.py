@@ -8,15 +8,17 @@ the other BASELINE configs.  A "step" is one pass of the hot path over one
 minibatch's synthetic gradient under the deterministic schedule (sync period 1,
 the paper's tau_max = 1): the local step (Nesterov momentum 0.9, weight decay
 1e-4 — PAPER.md:229) and the round boundary — mean of every rank's snapshot
-over NVLink, elastic pull, next snapshot.  Default `--pipeline fused`: one K7
-kernel per boundary step; `--pipeline overlap`: K5, then K4 with the K2/K3
-all-reduce on a low-priority side stream.  images/s = images whose gradients
-the sync path consumed per second over all ranks.
+over NVLink, elastic pull, next snapshot.  Default `--pipeline fused`: one
+kernel per boundary step (K7 one-shot at P=2, K8 push round at P>=3 — `--algo`
+overrides); `--pipeline overlap`: K5, then K4 with the K2/K3 all-reduce on a
+low-priority side stream.  images/s = images whose gradients the sync path
+consumed per second over all ranks.
 
 Also reported (not the headline): the real training step (forward/backward in
 PyTorch, bf16 autocast, channels_last) with the sync path under each pipeline,
-adaptive completion (tau histogram), and sync disabled (the no-sync ceiling) ->
-exposed sync ms/step.
+adaptive completion (tau histogram), the SGD-AR baseline (gradient mean every
+step, on the same P2P all-reduce and on NCCL), and sync disabled (the no-sync
+ceiling) -> exposed sync ms/step.
 
 `--impl reference` times the reference's own CPU algorithm (f64, delta
 bookkeeping, ring-order mean; the C restatement in oracle/, all host threads,
