@@ -70,6 +70,7 @@ def parse():
     ap.add_argument("--train-steps", type=int, default=30)
     ap.add_argument("--train-warmup", type=int, default=4)
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="training leg: eager fwd/bwd instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernels-only", action="store_true", help="short run for ncu: sync path only")
     return ap.parse_args()
@@ -574,6 +575,18 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     labels = torch.randint(0, spec["classes"], (args.batch,), device=dev, generator=gen)
     lossf = torch.nn.CrossEntropyLoss()
 
+    def fwd_bwd_eager():
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+            loss = lossf(model(images), labels)
+        loss.backward()
+
+    if args.no_graphs:
+        def fwd_bwd():
+            flat.zero_grad()
+            fwd_bwd_eager()
+    else:
+        fwd_bwd = L.GraphedStep(flat, fwd_bwd_eager)  # one CUDA graph per gradient buffer
+
     def train(steps, warm, **wkw):
         with torch.cuda.stream(compute):
             w = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=args.sync_period, alpha=args.alpha, mode="pull",
@@ -581,10 +594,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
                               fused_nblocks=args.fused_nblocks, **wkw)
 
             def one():
-                flat.zero_grad()
-                with torch.autocast("cuda", dtype=torch.bfloat16):
-                    loss = lossf(model(images), labels)
-                loss.backward()
+                fwd_bwd()
                 w.step()
 
             for _ in range(warm):
@@ -626,10 +636,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
                 update = L.SGDARWorker(flat.x, comm=comm, sgd=sgd, lr=lr, compute_stream=compute, flat=flat).step
 
             def one():
-                flat.zero_grad()
-                with torch.autocast("cuda", dtype=torch.bfloat16):
-                    loss = lossf(model(images), labels)
-                loss.backward()
+                fwd_bwd()
                 update()
 
             for _ in range(warm):
@@ -646,7 +653,8 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         return max_over_ranks(a.elapsed_time(b)) / steps
 
     out = {"model": f"{spec['ctor']} (torchvision, random init, {hw}x{hw}, {spec['classes']} classes)",
-           "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params", "steps": args.train_steps}
+           "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params", "steps": args.train_steps,
+           "fwd_bwd": "eager" if args.no_graphs else "cuda_graph (zero_grad+fwd+bwd captured once per gradient buffer)"}
     t_nosync, _ = train(args.train_steps, args.train_warmup, sync=False)
     runs = {"fused": dict(pipeline="fused"), "overlap": dict(pipeline="overlap"),
             "overlap_adaptive": dict(pipeline="overlap", adaptive=True, tau_max=5)}

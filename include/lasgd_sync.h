@@ -214,6 +214,16 @@ int lasgd_comm_destroy(lasgd_comm* c);
  * wrote into this rank's signal pad); used to drain adaptive runs without a host
  * collective.  Never waits behind the caller's streams. */
 int lasgd_comm_peer_max_seq(lasgd_comm* c, unsigned long long* out);
+/* 1 if some peer has already entered an all-reduce launch later than `seq` (this rank
+ * is the laggard of that round: its launch `seq` is complete or about to be), else 0.
+ * Reads the peers' entry flags of CTA 0 (32 bytes) on a private non-blocking stream.
+ * Used by the adaptive schedule to close a round without another local step. */
+int lasgd_comm_peers_ahead(lasgd_comm* c, unsigned long long seq);
+/* on = 1: every lasgd_comm_allreduce launch is preceded (same stream) by a one-warp
+ * gate kernel that waits until every peer reached the same launch, so a side-stream
+ * all-reduce never holds a CTA per SM while a late peer catches up (which would
+ * starve the compute stream).  Collective setting: every rank must use the same. */
+int lasgd_comm_set_gate(lasgd_comm* c, int on);
 /* The caller rewrote a snapshot slot outside the push round: the next push round
  * re-stages the current snapshot first. */
 int lasgd_comm_invalidate_staging(lasgd_comm* c);

@@ -26,6 +26,7 @@ from .collective import (  # noqa: E402
     ring_schedule,
 )
 from .engine import LASGDWorker, SGDARWorker  # noqa: E402
+from .graphs import GraphedStep  # noqa: E402
 from .flat import FlatParams  # noqa: E402
 from .optimizer import (  # noqa: E402
     HyperParamError,
@@ -44,7 +45,7 @@ from .problems import LrSchedule, lr_at  # noqa: E402
 
 __all__ = [
     "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
-    "DimensionMismatchError", "FlatParams", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "ModelDivergenceError",
+    "DimensionMismatchError", "FlatParams", "GraphedStep", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "ModelDivergenceError",
     "NodeState", "NonFiniteError", "P2PCommunicator", "SGDARWorker", "SgdConfig", "Status", "TickAction", "TransportFault",
     "all_reduce_average", "as_device_vector", "blend", "bytes_per_node", "lasgd_finalize_round", "lasgd_node_tick",
     "lr_at", "partition_chunks", "poll", "require_same_dim", "ring_schedule", "sgd_local_step", "sync_allreduce_sgd_round",

@@ -406,6 +406,14 @@ class P2PCommunicator:
     def set_trace(self, on: bool) -> None:
         N.check(N.lib().lasgd_comm_set_trace(self._h, int(bool(on))))
 
+    def set_gate(self, on: bool) -> None:
+        """Gate every all-reduce behind a one-warp wait for all peers (collective setting)."""
+        N.check(N.lib().lasgd_comm_set_gate(self._h, int(bool(on))))
+
+    def peers_ahead(self, seq: int) -> bool:
+        """True if some peer already entered a launch later than ``seq``."""
+        return bool(N.check(N.lib().lasgd_comm_peers_ahead(self._h, seq)))
+
     def read_trace(self):
         """Per-CTA globaltimer stamps (ns) of the last traced launch: list of
         (start, entry_passed, mid_passed, end); synchronises the device."""

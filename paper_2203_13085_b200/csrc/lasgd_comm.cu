@@ -311,6 +311,19 @@ __device__ bool rank_barrier(const CommArgs& a, int b, int rank) {
   return rank_wait<P>(a, 0, a.epoch, b, rank);
 }
 
+// Launch gate (one warp, launched in stream order just before a side-stream
+// all-reduce): announce launch `epoch` to every peer (rank-level slot kind 2), then
+// wait until every peer announced it too.  A wide all-reduce kernel whose peers are
+// late spins in its entry barrier holding a CTA on most SMs, which starves the
+// compute stream's large forward/backward CTAs; behind the gate it only starts once
+// every peer is about to start as well, and the waiting costs one warp.
+template <int P>
+__global__ void __launch_bounds__(32) k_gate(CommArgs a) {
+  const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)2 * kMaxR;
+  if (threadIdx.x < P) st_release_sys(a.pad[threadIdx.x] + slot + a.rank, a.epoch);
+  rank_wait<P>(a, 2, a.epoch, 0, a.rank);
+}
+
 // Aligned body of chunk c in packs, [cp0, cp1), plus its unaligned head/tail elements.
 template <typename T, int P>
 __device__ __forceinline__ void chunk_packs(size_t n, int c, size_t& cs, size_t& ce, size_t& cp0, size_t& cp1) {
@@ -1258,6 +1271,21 @@ int launch_any(int dtype, bool virt, int algo, int P, const CommArgs& a, dim3 gr
   return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
 }
 
+int launch_gate(int P, const CommArgs& a, cudaStream_t s) {
+  switch (P) {
+    case 2: k_gate<2><<<1, 32, 0, s>>>(a); break;
+    case 3: k_gate<3><<<1, 32, 0, s>>>(a); break;
+    case 4: k_gate<4><<<1, 32, 0, s>>>(a); break;
+    case 5: k_gate<5><<<1, 32, 0, s>>>(a); break;
+    case 6: k_gate<6><<<1, 32, 0, s>>>(a); break;
+    case 7: k_gate<7><<<1, 32, 0, s>>>(a); break;
+    case 8: k_gate<8><<<1, 32, 0, s>>>(a); break;
+    default: return fail(LASGD_ERR_UNSUPPORTED, "gate needs 2 <= P <= %d, got %d", kMaxR, P);
+  }
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
+
 size_t elem_bytes(int dtype) { return dtype == LASGD_F64 ? 8 : 4; }
 
 // One-shot reads (P-1)*B per rank, two-shot 2(P-1)/P*B plus one extra barrier
@@ -1446,6 +1474,7 @@ struct lasgd_comm {
   unsigned int* mid_ctr = nullptr;         // [kDoneSlots] rank-level barrier counters
   unsigned long long* trace_buf = nullptr;  // [kMaxB][4] globaltimer stamps of the last traced launch
   bool trace_on = false;
+  bool gate = false;           // launch k_gate ahead of every all-reduce (side-stream use)
   unsigned long long seq = 0;  // launches issued
   cudaEvent_t ev[kEvents];
   int nev = 0;
@@ -1577,25 +1606,65 @@ extern "C" int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo) {
   return resolve_fused_algo(algo, c->world, c->n * c->elem);
 }
 
-// Highest launch sequence number any peer has started, read from the entry flags the
-// peers' CTAs wrote into this rank's signal pad.  Uses a private non-blocking stream,
-// so it never waits behind the caller's (possibly stalled) streams.
+// Latest launch each peer has reached, from this rank's signal pad: the entry flags
+// of the first `rows` CTA slots and the gate slots (a gated launch announces itself
+// in its gate before its wide kernel writes entry flags).  Copied on a private
+// non-blocking stream, so it never waits behind the caller's (possibly stalled)
+// streams.  out[q] = epoch of peer q's latest launch (u32, wrapping compare).
+static int read_peer_epochs(lasgd_comm* c, int rows, uint32_t* out) {
+  static thread_local uint32_t* host = nullptr;
+  static thread_local cudaStream_t s = nullptr;
+  const size_t entry_words = (size_t)kMaxB * kMaxR;
+  if (!host) LASGD_CUDA_TRY(cudaHostAlloc((void**)&host, (entry_words + kMaxR) * sizeof(uint32_t), cudaHostAllocDefault));
+  if (!s) LASGD_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const size_t gate_word = (size_t)2 * kMaxB * kMaxR + (size_t)2 * kMaxR;  // k_gate's rank-level slots
+  LASGD_CUDA_TRY(cudaMemcpyAsync(host, c->base, (size_t)rows * kMaxR * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  LASGD_CUDA_TRY(cudaMemcpyAsync(host + entry_words, c->base + gate_word * sizeof(uint32_t), kMaxR * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost, s));
+  LASGD_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int q = 0; q < kMaxR; ++q) {
+    uint32_t best = host[entry_words + q];
+    for (int b = 0; b < rows; ++b) {
+      const uint32_t v = host[(size_t)b * kMaxR + q];
+      if ((int32_t)(v - best) > 0) best = v;
+    }
+    out[q] = best;
+  }
+  return LASGD_OK;
+}
+
+// Highest launch sequence number any peer has started (drain of adaptive runs).
 extern "C" int lasgd_comm_peer_max_seq(lasgd_comm* c, unsigned long long* out) {
   if (!c || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(c->device);
-  const size_t words = (size_t)kMaxB * kMaxR;  // phase-0 region
-  static thread_local uint32_t* host = nullptr;
-  static thread_local cudaStream_t s = nullptr;
-  if (!host) LASGD_CUDA_TRY(cudaHostAlloc((void**)&host, words * sizeof(uint32_t), cudaHostAllocDefault));
-  if (!s) LASGD_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  LASGD_CUDA_TRY(cudaMemcpyAsync(host, c->base, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  LASGD_CUDA_TRY(cudaStreamSynchronize(s));
+  uint32_t ep[kMaxR];
+  int rc = read_peer_epochs(c, kMaxB, ep);
+  if (rc) return rc;
   uint32_t best = 0;
-  for (int b = 0; b < kMaxB; ++b)
-    for (int q = 0; q < c->world; ++q)
-      if (q != c->rank && host[(size_t)b * kMaxR + q] > best) best = host[(size_t)b * kMaxR + q];
+  for (int q = 0; q < c->world; ++q)
+    if (q != c->rank && ep[q] > best) best = ep[q];
   *out = best;
   return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_set_gate(lasgd_comm* c, int on) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  c->gate = on != 0;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_peers_ahead(lasgd_comm* c, unsigned long long seq) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->world <= 1) return 0;
+  DeviceGuard g(c->device);
+  // CTA 0 of every K2/K3 launch writes its entry flag first, so the CTA-0 row (plus
+  // the gate row) holds each peer's latest launch: 64 bytes instead of the whole pad
+  uint32_t ep[kMaxR];
+  int rc = read_peer_epochs(c, 1, ep);
+  if (rc) return rc;
+  for (int q = 0; q < c->world; ++q)
+    if (q != c->rank && (int32_t)(ep[q] - (uint32_t)seq) > 0) return 1;
+  return 0;
 }
 
 extern "C" int lasgd_comm_invalidate_staging(lasgd_comm* c) {
@@ -1703,6 +1772,7 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
   if (rc) return rc;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   c->push_slot = -1;  // the caller rewrote a snapshot slot: staged push contributions are stale
+  if (c->gate && c->world > 1 && (rc = launch_gate(c->world, a, cs))) return rc;
   rc = launch_any(c->dtype, false, algo, c->world, a, dim3(c->nblocks, 1), c->threads, cs);
   if (rc) return rc;
   LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));

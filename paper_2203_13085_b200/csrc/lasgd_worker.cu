@@ -238,6 +238,9 @@ extern "C" int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* del
   int rc = issue(w, K_SNAPSHOT, w->compute,
                  [&] { return lasgd_snapshot(w->snap[0], w->x, w->n, w->dtype, (void*)w->compute); });
   if (!rc && comm) rc = lasgd_comm_invalidate_staging(comm);  // slot 0 rewritten: re-stage before a push round
+  // side-stream all-reduces (overlap pipeline) wait for late peers in a one-warp gate
+  // instead of a CTA per SM next to the compute stream's forward/backward
+  if (!rc && comm) rc = lasgd_comm_set_gate(comm, w->cfg.pipeline == 0);
   if (!rc && w->world > 1 && w->cfg.sync && w->cfg.pipeline == 0) rc = submit_allreduce(w, 0);
   if (rc) {
     lasgd_worker_destroy(w);
@@ -289,6 +292,14 @@ extern "C" int lasgd_worker_step(lasgd_worker* w, const void* g, double lr) {
     if (w->world > 1) {
       done = lasgd_comm_query(w->comm, w->seq);
       if (done < 0) return done;
+      // The host runs ahead of its GPU, so the completion flag alone is stale: a rank
+      // whose peers already entered a later launch is the round's laggard — its launch
+      // is done or about to be, and the peers wait for its next one.  Close now.
+      if (done == 0 && w->tau < w->cfg.tau_max) {
+        const int ahead = lasgd_comm_peers_ahead(w->comm, w->seq);
+        if (ahead < 0) return ahead;
+        done = ahead;
+      }
     }
     if (done == 1 || w->tau >= w->cfg.tau_max) {
       rc = close_round(w);

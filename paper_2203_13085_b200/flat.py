@@ -27,6 +27,7 @@ class FlatParams:
         self.g = torch.zeros(self.numel, dtype=dtype, device=device)
         self.params = params
         self.channels_last = channels_last
+        self._grad_views = {}
         self.offsets = []
         off = 0
         with torch.no_grad():
@@ -55,8 +56,13 @@ class FlatParams:
         backward writes the all-reduce input in place)."""
         if buf.dtype != self.x.dtype or buf.numel() != self.numel or not buf.is_contiguous():
             raise ValueError("gradient buffer must be a contiguous vector like x")
-        for p, off in zip(self.params, self.offsets):
-            p.grad = self._view(buf, off, p.shape, self.channels_last)
+        key = (buf.data_ptr(), buf.device)
+        views = self._grad_views.get(key)
+        if views is None:  # views are built once per buffer: rebinding every step stays cheap
+            views = [self._view(buf, off, p.shape, self.channels_last) for p, off in zip(self.params, self.offsets)]
+            self._grad_views[key] = views
+        for p, v in zip(self.params, views):
+            p.grad = v
         self.g = buf
 
     def zero_grad(self) -> None:

@@ -68,6 +68,18 @@ def _w_allreduce(rank, world, port):
                     torch.cuda.synchronize()
                     got = comm.xbar.cpu().numpy()
                     assert _same_bits(got, O.ring_mean(vecs)), (n, rnd, algo, rank)
+            # gated launches (side-stream use): same results; peers_ahead sees later launches
+            comm.set_gate(True)
+            for rnd in range(2):
+                vecs = [_vec(77 + 10 * r + rnd, n, npdt) for r in range(world)]
+                comm.snapshots[rnd].copy_(torch.from_numpy(vecs[rank]))
+                torch.cuda.synchronize()
+                seq = comm.allreduce(rnd)
+                assert comm.wait(seq, 30.0) == 1
+                assert _same_bits(comm.xbar.cpu().numpy(), O.ring_mean(vecs)), (n, "gated", rank)
+                dist.barrier()
+            assert comm.peers_ahead(seq - 1) and not comm.peers_ahead(seq)
+            comm.set_gate(False)
             dist.barrier()
             comm.close()
     dist.destroy_process_group()
