@@ -1,0 +1,101 @@
+"""``python -m paper_2203_13085_b200 run`` on the GPU: config-1 MLP runs (LASGD
+deterministic / adaptive, SGD-AR) write a valid RunTrace, summary and resolved
+config; multi-GPU runs under one process per GPU; compare and plotdata over them."""
+
+import json
+import os
+import socket
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _cfg(tmp, name, **over):
+    cfg = {"problem": {"n": 2048, "d": 64, "hidden": [32], "batch": 32}, "steps": 24,
+           "lr": {"base_lr": 0.05}, "lasgd": {"tau_max": 4}}
+    for k, v in over.items():
+        if isinstance(v, dict):
+            cfg.setdefault(k, {}).update(v)
+        else:
+            cfg[k] = v
+    p = os.path.join(tmp, name + ".json")
+    with open(p, "w") as f:
+        json.dump(cfg, f)
+    return p
+
+
+def _rows(out):
+    from paper_2203_13085_b200.trace import read_trace_csv
+
+    return read_trace_csv(os.path.join(out, "trace.csv"))
+
+
+def test_cli_run_single_gpu(tmp_path):
+    from paper_2203_13085_b200 import cli
+
+    outs = {}
+    for name, over in (("lasgd", {}), ("sgd_ar", {"algo": "sgd_ar"}),
+                       ("fused", {"lasgd": {"pipeline": "fused", "tau_max": 3}})):
+        out = str(tmp_path / name)
+        assert cli.main(["run", "--config", _cfg(str(tmp_path), name, **over), "--out", out]) == 0
+        s = json.load(open(os.path.join(out, "summary.json")))
+        rows = _rows(out)
+        outs[name] = out
+        k = 1 if name == "sgd_ar" else over.get("lasgd", {}).get("tau_max", 4)
+        assert s["rounds"] == len(rows) == 24 // k
+        assert all(r["node_tau"] == [k] for r in rows)
+        assert rows[-1]["grad_evals"] == 24 and rows[-1]["bytes_sent"] == 0  # P = 1: no exchange
+        assert s["final_loss"] < rows[0]["loss"]
+        cfgd = json.load(open(os.path.join(out, "config.resolved.json")))
+        assert cfgd["config_sha256"] == s["config_sha256"]
+        assert open(os.path.join(out, "trace.csv")).readline().strip() == f"# config_sha256={s['config_sha256']}"
+    assert cli.main(["compare", outs["sgd_ar"], outs["lasgd"]]) == 0
+    assert cli.main(["plotdata", outs["sgd_ar"], outs["lasgd"], "--out", str(tmp_path / "p.csv")]) == 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _w_cli(rank, world, port, tmp):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2203_13085_b200 import cli
+
+    for name, over in (("lasgd", {}), ("adaptive", {"lasgd": {"adaptive": True, "tau_max": 3}}),
+                       ("sgd_ar", {"algo": "sgd_ar"})):
+        path = _cfg(tmp, f"{name}_r{rank}", **over)
+        assert cli.main(["run", "--config", path, "--out", os.path.join(tmp, name)]) == 0
+    dist.destroy_process_group()
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_cli_run_multi_gpu(tmp_path):
+    import torch.multiprocessing as mp
+
+    from paper_2203_13085_b200.collective import bytes_per_node
+
+    world = min(NGPU, 4)
+    mp.spawn(_w_cli, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for name in ("lasgd", "adaptive", "sgd_ar"):
+        out = str(tmp_path / name)
+        s = json.load(open(os.path.join(out, "summary.json")))
+        rows = _rows(out)
+        assert s["nodes"] == world and len(rows[0]["node_tau"]) == world
+        assert s["bytes"]["per_node"] == s["rounds"] * bytes_per_node(s["n_params"], world, 4)
+        if name == "lasgd":
+            assert all(r["node_tau"] == [4] * world for r in rows)
+        if name == "adaptive":
+            assert all(t is None or 1 <= t <= 3 for r in rows for t in r["node_tau"])
+        assert s["final_loss"] == s["final_loss"]  # finite
