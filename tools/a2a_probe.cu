@@ -23,6 +23,20 @@ __global__ void k_a2a(Ptrs p, int npeers, size_t n16) {
   for (; i < n16; i += st) __stcg(d + i, __ldcg(s + i));
 }
 
+// fan-out push: every thread stores its pack to ALL peers (the push round's mean
+// broadcast pattern); stcg = 1: st.global.cg, 0: plain st.global
+template <int STCG>
+__global__ void k_fanout(Ptrs p, int npeers, size_t n16) {
+  const size_t st = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += st) {
+    const uint4 v = __ldcs(p.src[0] + i);
+    for (int k = 0; k < npeers; ++k) {
+      if (STCG) __stcg(p.dst[k] + i, v);
+      else p.dst[k][i] = v;
+    }
+  }
+}
+
 int main() {
   int P = 0;
   cudaGetDeviceCount(&P);
@@ -39,8 +53,8 @@ int main() {
     CK(cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking));
     CK(cudaEventCreate(&e0[d])); CK(cudaEventCreate(&e1[d]));
   }
-  for (int mode = 0; mode < 2; ++mode) {
-    for (int ctas : {148, 296}) {
+  for (int mode = 0; mode < 4; ++mode) {
+    for (int ctas : {148, 296, 592}) {
       float best = 1e9;
       for (int rep = 0; rep < 4; ++rep) {
         for (int d = 0; d < P; ++d) {
@@ -49,12 +63,15 @@ int main() {
           for (int q = 0; q < P; ++q) {
             if (q == d) continue;
             if (mode == 0) { p.src[k] = (const uint4*)(in[q] + S * d); p.dst[k] = (uint4*)(out[d] + S * q); }
-            else { p.src[k] = (const uint4*)(in[d] + S * q); p.dst[k] = (uint4*)(out[q] + S * d); }
+            else if (mode == 1) { p.src[k] = (const uint4*)(in[d] + S * q); p.dst[k] = (uint4*)(out[q] + S * d); }
+            else { p.src[k] = (const uint4*)in[d]; p.dst[k] = (uint4*)(out[q] + S * d); }
             ++k;
           }
           CK(cudaSetDevice(d));
           CK(cudaEventRecord(e0[d], st[d]));
-          k_a2a<<<ctas / (P - 1) * (P - 1), 512, 0, st[d]>>>(p, P - 1, S / 16);
+          if (mode < 2) k_a2a<<<ctas / (P - 1) * (P - 1), 512, 0, st[d]>>>(p, P - 1, S / 16);
+          else if (mode == 2) k_fanout<1><<<ctas, 256, 0, st[d]>>>(p, P - 1, S / 16);
+          else k_fanout<0><<<ctas, 256, 0, st[d]>>>(p, P - 1, S / 16);
           CK(cudaEventRecord(e1[d], st[d]));
         }
         float ms = 0;
@@ -66,7 +83,8 @@ int main() {
         }
         if (rep && ms < best) best = ms;
       }
-      printf("{\"P\": %d, \"mode\": \"%s\", \"ctas\": %d, \"GBps_per_gpu\": %.1f}\n", P, mode ? "push_stores" : "pull_loads",
+      const char* mn[] = {"pull_loads", "push_stores", "fanout_stcg", "fanout_st"};
+      printf("{\"P\": %d, \"mode\": \"%s\", \"ctas\": %d, \"GBps_per_gpu\": %.1f}\n", P, mn[mode],
              ctas, (double)S * (P - 1) / (best * 1e-3) / 1e9);
       fflush(stdout);
     }
