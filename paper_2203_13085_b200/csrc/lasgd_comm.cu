@@ -72,6 +72,7 @@ struct CommArgs {
   size_t stage_elems;
   int cur;                       // snapshot slot / staging parity read this round
   uint32_t prev_push;            // launch whose end signals certify the staged contributions
+  uint32_t prev_end;             // K7: the previous launch, if its end signals certify this one's inputs (else 0)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer();
@@ -615,7 +616,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
   const int b = blockIdx.x;
   bool ok = true;
   trace_mark(a, b, 0);
-  if (!VIRTUAL && P > 1) ok = cta_barrier<P>(a, 0, b, rank);
+  // Entry: every peer's snapshot slot must be final and every peer must be done reading
+  // this rank's other slot.  When the previous launch was a round that raised end
+  // signals (K7 one-shot or K8), those certify both and were raised before the peers
+  // even launched this kernel; otherwise the per-CTA entry barrier.
+  if (!VIRTUAL && P > 1) ok = a.prev_end ? rank_wait<P>(a, 1, a.prev_end, b, rank) : cta_barrier<P>(a, 0, b, rank);
   trace_mark(a, b, 1);
   unsigned bad = 0;
   if (ok) {
@@ -705,6 +710,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
       }
     }
   }
+  if (!VIRTUAL && P > 1 && ok) rank_signal<P>(a, 1, a.end_ctr, rank);  // certifies the next round's entry
   report_nonfinite(a.nonfinite, bad);
   trace_mark(a, b, 3);
   if (!VIRTUAL) publish_done(a);
@@ -1461,6 +1467,7 @@ struct lasgd_comm {
   size_t region_bytes = 0, off_snap[2] = {0, 0}, off_xbar = 0, off_stage = 0, stage_elems = 0;
   int push_slot = -1;            // staging parity that holds the current contributions (-1: none)
   unsigned long long last_push = 0;  // launch whose end signals certify them
+  unsigned long long end_seq = 0;    // last launch that raised end signals (K7 one-shot, K8)
   unsigned int* end_ctr = nullptr;   // [kDoneSlots] rank-level end-signal counters
   char* peer_base[kMaxR] = {nullptr};
   bool opened = false;
@@ -1820,6 +1827,7 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
       if (rc) return rc;
       LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
       c->last_push = s;
+      c->end_seq = s;
     }
     rc = prepare_launch(c, snap_slot, a, s);
     if (rc) return rc;
@@ -1831,6 +1839,7 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
                                : launch_push<double, false>(c->world, a, fd, dim3(nblocks, 1), c->threads, cs);
     if (rc) return rc;
     c->last_push = s;
+    c->end_seq = s;
     c->push_slot = 1 - snap_slot;
     LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
     if (seq) *seq = s;
@@ -1840,12 +1849,14 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
   if (rc) return rc;
   a.nblocks = nblocks;
   a.nonfinite = nonfinite;
+  if (algo == LASGD_ALGO_ONESHOT && c->end_seq != 0 && c->end_seq + 1 == s) a.prev_end = (uint32_t)c->end_seq;
   c->push_slot = -1;  // this round writes the next snapshot without staging it
   if (c->dtype == LASGD_F32)
     rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, algo);
   else
     rc = launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, algo);
   if (rc) return rc;
+  c->end_seq = algo == LASGD_ALGO_ONESHOT ? s : 0;  // the one-shot K7 raises end signals
   LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
   if (seq) *seq = s;
   return LASGD_OK;
