@@ -51,7 +51,8 @@ extern "C" {
 #define LASGD_ALGO_AUTO 0
 #define LASGD_ALGO_ONESHOT 1
 #define LASGD_ALGO_TWOSHOT 2
-#define LASGD_ALGO_PUSH 3 /* fused round only: owners reduce locally staged chunks, results pushed */
+#define LASGD_ALGO_PUSH 3 /* fused round only, data moved by remote stores: P = 2 mirrors the peer's
+                             snapshot; P >= 3 owners reduce locally staged chunks, means pushed */
 
 #define LASGD_MAX_RANKS 8
 #define LASGD_MAX_BLOCKS 512
@@ -197,8 +198,9 @@ int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len);
 /* NVLink bytes this rank's peers read from it in one launch (collective.py:206-226 analogue). */
 unsigned long long lasgd_comm_bytes_per_node(lasgd_comm* c, int algo);
 int lasgd_comm_resolve_algo(lasgd_comm* c, int algo);
-/* The algorithm lasgd_comm_fused_round runs for `algo`: AUTO resolves to one-shot where
- * the all-reduce would be one-shot and to PUSH where it would be two-shot. */
+/* The algorithm lasgd_comm_fused_round runs for `algo`: AUTO resolves to PUSH (the
+ * mirror form) at P = 2 for buffers >= 1 MiB, otherwise to one-shot where the all-reduce
+ * would be one-shot and to PUSH where it would be two-shot. */
 int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo);
 /* Change the SM budget (CTAs per launch) for subsequent launches; every rank must
  * make the same call between the same two launches. */

@@ -1194,6 +1194,126 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
   if (!VIRTUAL) publish_done(a);
 }
 
+// ------------------------------------------------------------------ mirror push round (K8, P = 2)
+// At P = 2 the push round keeps a full mirror of the peer's snapshot in local HBM: the
+// staging area (2 parities x 2 sources x n/2) is re-used as [parity][n].  Each round
+// reads the own snapshot and the mirror (both local), forms the ring-order mean per
+// element exactly like the one-shot K7, applies local step + pull, writes the next
+// snapshot locally AND stores it into the peer's mirror (other parity) as posted NVLink
+// writes; the rank-level end signals certify the mirror for the next round's entry.
+// One phase, no mid barrier; NVLink out B per round (= the one-shot's B in), as stores.
+template <typename T>
+__device__ __forceinline__ T* mirror_ptr(const CommArgs& a, int owner, int parity) {
+  return reinterpret_cast<T*>(a.stage[owner]) + (size_t)parity * 2 * a.stage_elems;
+}
+
+template <typename T, bool VIRTUAL, int U>
+__global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T> f) {
+  constexpr int P = 2;
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
+  const int peer = 1 - rank;
+  const int b = blockIdx.x;
+  const size_t n = a.n;
+  const int cur = a.cur, nxt = 1 - a.cur;
+  bool ok = true;
+  unsigned bad = 0;
+  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  trace_mark(a, b, 0);
+  if (a.phases & 4) {  // initial mirror: the current snapshot -> the peer's mirror, parity cur
+    T* dst = mirror_ptr<T>(a, peer, cur);
+    for_tiles<U>(a, b, n / W, [&](size_t p0, size_t p1) {
+      for (size_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) st_plain(dst + p * W, ld_stream(snap_own + p * W));
+    });
+    if (b == a.nblocks - 1)
+      for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) dst[j] = snap_own[j];
+    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+  }
+  if (a.phases & 1) {
+    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
+    trace_mark(a, b, 1);
+    if (ok) {
+      size_t bnd[P + 1];
+#pragma unroll
+      for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
+      const T* const mir = mirror_ptr<T>(a, rank, cur);  // the peer's snapshot, local copy
+      T* const out = mirror_ptr<T>(a, peer, nxt);          // the peer's copy of our next snapshot
+      T* const x = f.x[vr];
+      const T* const g = f.g[vr];
+      T* const m = f.m[vr];
+      T* const dl = f.delta[vr];
+      T* const sn = f.snap_next[vr];
+      const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
+      const bool store_d = f.c.use_delta && f.mode == 0;
+      auto element = [&](T& xv, T gv, T& mv, T& dv, T own, T oth, int cidx) {
+        unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+        T lane[P];  // lanes by rank, selected without dynamic register indexing
+        lane[0] = rank == 0 ? own : oth;
+        lane[1] = rank == 0 ? oth : own;
+        const T zb = mean_div<T, P>(rot_sum<T, P>(lane, cidx));
+        if (f.mode == 0) {
+          bb += pull_elem(f.neg_alpha, xv, own, zb);
+        } else {
+          xv = add_rn(zb, dv);
+          bb += !finite(xv);
+        }
+        bad += bb;
+      };
+      for_tiles<U>(a, b, n / W, [&](size_t p0, size_t p1) {
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vo[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+              vx[u] = ld_stream(x + j);
+              vg[u] = ld_stream(g + j);
+              if (load_m) vm[u] = ld_stream(m + j);
+              if (load_d) vd[u] = ld_stream(dl + j);
+              vs[u] = ld_stream(snap_own + j);
+              vo[u] = ld_stream(mir + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j0 = pu * W;
+              const int c0 = chunk_of<P>(j0, bnd), c1 = chunk_of<P>(j0 + W - 1, bnd);
+#pragma unroll
+              for (int k = 0; k < W; ++k)
+                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vo[u].v[k],
+                        c0 == c1 ? c0 : chunk_of<P>(j0 + k, bnd));
+              st_plain(out + j0, vx[u]);  // posted NVLink write into the peer's mirror
+              st_stream(x + j0, vx[u]);
+              if (f.c.use_mom) st_stream(m + j0, vm[u]);
+              if (store_d) st_stream(dl + j0, vd[u]);
+              st_stream(sn + j0, vx[u]);
+            }
+          }
+        }
+      });
+      if (b == a.nblocks - 1) {  // scalar tail n % W
+        for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, snap_own[j], mir[j], chunk_of<P>(j, bnd));
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+          out[j] = xv;
+        }
+      }
+      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
+  if (!VIRTUAL) publish_done(a);
+}
+
 // ------------------------------------------------------------------ dispatch
 template <int P>
 constexpr int unroll_for() { return P <= 2 ? 8 : (P <= 4 ? 4 : 2); }
@@ -1245,8 +1365,17 @@ int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int
     }                                                                                               \
     return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                  \
   }
+  if (P == 2) {  // mirror form
+    auto kern = k_push_mirror<T, VIRTUAL, 2>;
+    CommArgs aa = a;
+    if (!VIRTUAL) {
+      const int cap = coop_capacity(kern, threads);
+      if ((int)grid.x > cap) grid.x = cap;
+      aa.nblocks = grid.x;
+    }
+    return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);
+  }
   switch (P) {
-    LASGD_PCASE(2)
     LASGD_PCASE(3)
     LASGD_PCASE(4)
     LASGD_PCASE(5)
@@ -1305,10 +1434,13 @@ int resolve_algo(int algo, int P, size_t bytes) {
 
 // Fused round (K7/K8): where the all-reduce would be two-shot, the push round moves
 // the same NVLink bytes with stores only and no entry wait on peers' snapshots
-// (measured ~3% faster per round at P=4, profiles/bench_r01_push_*.json).
+// (measured 3-5% faster per round at P=3/4, profiles/bench_r01_algo_*.json).
+// At P = 2 the push round is the mirror form: same bytes as the one-shot, moved as
+// posted stores, ~6% faster per round at ResNet-50 size (profiles/k8_mirror_ab_r01_p2.jsonl).
 int resolve_fused_algo(int algo, int P, size_t bytes) {
   if (P <= 1) return LASGD_ALGO_ONESHOT;
   if (algo != LASGD_ALGO_AUTO) return algo;
+  if (P == 2) return bytes >= ((size_t)1 << 20) ? LASGD_ALGO_PUSH : LASGD_ALGO_ONESHOT;
   const int a = resolve_algo(algo, P, bytes);
   return a == LASGD_ALGO_TWOSHOT ? LASGD_ALGO_PUSH : a;
 }
