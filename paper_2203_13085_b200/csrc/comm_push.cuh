@@ -1,0 +1,343 @@
+// Push round kernels (K8): data moved by remote stores; staged-chunk form for P >= 3, mirror form for P = 2.
+// Part of the communicator translation unit (lasgd_comm.cu includes it); see the
+// overview there.
+#ifndef LASGD_COMM_PUSH_CUH
+#define LASGD_COMM_PUSH_CUH
+
+#include "comm_fused.cuh"
+
+namespace lasgd {
+
+// ------------------------------------------------------------------ push round (K8)
+// The fused round with the data movement done by remote STORES from the producer.
+// Chunk c is owned by rank c.  Every rank keeps, in its IPC region, a staging area
+// stage[parity][source][chunk] for the contributions to its own chunk.
+//   init (phase bit 4): push chunk c of the current snapshot to owner c's staging.
+//   phase A (bit 1): wait for every rank's end signal of the previous push launch
+//     (staged contributions complete; peers finished their previous round); the owner
+//     forms the ring-order mean of its chunk from local staging + its own snapshot,
+//     applies the local step + pull to its own chunk, and pushes the mean to every
+//     peer's xbar.
+//   rank-level mid barrier (all means pushed).
+//   phase B (bit 2): every other chunk: local step + pull with the mean in the local
+//     xbar, next snapshot written locally and pushed to the owner's staging (other
+//     parity); then the rank-level end signal.
+// Per rank and round: NVLink out 2(P-1)/P*B as posted writes, all reads local.  Same
+// element functions and summation order as K7, so results are bit-identical.
+template <typename T>
+__device__ __forceinline__ T* stage_ptr(const CommArgs& a, int owner, int parity, int src, int P) {
+  return reinterpret_cast<T*>(a.stage[owner]) + ((size_t)parity * P + src) * a.stage_elems;
+}
+
+template <typename T, int P, bool VIRTUAL, int U>
+__global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T> f) {
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
+  const int b = blockIdx.x;
+  const size_t n = a.n;
+  const int cur = a.cur, nxt = 1 - a.cur;
+  bool ok = true;
+  unsigned bad = 0;
+  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
+  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
+  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  trace_mark(a, b, 0);
+  // offset of element j of chunk c inside a staging slot (keeps 16-byte alignment)
+  auto soff = [&](int c, size_t j) { return j - chunk_bound(n, P, c) / W * W; };
+  if (a.phases & 4) {
+    // initial contributions: chunk c of the current snapshot -> owner c, parity cur
+    chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
+      [&](int c, size_t p0, size_t p1) {
+        T* dst = stage_ptr<T>(a, c, cur, rank, P);
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) v[u] = ld_stream(snap_own + pu * W);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) st_plain(dst + soff(c, pu * W), v[u]);
+          }
+        }
+      },
+      [&](int c, size_t j) { stage_ptr<T>(a, c, cur, rank, P)[soff(c, j)] = snap_own[j]; });
+    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+  }
+  T* const x = f.x[vr];
+  const T* const g = f.g[vr];
+  T* const m = f.m[vr];
+  T* const dl = f.delta[vr];
+  T* const sn = f.snap_next[vr];
+  const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
+  const bool store_d = f.c.use_delta && f.mode == 0;
+  auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
+    unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+    if (f.mode == 0) {
+      bb += pull_elem(f.neg_alpha, xv, sv, zb);
+    } else {
+      xv = add_rn(zb, dv);
+      bb += !finite(xv);
+    }
+    bad += bb;
+  };
+  if (a.phases & 1) {
+    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
+    trace_mark(a, b, 1);
+    if (ok) {
+      const T* src[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) src[q] = q == rank ? snap_own : stage_ptr<T>(a, rank, cur, q, P);
+      size_t cs, ce, cp0, cp1;
+      chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
+      const size_t base = cs / W * W;  // staging offset origin of the own chunk
+      tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> v[U][P], vx[U], vg[U], vm[U], vd[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+#pragma unroll
+              for (int q = 0; q < P; ++q) v[u][q] = ld_stream(src[q] + (q == rank ? j : j - base));
+              vx[u] = ld_stream(x + j);
+              vg[u] = ld_stream(g + j);
+              if (load_m) vm[u] = ld_stream(m + j);
+              if (load_d) vd[u] = ld_stream(dl + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+              Pack<T> z;
+#pragma unroll
+              for (int k = 0; k < W; ++k) {
+                T lane[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+                T sv = lane[0];
+#pragma unroll
+                for (int q = 1; q < P; ++q) sv = (q == rank) ? lane[q] : sv;
+                z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], sv, z.v[k]);
+              }
+#pragma unroll
+              for (int q = 0; q < P; ++q)
+                if (q != rank) st_plain(reinterpret_cast<T*>(a.xbar[q]) + j, z);  // the mean to every peer
+              st_stream(x + j, vx[u]);
+              if (f.c.use_mom) st_stream(m + j, vm[u]);
+              if (store_d) st_stream(dl + j, vd[u]);
+              st_stream(sn + j, vx[u]);
+            }
+          }
+        }
+      });
+      if (b == 0) {  // unaligned head / tail elements of the own chunk
+        const size_t he = cp0 * W < ce ? cp0 * W : ce;
+        const size_t ts = cp1 * W > he ? cp1 * W : he;
+        auto scalar = [&](size_t j) {
+          T lane[P];
+#pragma unroll
+          for (int q = 0; q < P; ++q) lane[q] = src[q][q == rank ? j : j - base];
+          const T zb = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+            if (q != rank) reinterpret_cast<T*>(a.xbar[q])[j] = zb;
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, snap_own[j], zb);
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+        };
+        for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
+        for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
+      }
+    }
+  }
+  if (a.phases & 2) {
+    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
+    trace_mark(a, b, 2);
+    if (ok) {
+      const T* zl = reinterpret_cast<const T*>(a.xbar[rank]);  // means pushed by their owners
+      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
+        [&](int c, size_t p0, size_t p1) {
+          T* dst = stage_ptr<T>(a, c, nxt, rank, P);
+          for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+            Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) {
+                const size_t j = pu * W;
+                vz[u] = ld_stream(zl + j);
+                vx[u] = ld_stream(x + j);
+                vg[u] = ld_stream(g + j);
+                if (load_m) vm[u] = ld_stream(m + j);
+                if (load_d) vd[u] = ld_stream(dl + j);
+                if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const size_t pu = p + (size_t)u * blockDim.x;
+              if (pu < p1) {
+                const size_t j = pu * W;
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                  element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
+                st_plain(dst + soff(c, j), vx[u]);  // next-round contribution to owner c
+                st_stream(x + j, vx[u]);
+                if (f.c.use_mom) st_stream(m + j, vm[u]);
+                if (store_d) st_stream(dl + j, vd[u]);
+                st_stream(sn + j, vx[u]);
+              }
+            }
+          }
+        },
+        [&](int c, size_t j) {
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), zl[j]);
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+          stage_ptr<T>(a, c, nxt, rank, P)[soff(c, j)] = xv;
+        });
+      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
+  if (!VIRTUAL) publish_done(a);
+}
+
+// ------------------------------------------------------------------ mirror push round (K8, P = 2)
+// At P = 2 the push round keeps a full mirror of the peer's snapshot in local HBM: the
+// staging area (2 parities x 2 sources x n/2) is re-used as [parity][n].  Each round
+// reads the own snapshot and the mirror (both local), forms the ring-order mean per
+// element exactly like the one-shot K7, applies local step + pull, writes the next
+// snapshot locally AND stores it into the peer's mirror (other parity) as posted NVLink
+// writes; the rank-level end signals certify the mirror for the next round's entry.
+// One phase, no mid barrier; NVLink out B per round (= the one-shot's B in), as stores.
+template <typename T>
+__device__ __forceinline__ T* mirror_ptr(const CommArgs& a, int owner, int parity) {
+  return reinterpret_cast<T*>(a.stage[owner]) + (size_t)parity * 2 * a.stage_elems;
+}
+
+template <typename T, bool VIRTUAL, int U>
+__global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T> f) {
+  constexpr int P = 2;
+  constexpr int W = Pack<T>::W;
+  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
+  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
+  const int peer = 1 - rank;
+  const int b = blockIdx.x;
+  const size_t n = a.n;
+  const int cur = a.cur, nxt = 1 - a.cur;
+  bool ok = true;
+  unsigned bad = 0;
+  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  trace_mark(a, b, 0);
+  if (a.phases & 4) {  // initial mirror: the current snapshot -> the peer's mirror, parity cur
+    T* dst = mirror_ptr<T>(a, peer, cur);
+    for_tiles<U>(a, b, n / W, [&](size_t p0, size_t p1) {
+      for (size_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) st_plain(dst + p * W, ld_stream(snap_own + p * W));
+    });
+    if (b == a.nblocks - 1)
+      for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) dst[j] = snap_own[j];
+    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+  }
+  if (a.phases & 1) {
+    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
+    trace_mark(a, b, 1);
+    if (ok) {
+      size_t bnd[P + 1];
+#pragma unroll
+      for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
+      const T* const mir = mirror_ptr<T>(a, rank, cur);  // the peer's snapshot, local copy
+      T* const out = mirror_ptr<T>(a, peer, nxt);          // the peer's copy of our next snapshot
+      T* const x = f.x[vr];
+      const T* const g = f.g[vr];
+      T* const m = f.m[vr];
+      T* const dl = f.delta[vr];
+      T* const sn = f.snap_next[vr];
+      const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
+      const bool store_d = f.c.use_delta && f.mode == 0;
+      auto element = [&](T& xv, T gv, T& mv, T& dv, T own, T oth, int cidx) {
+        unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+        T lane[P];  // lanes by rank, selected without dynamic register indexing
+        lane[0] = rank == 0 ? own : oth;
+        lane[1] = rank == 0 ? oth : own;
+        const T zb = mean_div<T, P>(rot_sum<T, P>(lane, cidx));
+        if (f.mode == 0) {
+          bb += pull_elem(f.neg_alpha, xv, own, zb);
+        } else {
+          xv = add_rn(zb, dv);
+          bb += !finite(xv);
+        }
+        bad += bb;
+      };
+      for_tiles<U>(a, b, n / W, [&](size_t p0, size_t p1) {
+        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+          Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vo[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j = pu * W;
+              vx[u] = ld_stream(x + j);
+              vg[u] = ld_stream(g + j);
+              if (load_m) vm[u] = ld_stream(m + j);
+              if (load_d) vd[u] = ld_stream(dl + j);
+              vs[u] = ld_stream(snap_own + j);
+              vo[u] = ld_stream(mir + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const size_t pu = p + (size_t)u * blockDim.x;
+            if (pu < p1) {
+              const size_t j0 = pu * W;
+              const int c0 = chunk_of<P>(j0, bnd), c1 = chunk_of<P>(j0 + W - 1, bnd);
+#pragma unroll
+              for (int k = 0; k < W; ++k)
+                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vo[u].v[k],
+                        c0 == c1 ? c0 : chunk_of<P>(j0 + k, bnd));
+              st_plain(out + j0, vx[u]);  // posted NVLink write into the peer's mirror
+              st_stream(x + j0, vx[u]);
+              if (f.c.use_mom) st_stream(m + j0, vm[u]);
+              if (store_d) st_stream(dl + j0, vd[u]);
+              st_stream(sn + j0, vx[u]);
+            }
+          }
+        }
+      });
+      if (b == a.nblocks - 1) {  // scalar tail n % W
+        for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
+          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
+          element(xv, g[j], mv, dv, snap_own[j], mir[j], chunk_of<P>(j, bnd));
+          x[j] = xv;
+          if (f.c.use_mom) m[j] = mv;
+          if (store_d) dl[j] = dv;
+          sn[j] = xv;
+          out[j] = xv;
+        }
+      }
+      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+    }
+  }
+  report_nonfinite(a.nonfinite, bad);
+  trace_mark(a, b, 3);
+  if (!VIRTUAL) publish_done(a);
+}
+
+}  // namespace lasgd
+
+#endif  // LASGD_COMM_PUSH_CUH

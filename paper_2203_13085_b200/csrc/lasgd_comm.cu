@@ -1,6 +1,12 @@
-// Mean all-reduce of the LASGD snapshot over NVLink P2P (K2 one-shot, K3 two-shot)
-// with epoch-tagged per-CTA flags in IPC-mapped signal pads (K6) and a
-// host-mapped completion word for flag polling.
+// NVLink P2P communicator of the LASGD sync path: the C-ABI entry points, launch
+// dispatch, virtual-rank test paths and the communicator lifecycle (IPC region,
+// signal pad, work queues, host-mapped status).  The kernels live in headers of this
+// one translation unit:
+//   comm_device.cuh    CommArgs, system-scope flags, per-CTA / rank-level barriers,
+//                      launch gate (K9), completion word, tile work queues
+//   comm_allreduce.cuh K2 one-shot and K3 two-shot mean all-reduce
+//   comm_fused.cuh     K7 fused round (local step + mean + pull + next snapshot)
+//   comm_push.cuh      K8 push round (staged chunks for P >= 3, mirror for P = 2)
 //
 // Replaces collective.py:154-203 (`execute_allreduce`) and the
 // LoopbackTransport round (collective.py:229-287).  The arithmetic reproduces the
@@ -32,856 +38,14 @@
 #include <mutex>
 #include <utility>
 
+#include "comm_allreduce.cuh"
+#include "comm_device.cuh"
+#include "comm_fused.cuh"
+#include "comm_push.cuh"
 #include "lasgd_common.cuh"
 
 namespace lasgd {
 
-constexpr int kMaxR = LASGD_MAX_RANKS;
-constexpr int kMaxB = LASGD_MAX_BLOCKS;  // flag slots per phase and rank
-constexpr int kPhases = 3;  // 0 entry (per CTA), 1 mid (per CTA), 2 rank-level mid
-constexpr size_t kPadBytes = (size_t)kPhases * kMaxB * kMaxR * sizeof(uint32_t);
-constexpr int kDoneSlots = 64;
-constexpr int kEvents = 64;
-
-// host-mapped status block layout (uint32 words)
-enum { ST_ERR = 0, ST_PEER, ST_PHASE, ST_BLOCK, ST_SEQ_LO, ST_SEQ_HI, ST_RANK, ST_WORDS = 16 };
-enum { ERR_NONE = 0, ERR_TIMEOUT = 1, ERR_INJECTED = 2 };
-
-struct CommArgs {
-  const char* snap[kMaxR];
-  char* xbar[kMaxR];
-  uint32_t* pad[kMaxR];
-  size_t n;
-  int rank;
-  int nblocks;
-  uint32_t epoch;
-  int phases;  // bit 0: reduce (one-shot / RS), bit 1: all-gather (two-shot)
-  long long timeout_ns;
-  int skip_signal_phase;
-  uint32_t* status;
-  unsigned int* done_ctr;
-  unsigned long long* done_seq;
-  unsigned long long seq;
-  unsigned long long* nonfinite;
-  unsigned long long* trace;  // optional per-CTA timeline: [b][0..3] = start, entry passed, mid passed, end
-  unsigned long long* tile_ctr;  // two work queues of this launch (nullptr: static slices)
-  unsigned int* mid_ctr;         // CTAs of this rank past the reduce-scatter (rank-level barrier)
-  unsigned int* end_ctr;         // CTAs of this rank done pushing (push round, rank-level end signal)
-  // push round (K8): per-rank staging regions and round bookkeeping
-  char* stage[kMaxR];            // owner o's staging: [parity][source rank][stage_elems]
-  size_t stage_elems;
-  int cur;                       // snapshot slot / staging parity read this round
-  uint32_t prev_push;            // launch whose end signals certify the staged contributions
-  uint32_t prev_end;             // K7: the previous launch, if its end signals certify this one's inputs (else 0)
-};
-
-__device__ __forceinline__ unsigned long long globaltimer();
-
-__device__ __forceinline__ void trace_mark(const CommArgs& a, int b, int k) {
-  if (a.trace != nullptr && threadIdx.x == 0) a.trace[b * 4 + k] = globaltimer();
-}
-
-// ------------------------------------------------------------------ primitives
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Bounds of partition_chunks(n, P): bound(c) = c*base + min(c, rem).
-__device__ __forceinline__ size_t chunk_bound(size_t n, int P, int c) {
-  const size_t base = n / (size_t)P, rem = n % (size_t)P;
-  return (size_t)c * base + ((size_t)c < rem ? (size_t)c : rem);
-}
-
-template <int P>
-__device__ __forceinline__ int chunk_of(size_t j, const size_t (&bnd)[P + 1]) {
-  int c = 0;
-#pragma unroll
-  for (int k = 1; k < P; ++k) c += (j >= bnd[k]);
-  return c;
-}
-
-// Sum v[c], v[c+1], ..., v[c-1] (mod P) left to right: the reference ring order.
-template <typename T, int P>
-__device__ __forceinline__ T rot_sum(const T (&v)[P], int c) {
-  T acc = v[0];
-#pragma unroll
-  for (int cc = 0; cc < P; ++cc) {
-    if (c == cc) {
-      T s = v[cc];
-#pragma unroll
-      for (int k = 1; k < P; ++k) s = add_rn(s, v[(cc + k) % P]);
-      acc = s;
-    }
-  }
-  return acc;
-}
-
-// buf / P (collective.py:200).  For power-of-two P, x*(1/P) is the same correctly
-// rounded value as x/P (exact scaling), so use the cheaper multiply.
-template <typename T, int P>
-__device__ __forceinline__ T mean_div(T s) {
-  if constexpr ((P & (P - 1)) == 0) {
-    return mul_rn(s, T(1.0 / P));
-  } else {
-    return div_rn(s, T(P));
-  }
-}
-
-__device__ void report_failure(const CommArgs& a, int code, int peer, int phase, int block, int rank) {
-  if (atomicCAS(&a.status[ST_ERR], 0u, (uint32_t)code) == 0u) {
-    a.status[ST_PEER] = peer;
-    a.status[ST_PHASE] = phase;
-    a.status[ST_BLOCK] = block;
-    a.status[ST_SEQ_LO] = (uint32_t)(a.seq & 0xffffffffu);
-    a.status[ST_SEQ_HI] = (uint32_t)(a.seq >> 32);
-    a.status[ST_RANK] = rank;
-    __threadfence_system();
-  }
-}
-
-// Per-CTA barrier with the same CTA index on every peer.  Thread q < P signals
-// peer q and waits for peer q's signal.
-template <int P>
-__device__ bool cta_barrier(const CommArgs& a, int phase, int b, int rank) {
-  __syncthreads();
-  int ok = 1;
-  if (threadIdx.x < P) {
-    const int q = threadIdx.x;
-    const size_t slot = ((size_t)phase * kMaxB + b) * kMaxR;
-    if (a.skip_signal_phase != phase) {
-      __threadfence_system();
-      st_release_sys(a.pad[q] + slot + rank, a.epoch);
-    }
-    const uint32_t* f = a.pad[rank] + slot + q;
-    const unsigned long long t0 = globaltimer();
-    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
-      if ((long long)(globaltimer() - t0) > a.timeout_ns) {
-        report_failure(a, ERR_TIMEOUT, q, phase, b, rank);
-        ok = 0;
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  return __syncthreads_and(ok) != 0;
-}
-
-// Last CTA of a launch publishes the sequence number to host-mapped memory.
-__device__ void publish_done(const CommArgs& a) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    const unsigned slot = (unsigned)(a.seq % kDoneSlots);
-    const unsigned prev = atomicAdd(&a.done_ctr[slot], 1u);
-    if (prev == (unsigned)a.nblocks - 1u) {
-      a.done_ctr[slot] = 0u;
-      if (a.tile_ctr) a.tile_ctr[0] = a.tile_ctr[1] = 0ull;  // every CTA has left its tile loops
-      __threadfence_system();
-      st_release_sys64(a.done_seq, a.seq);
-    }
-  }
-}
-
-// Even split of `npack` packs over `nb` CTAs.
-__device__ __forceinline__ void split(size_t npack, int nb, int b, size_t& p0, size_t& p1) {
-  const size_t per = (npack + nb - 1) / nb;
-  p0 = (size_t)b * per;
-  if (p0 > npack) p0 = npack;
-  p1 = p0 + per;
-  if (p1 > npack) p1 = npack;
-}
-
-// Work distribution of the one-shot kernels over packs [0, npack): with a launch work
-// queue (P2P launches) CTAs take tiles of TILE_ITERS*U*blockDim packs from an atomic
-// counter, the next index fetched while the current tile streams, so fast CTAs absorb
-// the tail; otherwise (virtual ranks) CTA b takes the b-th even slice.  Every CTA has
-// passed its entry barrier before it takes a tile, so the double-buffer argument is
-// unchanged (it only needs every CTA to wait for its peers' same-index CTA).
-constexpr int kTileIters = 2;
-
-// Tiles of `tile` packs over [base, base + npack): from the atomic queue `ctr` when
-// given (next index prefetched while the current tile streams), else a contiguous
-// even slice per CTA.
-// `rot` rotates the order in which the packs are visited (logical pack l maps to
-// (l + rot) mod npack): the two-shot all-gather starts every rank at a different
-// owner's chunk so no owner serves all readers at once.
-template <typename F>
-__device__ __forceinline__ void tile_loop(unsigned long long* ctr, int b, int nblocks, size_t base, size_t npack,
-                                          size_t tile, F&& range, size_t rot = 0) {
-  if (npack == 0) return;
-  auto visit = [&](size_t l0, size_t l1) {
-    if (l0 >= l1) return;
-    size_t a0 = l0 + rot;
-    if (a0 >= npack) a0 -= npack;
-    const size_t len = l1 - l0;
-    if (a0 + len <= npack) {
-      range(base + a0, base + a0 + len);
-    } else {
-      range(base + a0, base + npack);
-      range(base, base + a0 + len - npack);
-    }
-  };
-  if (ctr == nullptr) {
-    size_t p0, p1;
-    split(npack, nblocks, b, p0, p1);
-    visit(p0, p1);
-    return;
-  }
-  __shared__ unsigned long long s_next;
-  const unsigned long long ntiles = (npack + tile - 1) / tile;
-  __syncthreads();
-  if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);
-  __syncthreads();
-  unsigned long long t = s_next;
-  while (t < ntiles) {
-    __syncthreads();  // everyone has read s_next
-    if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);  // prefetch the next index
-    const size_t p0 = (size_t)t * tile;
-    visit(p0, p0 + tile < npack ? p0 + tile : npack);
-    __syncthreads();
-    t = s_next;
-  }
-}
-
-template <int U, typename F>
-__device__ __forceinline__ void for_tiles(const CommArgs& a, int b, size_t npack, F&& range) {
-  tile_loop(a.tile_ctr, b, a.nblocks, 0, npack, (size_t)kTileIters * U * blockDim.x, range);
-}
-
-// Rank-level signal of kind k (0 = mid: reduce-scatter / mean pushes done, 1 = end:
-// next-snapshot chunks pushed to their owners): every CTA counts itself in (after a
-// __threadfence_system, so its stores — remote ones included — are visible system
-// wide); the last CTA of the rank writes `epoch` into slot [k][rank] of every peer.
-template <int P>
-__device__ void rank_signal(const CommArgs& a, int kind, unsigned* ctr, int rank) {
-  __shared__ int s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    const unsigned prev = atomicAdd(ctr, 1u);
-    s_last = prev == (unsigned)a.nblocks - 1u;
-    if (s_last) *ctr = 0u;  // every CTA of this launch has counted itself in
-  }
-  __syncthreads();
-  const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)kind * kMaxR;
-  if (s_last && threadIdx.x < P && !(kind == 0 && a.skip_signal_phase == 1)) {
-    __threadfence_system();
-    st_release_sys(a.pad[threadIdx.x] + slot + rank, a.epoch);
-  }
-}
-
-// Wait until every rank has signalled kind k with an epoch >= `epoch`.
-template <int P>
-__device__ bool rank_wait(const CommArgs& a, int kind, uint32_t epoch, int b, int rank) {
-  const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)kind * kMaxR;
-  int ok = 1;
-  if (threadIdx.x < P) {
-    const int q = threadIdx.x;
-    const uint32_t* f = a.pad[rank] + slot + q;
-    const unsigned long long t0 = globaltimer();
-    while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
-      if ((long long)(globaltimer() - t0) > a.timeout_ns) {
-        report_failure(a, ERR_TIMEOUT, q, 1, b, rank);
-        ok = 0;
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  return __syncthreads_and(ok) != 0;
-}
-
-// Rank-level barrier between the two phases of the two-shot kernels.  Requires all
-// CTAs co-resident: the P2P two-shot kernels are launched cooperatively.
-template <int P>
-__device__ bool rank_barrier(const CommArgs& a, int b, int rank) {
-  rank_signal<P>(a, 0, a.mid_ctr, rank);
-  return rank_wait<P>(a, 0, a.epoch, b, rank);
-}
-
-// Launch gate (one warp, launched in stream order just before a side-stream
-// all-reduce): announce launch `epoch` to every peer (rank-level slot kind 2), then
-// wait until every peer announced it too.  A wide all-reduce kernel whose peers are
-// late spins in its entry barrier holding a CTA on most SMs, which starves the
-// compute stream's large forward/backward CTAs; behind the gate it only starts once
-// every peer is about to start as well, and the waiting costs one warp.
-template <int P>
-__global__ void __launch_bounds__(32) k_gate(CommArgs a) {
-  const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)2 * kMaxR;
-  if (threadIdx.x < P) st_release_sys(a.pad[threadIdx.x] + slot + a.rank, a.epoch);
-  rank_wait<P>(a, 2, a.epoch, 0, a.rank);
-}
-
-// Aligned body of chunk c in packs, [cp0, cp1), plus its unaligned head/tail elements.
-template <typename T, int P>
-__device__ __forceinline__ void chunk_packs(size_t n, int c, size_t& cs, size_t& ce, size_t& cp0, size_t& cp1) {
-  constexpr int W = Pack<T>::W;
-  cs = chunk_bound(n, P, c);
-  ce = chunk_bound(n, P, c + 1);
-  cp0 = (cs + W - 1) / W;
-  cp1 = ce / W;
-  if (cp1 < cp0) cp1 = cp0;
-}
-
-// ------------------------------------------------------------------ one-shot (K2)
-template <typename T, int P, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(256, 2) k_oneshot(CommArgs a) {
-  constexpr int W = Pack<T>::W;
-  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
-  const int b = blockIdx.x;
-  bool ok = true;
-  trace_mark(a, b, 0);
-  if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
-  trace_mark(a, b, 1);
-  unsigned bad = 0;
-  if (ok) {
-    const size_t n = a.n;
-    size_t bnd[P + 1];
-#pragma unroll
-    for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
-    const T* src[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
-    T* out = reinterpret_cast<T*>(a.xbar[rank]);
-    auto range = [&](size_t p0, size_t p1) {
-    for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-      Pack<T> v[U][P];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t pu = p + (size_t)u * blockDim.x;
-        if (pu < p1) {
-#pragma unroll
-          for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t pu = p + (size_t)u * blockDim.x;
-        if (pu < p1) {
-          const size_t j0 = pu * W;
-          const int c0 = chunk_of<P>(j0, bnd), c1 = chunk_of<P>(j0 + W - 1, bnd);
-          Pack<T> o;
-#pragma unroll
-          for (int k = 0; k < W; ++k) {
-            T lane[P];
-#pragma unroll
-            for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
-            const int c = (c0 == c1) ? c0 : chunk_of<P>(j0 + k, bnd);
-            o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, c));
-            bad += !finite(o.v[k]);
-          }
-          st_stream(out + j0, o);
-        }
-      }
-    }
-    };
-    for_tiles<U>(a, b, n / W, range);
-    if (b == a.nblocks - 1) {  // scalar tail n % W
-      for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
-        T lane[P];
-#pragma unroll
-        for (int q = 0; q < P; ++q) lane[q] = src[q][j];
-        T r = mean_div<T, P>(rot_sum<T, P>(lane, chunk_of<P>(j, bnd)));
-        out[j] = r;
-        bad += !finite(r);
-      }
-    }
-  }
-  report_nonfinite(a.nonfinite, bad);
-  trace_mark(a, b, 3);
-  if (!VIRTUAL) publish_done(a);
-}
-
-// ------------------------------------------------------------------ two-shot (K3)
-template <typename T, int P>
-__device__ __forceinline__ T ordered_sum(const T* const (&src)[P], int rank, size_t j) {
-  T v[P];
-#pragma unroll
-  for (int q = 0; q < P; ++q) v[q] = src[q][j];
-  return rot_sum<T, P>(v, rank);
-}
-
-// Visit tiles 0..ntiles-1 from the atomic queue `ctr` (next index prefetched), or
-// statically strided over the CTAs when there is no queue (virtual ranks).
-template <typename V>
-__device__ __forceinline__ void queue_loop(unsigned long long* ctr, int b, int nblocks, unsigned long long ntiles,
-                                           V&& visit) {
-  if (ctr == nullptr) {
-    for (unsigned long long t = b; t < ntiles; t += nblocks) visit(t);
-    return;
-  }
-  __shared__ unsigned long long s_next;
-  __syncthreads();
-  if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);
-  __syncthreads();
-  unsigned long long t = s_next;
-  while (t < ntiles) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1ull);
-    visit(t);
-    __syncthreads();
-    t = s_next;
-  }
-}
-
-// Phase-2 work of the two-shot kernels: the aligned body of every chunk c (minus the
-// own chunk when skip_own) in tiles interleaved across chunks and rotated per rank —
-// tile t is the (t / P)-th tile of chunk (rank + 1 + t) % P — so at any moment the
-// CTAs are spread over every owner (NVLink) and over the own chunk (HBM only), and
-// no owner serves all readers at once.  CTA 0 then does the unaligned head/tail
-// elements of every chunk (at most 2W-2 per chunk boundary).
-template <typename T, int P, typename FB, typename FS>
-__device__ __forceinline__ void chunk_tiles(unsigned long long* ctr, int b, int nblocks, size_t n, int rank,
-                                            bool skip_own, size_t tile, FB&& body, FS&& scalar) {
-  constexpr int W = Pack<T>::W;
-  size_t tmax = 0;
-#pragma unroll
-  for (int c = 0; c < P; ++c) {
-    size_t cs, ce, cp0, cp1;
-    chunk_packs<T, P>(n, c, cs, ce, cp0, cp1);
-    const size_t tc = (cp1 - cp0 + tile - 1) / tile;
-    tmax = tc > tmax ? tc : tmax;
-  }
-  queue_loop(ctr, b, nblocks, (unsigned long long)tmax * P, [&](unsigned long long t) {
-    const int c = (rank + 1 + (int)(t % P)) % P;
-    if (skip_own && c == rank) return;
-    size_t cs, ce, cp0, cp1;
-    chunk_packs<T, P>(n, c, cs, ce, cp0, cp1);
-    const size_t a0 = cp0 + (size_t)(t / P) * tile;
-    if (a0 >= cp1) return;
-    body(c, a0, a0 + tile < cp1 ? a0 + tile : cp1);
-  });
-  if (b == 0) {
-    for (int c = 0; c < P; ++c) {
-      if (skip_own && c == rank) continue;
-      size_t cs, ce, cp0, cp1;
-      chunk_packs<T, P>(n, c, cs, ce, cp0, cp1);
-      const size_t he = cp0 * W < ce ? cp0 * W : ce;
-      const size_t ts = cp1 * W > he ? cp1 * W : he;
-      for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(c, j);
-      for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(c, j);
-    }
-  }
-}
-
-// Reduce-scatter of this rank's chunk (ring order x_rank, x_rank+1, ..., x_rank-1)
-// into its xbar buffer: aligned packs from work queue 0, head/tail elements on CTA 0.
-template <typename T, int P, int U>
-__device__ __forceinline__ unsigned reduce_own_chunk(const CommArgs& a, int b, int rank, unsigned long long* q0) {
-  constexpr int W = Pack<T>::W;
-  const size_t n = a.n;
-  unsigned bad = 0;
-  T* own = reinterpret_cast<T*>(a.xbar[rank]);
-  const T* src[P];
-#pragma unroll
-  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
-  size_t cs, ce, cp0, cp1;
-  chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
-  auto range = [&](size_t p0, size_t p1) {
-    for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-      Pack<T> v[U][P];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t pu = p + (size_t)u * blockDim.x;
-        if (pu < p1) {
-#pragma unroll
-          for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + pu * W);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t pu = p + (size_t)u * blockDim.x;
-        if (pu < p1) {
-          Pack<T> o;
-#pragma unroll
-          for (int k = 0; k < W; ++k) {
-            T lane[P];
-#pragma unroll
-            for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
-            o.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
-            bad += !finite(o.v[k]);
-          }
-          st_plain(own + pu * W, o);
-        }
-      }
-    }
-  };
-  tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, range);
-  if (b == 0) {  // unaligned head / tail of the chunk (and tiny chunks)
-    const size_t hs = cs, he = cp0 * W < ce ? cp0 * W : ce;
-    const size_t ts = cp1 * W > hs ? (cp1 * W > he ? cp1 * W : he) : he;
-    for (size_t j = hs + threadIdx.x; j < he; j += blockDim.x) {
-      T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
-      own[j] = r;
-      bad += !finite(r);
-    }
-    for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) {
-      T r = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
-      own[j] = r;
-      bad += !finite(r);
-    }
-  }
-  return bad;
-}
-
-template <typename T, int P, bool VIRTUAL, int U, int UAG>
-__global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
-  constexpr int W = Pack<T>::W;
-  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
-  const int b = blockIdx.x;
-  const size_t n = a.n;
-  bool ok = true;
-  unsigned bad = 0;
-  T* out = reinterpret_cast<T*>(a.xbar[rank]);
-  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
-  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
-  trace_mark(a, b, 0);
-  if (a.phases & 1) {
-    if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
-    trace_mark(a, b, 1);
-    if (ok) bad += reduce_own_chunk<T, P, U>(a, b, rank, q0);
-  }
-  if (a.phases & 2) {
-    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
-    trace_mark(a, b, 2);
-    if (ok) {
-      // all-gather: every pack outside the own chunk comes from its owner's xbar
-      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * UAG * blockDim.x,
-        [&](int c, size_t p0, size_t p1) {
-          const T* zc = reinterpret_cast<const T*>(a.xbar[c]);
-          for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)UAG * blockDim.x) {
-            Pack<T> v[UAG];
-#pragma unroll
-            for (int u = 0; u < UAG; ++u) {
-              const size_t pu = p + (size_t)u * blockDim.x;
-              if (pu < p1) v[u] = ld_cg(zc + pu * W);
-            }
-#pragma unroll
-            for (int u = 0; u < UAG; ++u) {
-              const size_t pu = p + (size_t)u * blockDim.x;
-              if (pu < p1) st_stream(out + pu * W, v[u]);
-            }
-          }
-        },
-        [&](int c, size_t j) { out[j] = reinterpret_cast<const T*>(a.xbar[c])[j]; });
-    }
-  }
-  report_nonfinite(a.nonfinite, bad);
-  trace_mark(a, b, 3);
-  if (!VIRTUAL) publish_done(a);
-}
-
-// ------------------------------------------------------------------ fused round (K7)
-// One pass at a round boundary of the deterministic schedule: the local step (K5) of
-// this minibatch, the mean of the round's snapshots read straight from every peer over
-// NVLink (K2 order), the pull / finalize (K4) and the next snapshot (K1), per element:
-//   x' = K5(x, g, m)                          (sgd_elem)
-//   xbar = (sum_k snap_{(c+k)%P}) / P         (rot_sum / mean_div, ring order)
-//   pull:     x'' = x' + (-alpha)*(snap_own + (-1)*xbar)       (pull_elem)
-//   finalize: x'' = xbar + delta'             (optimizer.py:171; delta' = delta + s)
-//   snap_next = x''
-// Same element functions as the separate kernels, so the result is bit-identical to
-// K5 -> (K2 completes) -> K4 under the deterministic schedule; HBM and NVLink stream
-// concurrently instead of back to back, and xbar never touches HBM.
-template <typename T>
-struct FusedRound {
-  T* x[kMaxR];
-  const T* g[kMaxR];
-  T* m[kMaxR];
-  T* delta[kMaxR];
-  T* snap_next[kMaxR];
-  SgdCoef<T> c;
-  T neg_alpha;
-  int mode;  // 0 pull, 1 reference finalize (delta)
-};
-
-template <typename T, int P, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs a, FusedRound<T> f) {
-  constexpr int W = Pack<T>::W;
-  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
-  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
-  const int b = blockIdx.x;
-  bool ok = true;
-  trace_mark(a, b, 0);
-  // Entry: every peer's snapshot slot must be final and every peer must be done reading
-  // this rank's other slot.  When the previous launch was a round that raised end
-  // signals (K7 one-shot or K8), those certify both and were raised before the peers
-  // even launched this kernel; otherwise the per-CTA entry barrier.
-  if (!VIRTUAL && P > 1) ok = a.prev_end ? rank_wait<P>(a, 1, a.prev_end, b, rank) : cta_barrier<P>(a, 0, b, rank);
-  trace_mark(a, b, 1);
-  unsigned bad = 0;
-  if (ok) {
-    const size_t n = a.n;
-    size_t bnd[P + 1];
-#pragma unroll
-    for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
-    const T* src[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
-    T* const x = f.x[vr];
-    const T* const g = f.g[vr];
-    T* const m = f.m[vr];
-    T* const dl = f.delta[vr];
-    T* const sn = f.snap_next[vr];
-    const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-    const bool store_d = f.c.use_delta && (P == 1 || f.mode == 0);  // finalize resets delta
-    auto element = [&](T& xv, T gv, T& mv, T& dv, const T (&lane)[P], int cidx) -> T {
-      unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
-      if constexpr (P > 1) {
-        const T zb = mean_div<T, P>(rot_sum<T, P>(lane, cidx));
-        if (f.mode == 0) {
-          T own = lane[0];
-#pragma unroll
-          for (int q = 1; q < P; ++q) own = (q == rank) ? lane[q] : own;  // no dynamic register indexing
-          bb += pull_elem(f.neg_alpha, xv, own, zb);
-        } else {
-          xv = add_rn(zb, dv);
-          bb += !finite(xv);
-        }
-      }
-      bad += bb;
-      return xv;
-    };
-    auto range = [&](size_t p0, size_t p1) {
-    for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-      Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U][P];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t pu = p + (size_t)u * blockDim.x;
-        if (pu < p1) {
-          const size_t j = pu * W;
-          vx[u] = ld_stream(x + j);
-          vg[u] = ld_stream(g + j);
-          if (load_m) vm[u] = ld_stream(m + j);
-          if (load_d) vd[u] = ld_stream(dl + j);
-          if constexpr (P > 1) {
-#pragma unroll
-            for (int q = 0; q < P; ++q) vs[u][q] = ld_cg(src[q] + j);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const size_t pu = p + (size_t)u * blockDim.x;
-        if (pu < p1) {
-          const size_t j0 = pu * W;
-          const int c0 = chunk_of<P>(j0, bnd), c1 = chunk_of<P>(j0 + W - 1, bnd);
-#pragma unroll
-          for (int k = 0; k < W; ++k) {
-            T lane[P];
-#pragma unroll
-            for (int q = 0; q < P; ++q) lane[q] = (P > 1) ? vs[u][q].v[k] : T(0);
-            const int cidx = (c0 == c1) ? c0 : chunk_of<P>(j0 + k, bnd);
-            element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], lane, cidx);
-          }
-          st_stream(x + j0, vx[u]);
-          if (f.c.use_mom) st_stream(m + j0, vm[u]);
-          if (store_d) st_stream(dl + j0, vd[u]);
-          st_stream(sn + j0, vx[u]);
-        }
-      }
-    }
-    };
-    for_tiles<U>(a, b, n / W, range);
-    if (b == a.nblocks - 1) {  // scalar tail n % W
-      for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
-        T lane[P];
-#pragma unroll
-        for (int q = 0; q < P; ++q) lane[q] = (P > 1) ? src[q][j] : T(0);
-        T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-        element(xv, g[j], mv, dv, lane, chunk_of<P>(j, bnd));
-        x[j] = xv;
-        if (f.c.use_mom) m[j] = mv;
-        if (store_d) dl[j] = dv;
-        sn[j] = xv;
-      }
-    }
-  }
-  if (!VIRTUAL && P > 1 && ok) rank_signal<P>(a, 1, a.end_ctr, rank);  // certifies the next round's entry
-  report_nonfinite(a.nonfinite, bad);
-  trace_mark(a, b, 3);
-  if (!VIRTUAL) publish_done(a);
-}
-
-// Two-shot form of K7 for larger P: (1) reduce-scatter of this rank's chunk into its
-// xbar buffer (ring order, same as K3), (2) rank-level mid barrier, (3) over every
-// pack: local step + pull with the pack's mean read straight from its owner's xbar
-// (NVLink unless the pack is in the own chunk), next snapshot.  NVLink in-bytes
-// 2(P-1)/P*B; xbar is written only for the own chunk.  Both phases take tiles from
-// work queues.  Virtual ranks run phase 1 and phase 2 as two launches.
-template <typename T, int P, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound<T> f) {
-  constexpr int W = Pack<T>::W;
-  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
-  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
-  const int b = blockIdx.x;
-  const size_t n = a.n;
-  bool ok = true;
-  unsigned bad = 0;
-  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
-  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
-  T* const x = f.x[vr];
-  const T* const g = f.g[vr];
-  T* const m = f.m[vr];
-  T* const dl = f.delta[vr];
-  T* const sn = f.snap_next[vr];
-  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
-  const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-  const bool store_d = f.c.use_delta && f.mode == 0;
-  auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
-    unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
-    if (f.mode == 0) {
-      bb += pull_elem(f.neg_alpha, xv, sv, zb);
-    } else {
-      xv = add_rn(zb, dv);
-      bb += !finite(xv);
-    }
-    bad += bb;
-  };
-  trace_mark(a, b, 0);
-  if (a.phases & 1) {
-    if (!VIRTUAL) ok = cta_barrier<P>(a, 0, b, rank);
-    trace_mark(a, b, 1);
-    if (ok) {
-      // Own chunk, complete in this phase: its mean is formed here (ring order, stored
-      // for the peers' phase 2) and the local step + pull applied right away — the own
-      // snapshot is one of the P sources already in registers.
-      T* own = reinterpret_cast<T*>(a.xbar[rank]);
-      const T* src[P];
-#pragma unroll
-      for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
-      size_t cs, ce, cp0, cp1;
-      chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
-      tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
-        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-          Pack<T> v[U][P], vx[U], vg[U], vm[U], vd[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) {
-              const size_t j = pu * W;
-#pragma unroll
-              for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + j);
-              vx[u] = ld_stream(x + j);
-              vg[u] = ld_stream(g + j);
-              if (load_m) vm[u] = ld_stream(m + j);
-              if (load_d) vd[u] = ld_stream(dl + j);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) {
-              const size_t j = pu * W;
-              Pack<T> z;
-#pragma unroll
-              for (int k = 0; k < W; ++k) {
-                T lane[P];
-#pragma unroll
-                for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
-                T sv = lane[0];
-#pragma unroll
-                for (int q = 1; q < P; ++q) sv = (q == rank) ? lane[q] : sv;
-                z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
-                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], sv, z.v[k]);
-              }
-              st_plain(own + j, z);
-              st_stream(x + j, vx[u]);
-              if (f.c.use_mom) st_stream(m + j, vm[u]);
-              if (store_d) st_stream(dl + j, vd[u]);
-              st_stream(sn + j, vx[u]);
-            }
-          }
-        }
-      });
-      if (b == 0) {  // unaligned head / tail elements of the own chunk
-        const size_t he = cp0 * W < ce ? cp0 * W : ce;
-        const size_t ts = cp1 * W > he ? cp1 * W : he;
-        auto scalar = [&](size_t j) {
-          const T zb = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
-          own[j] = zb;
-          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, snap_own[j], zb);
-          x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
-          if (store_d) dl[j] = dv;
-          sn[j] = xv;
-        };
-        for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
-        for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
-      }
-    }
-  }
-  if (a.phases & 2) {
-    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
-    trace_mark(a, b, 2);
-    if (ok) {
-      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
-        [&](int c, size_t p0, size_t p1) {
-          const T* zc = reinterpret_cast<const T*>(a.xbar[c]);  // owner's reduced chunk (NVLink unless c == rank)
-          for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-            Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const size_t pu = p + (size_t)u * blockDim.x;
-              if (pu < p1) {
-                const size_t j = pu * W;
-                vz[u] = ld_cg(zc + j);
-                vx[u] = ld_stream(x + j);
-                vg[u] = ld_stream(g + j);
-                if (load_m) vm[u] = ld_stream(m + j);
-                if (load_d) vd[u] = ld_stream(dl + j);
-                if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const size_t pu = p + (size_t)u * blockDim.x;
-              if (pu < p1) {
-                const size_t j = pu * W;
-#pragma unroll
-                for (int k = 0; k < W; ++k)
-                  element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
-                st_stream(x + j, vx[u]);
-                if (f.c.use_mom) st_stream(m + j, vm[u]);
-                if (store_d) st_stream(dl + j, vd[u]);
-                st_stream(sn + j, vx[u]);
-              }
-            }
-          }
-        },
-        [&](int c, size_t j) {
-          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), reinterpret_cast<const T*>(a.xbar[c])[j]);
-          x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
-          if (store_d) dl[j] = dv;
-          sn[j] = xv;
-        });
-    }
-  }
-  report_nonfinite(a.nonfinite, bad);
-  trace_mark(a, b, 3);
-  if (!VIRTUAL) publish_done(a);
-}
-
-// Launch `kernel` normally, or cooperatively (all CTAs co-resident, required by the
-// rank-level barrier of the P2P two-shot kernels).  A cooperative grid is clamped to
-// what fits on the device — every rank computes the same clamp on the same GPU type,
-// so the per-CTA flag slots still line up.
 template <typename... Args>
 int launch_kernel(bool coop, void (*kernel)(Args...), dim3 grid, int threads, cudaStream_t s, Args... args) {
   if (!coop) {
@@ -982,336 +146,6 @@ int check_fused_args(int nr, void* const* x, const void* const* g, void* const* 
     if (sgd->momentum != 0.0 && !m[r]) return fail(LASGD_ERR_INVALID_ARGUMENT, "momentum needs m");
   }
   return LASGD_OK;
-}
-
-// ------------------------------------------------------------------ push round (K8)
-// The fused round with the data movement done by remote STORES from the producer.
-// Chunk c is owned by rank c.  Every rank keeps, in its IPC region, a staging area
-// stage[parity][source][chunk] for the contributions to its own chunk.
-//   init (phase bit 4): push chunk c of the current snapshot to owner c's staging.
-//   phase A (bit 1): wait for every rank's end signal of the previous push launch
-//     (staged contributions complete; peers finished their previous round); the owner
-//     forms the ring-order mean of its chunk from local staging + its own snapshot,
-//     applies the local step + pull to its own chunk, and pushes the mean to every
-//     peer's xbar.
-//   rank-level mid barrier (all means pushed).
-//   phase B (bit 2): every other chunk: local step + pull with the mean in the local
-//     xbar, next snapshot written locally and pushed to the owner's staging (other
-//     parity); then the rank-level end signal.
-// Per rank and round: NVLink out 2(P-1)/P*B as posted writes, all reads local.  Same
-// element functions and summation order as K7, so results are bit-identical.
-template <typename T>
-__device__ __forceinline__ T* stage_ptr(const CommArgs& a, int owner, int parity, int src, int P) {
-  return reinterpret_cast<T*>(a.stage[owner]) + ((size_t)parity * P + src) * a.stage_elems;
-}
-
-template <typename T, int P, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T> f) {
-  constexpr int W = Pack<T>::W;
-  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
-  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
-  const int b = blockIdx.x;
-  const size_t n = a.n;
-  const int cur = a.cur, nxt = 1 - a.cur;
-  bool ok = true;
-  unsigned bad = 0;
-  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
-  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
-  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
-  trace_mark(a, b, 0);
-  // offset of element j of chunk c inside a staging slot (keeps 16-byte alignment)
-  auto soff = [&](int c, size_t j) { return j - chunk_bound(n, P, c) / W * W; };
-  if (a.phases & 4) {
-    // initial contributions: chunk c of the current snapshot -> owner c, parity cur
-    chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
-      [&](int c, size_t p0, size_t p1) {
-        T* dst = stage_ptr<T>(a, c, cur, rank, P);
-        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-          Pack<T> v[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) v[u] = ld_stream(snap_own + pu * W);
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) st_plain(dst + soff(c, pu * W), v[u]);
-          }
-        }
-      },
-      [&](int c, size_t j) { stage_ptr<T>(a, c, cur, rank, P)[soff(c, j)] = snap_own[j]; });
-    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
-  }
-  T* const x = f.x[vr];
-  const T* const g = f.g[vr];
-  T* const m = f.m[vr];
-  T* const dl = f.delta[vr];
-  T* const sn = f.snap_next[vr];
-  const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-  const bool store_d = f.c.use_delta && f.mode == 0;
-  auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
-    unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
-    if (f.mode == 0) {
-      bb += pull_elem(f.neg_alpha, xv, sv, zb);
-    } else {
-      xv = add_rn(zb, dv);
-      bb += !finite(xv);
-    }
-    bad += bb;
-  };
-  if (a.phases & 1) {
-    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
-    trace_mark(a, b, 1);
-    if (ok) {
-      const T* src[P];
-#pragma unroll
-      for (int q = 0; q < P; ++q) src[q] = q == rank ? snap_own : stage_ptr<T>(a, rank, cur, q, P);
-      size_t cs, ce, cp0, cp1;
-      chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
-      const size_t base = cs / W * W;  // staging offset origin of the own chunk
-      tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
-        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-          Pack<T> v[U][P], vx[U], vg[U], vm[U], vd[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) {
-              const size_t j = pu * W;
-#pragma unroll
-              for (int q = 0; q < P; ++q) v[u][q] = ld_stream(src[q] + (q == rank ? j : j - base));
-              vx[u] = ld_stream(x + j);
-              vg[u] = ld_stream(g + j);
-              if (load_m) vm[u] = ld_stream(m + j);
-              if (load_d) vd[u] = ld_stream(dl + j);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) {
-              const size_t j = pu * W;
-              Pack<T> z;
-#pragma unroll
-              for (int k = 0; k < W; ++k) {
-                T lane[P];
-#pragma unroll
-                for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
-                T sv = lane[0];
-#pragma unroll
-                for (int q = 1; q < P; ++q) sv = (q == rank) ? lane[q] : sv;
-                z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
-                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], sv, z.v[k]);
-              }
-#pragma unroll
-              for (int q = 0; q < P; ++q)
-                if (q != rank) st_plain(reinterpret_cast<T*>(a.xbar[q]) + j, z);  // the mean to every peer
-              st_stream(x + j, vx[u]);
-              if (f.c.use_mom) st_stream(m + j, vm[u]);
-              if (store_d) st_stream(dl + j, vd[u]);
-              st_stream(sn + j, vx[u]);
-            }
-          }
-        }
-      });
-      if (b == 0) {  // unaligned head / tail elements of the own chunk
-        const size_t he = cp0 * W < ce ? cp0 * W : ce;
-        const size_t ts = cp1 * W > he ? cp1 * W : he;
-        auto scalar = [&](size_t j) {
-          T lane[P];
-#pragma unroll
-          for (int q = 0; q < P; ++q) lane[q] = src[q][q == rank ? j : j - base];
-          const T zb = mean_div<T, P>(rot_sum<T, P>(lane, rank));
-#pragma unroll
-          for (int q = 0; q < P; ++q)
-            if (q != rank) reinterpret_cast<T*>(a.xbar[q])[j] = zb;
-          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, snap_own[j], zb);
-          x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
-          if (store_d) dl[j] = dv;
-          sn[j] = xv;
-        };
-        for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
-        for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
-      }
-    }
-  }
-  if (a.phases & 2) {
-    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
-    trace_mark(a, b, 2);
-    if (ok) {
-      const T* zl = reinterpret_cast<const T*>(a.xbar[rank]);  // means pushed by their owners
-      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
-        [&](int c, size_t p0, size_t p1) {
-          T* dst = stage_ptr<T>(a, c, nxt, rank, P);
-          for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-            Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vz[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const size_t pu = p + (size_t)u * blockDim.x;
-              if (pu < p1) {
-                const size_t j = pu * W;
-                vz[u] = ld_stream(zl + j);
-                vx[u] = ld_stream(x + j);
-                vg[u] = ld_stream(g + j);
-                if (load_m) vm[u] = ld_stream(m + j);
-                if (load_d) vd[u] = ld_stream(dl + j);
-                if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const size_t pu = p + (size_t)u * blockDim.x;
-              if (pu < p1) {
-                const size_t j = pu * W;
-#pragma unroll
-                for (int k = 0; k < W; ++k)
-                  element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
-                st_plain(dst + soff(c, j), vx[u]);  // next-round contribution to owner c
-                st_stream(x + j, vx[u]);
-                if (f.c.use_mom) st_stream(m + j, vm[u]);
-                if (store_d) st_stream(dl + j, vd[u]);
-                st_stream(sn + j, vx[u]);
-              }
-            }
-          }
-        },
-        [&](int c, size_t j) {
-          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), zl[j]);
-          x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
-          if (store_d) dl[j] = dv;
-          sn[j] = xv;
-          stage_ptr<T>(a, c, nxt, rank, P)[soff(c, j)] = xv;
-        });
-      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
-    }
-  }
-  report_nonfinite(a.nonfinite, bad);
-  trace_mark(a, b, 3);
-  if (!VIRTUAL) publish_done(a);
-}
-
-// ------------------------------------------------------------------ mirror push round (K8, P = 2)
-// At P = 2 the push round keeps a full mirror of the peer's snapshot in local HBM: the
-// staging area (2 parities x 2 sources x n/2) is re-used as [parity][n].  Each round
-// reads the own snapshot and the mirror (both local), forms the ring-order mean per
-// element exactly like the one-shot K7, applies local step + pull, writes the next
-// snapshot locally AND stores it into the peer's mirror (other parity) as posted NVLink
-// writes; the rank-level end signals certify the mirror for the next round's entry.
-// One phase, no mid barrier; NVLink out B per round (= the one-shot's B in), as stores.
-template <typename T>
-__device__ __forceinline__ T* mirror_ptr(const CommArgs& a, int owner, int parity) {
-  return reinterpret_cast<T*>(a.stage[owner]) + (size_t)parity * 2 * a.stage_elems;
-}
-
-template <typename T, bool VIRTUAL, int U>
-__global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T> f) {
-  constexpr int P = 2;
-  constexpr int W = Pack<T>::W;
-  const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
-  const int vr = VIRTUAL ? (int)blockIdx.y : 0;
-  const int peer = 1 - rank;
-  const int b = blockIdx.x;
-  const size_t n = a.n;
-  const int cur = a.cur, nxt = 1 - a.cur;
-  bool ok = true;
-  unsigned bad = 0;
-  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
-  trace_mark(a, b, 0);
-  if (a.phases & 4) {  // initial mirror: the current snapshot -> the peer's mirror, parity cur
-    T* dst = mirror_ptr<T>(a, peer, cur);
-    for_tiles<U>(a, b, n / W, [&](size_t p0, size_t p1) {
-      for (size_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) st_plain(dst + p * W, ld_stream(snap_own + p * W));
-    });
-    if (b == a.nblocks - 1)
-      for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) dst[j] = snap_own[j];
-    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
-  }
-  if (a.phases & 1) {
-    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
-    trace_mark(a, b, 1);
-    if (ok) {
-      size_t bnd[P + 1];
-#pragma unroll
-      for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
-      const T* const mir = mirror_ptr<T>(a, rank, cur);  // the peer's snapshot, local copy
-      T* const out = mirror_ptr<T>(a, peer, nxt);          // the peer's copy of our next snapshot
-      T* const x = f.x[vr];
-      const T* const g = f.g[vr];
-      T* const m = f.m[vr];
-      T* const dl = f.delta[vr];
-      T* const sn = f.snap_next[vr];
-      const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-      const bool store_d = f.c.use_delta && f.mode == 0;
-      auto element = [&](T& xv, T gv, T& mv, T& dv, T own, T oth, int cidx) {
-        unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
-        T lane[P];  // lanes by rank, selected without dynamic register indexing
-        lane[0] = rank == 0 ? own : oth;
-        lane[1] = rank == 0 ? oth : own;
-        const T zb = mean_div<T, P>(rot_sum<T, P>(lane, cidx));
-        if (f.mode == 0) {
-          bb += pull_elem(f.neg_alpha, xv, own, zb);
-        } else {
-          xv = add_rn(zb, dv);
-          bb += !finite(xv);
-        }
-        bad += bb;
-      };
-      for_tiles<U>(a, b, n / W, [&](size_t p0, size_t p1) {
-        for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
-          Pack<T> vx[U], vg[U], vm[U], vd[U], vs[U], vo[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) {
-              const size_t j = pu * W;
-              vx[u] = ld_stream(x + j);
-              vg[u] = ld_stream(g + j);
-              if (load_m) vm[u] = ld_stream(m + j);
-              if (load_d) vd[u] = ld_stream(dl + j);
-              vs[u] = ld_stream(snap_own + j);
-              vo[u] = ld_stream(mir + j);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const size_t pu = p + (size_t)u * blockDim.x;
-            if (pu < p1) {
-              const size_t j0 = pu * W;
-              const int c0 = chunk_of<P>(j0, bnd), c1 = chunk_of<P>(j0 + W - 1, bnd);
-#pragma unroll
-              for (int k = 0; k < W; ++k)
-                element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vo[u].v[k],
-                        c0 == c1 ? c0 : chunk_of<P>(j0 + k, bnd));
-              st_plain(out + j0, vx[u]);  // posted NVLink write into the peer's mirror
-              st_stream(x + j0, vx[u]);
-              if (f.c.use_mom) st_stream(m + j0, vm[u]);
-              if (store_d) st_stream(dl + j0, vd[u]);
-              st_stream(sn + j0, vx[u]);
-            }
-          }
-        }
-      });
-      if (b == a.nblocks - 1) {  // scalar tail n % W
-        for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) {
-          T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, snap_own[j], mir[j], chunk_of<P>(j, bnd));
-          x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
-          if (store_d) dl[j] = dv;
-          sn[j] = xv;
-          out[j] = xv;
-        }
-      }
-      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
-    }
-  }
-  report_nonfinite(a.nonfinite, bad);
-  trace_mark(a, b, 3);
-  if (!VIRTUAL) publish_done(a);
 }
 
 // ------------------------------------------------------------------ dispatch
