@@ -204,6 +204,40 @@ def _w_sgd_ar(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_full_size(rank, world, port):
+    """The bench's configuration at BASELINE size: ResNet-50's n, Nesterov momentum +
+    weight decay, sync period 1, fused pipeline with the AUTO algorithm (mirror push at
+    P=2, staged push at P>=3) — bit-exact against the oracle on every rank."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+
+    _init(rank, world, port)
+    n, steps = 25_557_032, 2
+    rng = np.random.default_rng(2024)
+    x0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    grads = np.stack([np.stack([(np.random.default_rng(10 * t + r).standard_normal(n) * 0.01).astype(np.float32)
+                                for r in range(world)]) for t in range(steps)])
+    comm = L.P2PCommunicator(n, timeout_s=60.0)
+    x = torch.from_numpy(x0.copy()).cuda()
+    g = torch.empty_like(x)
+    sgd = L.SgdConfig(0.9, 0.0, 1e-4, True)
+    w = L.LASGDWorker(x, g, comm=comm, sync_period=1, alpha=1.0, sgd=sgd, lr=0.1, mode="pull", pipeline="fused")
+    for t in range(steps):
+        g.copy_(torch.from_numpy(grads[t, rank]))
+        w.step()
+    w.drain()
+    torch.cuda.synchronize()
+    ref, _, _, _ = O.run_lasgd_pull(x0, grads, np.full(steps, 0.1), world, 1, 1.0,
+                                    sgd=O.SgdConfig(0.1, 0.9, 0.0, 1e-4, True))
+    assert _same_bits(x.cpu().numpy(), ref[rank]), (world, rank)
+    dist.barrier()
+    w.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def _w_fault(rank, world, port):
     import torch.distributed as dist
 
@@ -250,6 +284,11 @@ def test_worker_round_protocol_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_sgd_ar_worker_bit_exact():
     _spawn(_w_sgd_ar)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_fused_auto_full_resnet50_size_bit_exact():
+    _spawn(_w_full_size)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
