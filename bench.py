@@ -505,13 +505,14 @@ def main():
         kernels[name] = entry
     dom = max(kernels, key=lambda k: sum(ktimes[k]))
     d = kernels[dom]
-    # ncu profiles one GPU only: the N=1 kernel has a measured DRAM traffic; the multi-rank
-    # kernels' traffic cannot be captured (their virtual-rank forms are in ncu_traffic.json)
+    # ncu profiles one GPU only: the N=1 kernel is measured directly; a multi-rank round is
+    # measured in its virtual-rank form (all ranks on one GPU, same device code, per rank)
     tr = traffic.get(dom) if world == 1 else traffic.get(f"{dom}_p{world}")
     roofline = {"kernel": dom, "bound": "hbm" if d["bound"] == "hbm" else "nvlink", "achieved": d["achieved_gbs"],
                 "peak": d["peak_gbs"], "unit": "GB/s", "frac": d["frac"], "traffic": tr,
-                "traffic_source": ("ncu --set full, profiles/ncu_traffic.json" if tr is not None
-                                   else "not measurable: ncu runs on one GPU, this kernel spans ranks"),
+                "traffic_source": ("not measured: ncu runs on one GPU and this round has no virtual-rank capture"
+                                   if tr is None else "ncu --set full, profiles/ncu_traffic.json" if world == 1
+                                   else "ncu --set full of the virtual-rank form, per rank, profiles/ncu_traffic.json"),
                 "algorithmic_bytes": d["bytes_per_launch"],
                 "peak_source": (f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})" if d["bound"] == "hbm"
                                 else "B200_PROFILING.md measured peer copy 770 GB/s/direction")}
