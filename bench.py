@@ -9,8 +9,8 @@ minibatch's synthetic gradient under the deterministic schedule (sync period 1,
 the paper's tau_max = 1): the local step (Nesterov momentum 0.9, weight decay
 1e-4 — PAPER.md:229) and the round boundary — mean of every rank's snapshot
 over NVLink, elastic pull, next snapshot.  Default `--pipeline fused`: one
-kernel per boundary step (K7 one-shot at P=2, K8 push round at P>=3 — `--algo`
-overrides); `--pipeline overlap`: K5, then K4 with the K2/K3 all-reduce on a
+kernel per boundary step (P=1: K5 + snapshot; P=2: K8 mirror push; P>=3: K8 staged
+push — `--algo` overrides); `--pipeline overlap`: K5, then K4 with the K2/K3 all-reduce on a
 low-priority side stream.  images/s = images whose gradients the sync path
 consumed per second over all ranks.
 
