@@ -199,7 +199,7 @@ int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len);
 unsigned long long lasgd_comm_bytes_per_node(lasgd_comm* c, int algo);
 int lasgd_comm_resolve_algo(lasgd_comm* c, int algo);
 /* The algorithm lasgd_comm_fused_round runs for `algo`: AUTO resolves to PUSH (the
- * mirror form) at P = 2 for buffers >= 1 MiB, otherwise to one-shot where the all-reduce
+ * mirror form) at P = 2 for buffers >= 32 MiB, otherwise to one-shot where the all-reduce
  * would be one-shot and to PUSH where it would be two-shot. */
 int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo);
 /* Change the SM budget (CTAs per launch) for subsequent launches; every rank must

@@ -270,11 +270,13 @@ int resolve_algo(int algo, int P, size_t bytes) {
 // the same NVLink bytes with stores only and no entry wait on peers' snapshots
 // (measured 3-5% faster per round at P=3/4, profiles/bench_r01_algo_*.json).
 // At P = 2 the push round is the mirror form: same bytes as the one-shot, moved as
-// posted stores, ~6% faster per round at ResNet-50 size (profiles/k8_mirror_ab_r01_p2.jsonl).
+// posted stores: ~6% faster per round at ResNet-50 size (profiles/k8_mirror_ab_r01_p2.jsonl)
+// and at ResNet-18 size (90 vs 96 us), 4% slower at MobileNetV2 size (48 vs 46 us), so the
+// crossover sits between 14 and 45 MB (profiles/small_models_r01.jsonl).
 int resolve_fused_algo(int algo, int P, size_t bytes) {
   if (P <= 1) return LASGD_ALGO_ONESHOT;
   if (algo != LASGD_ALGO_AUTO) return algo;
-  if (P == 2) return bytes >= ((size_t)1 << 20) ? LASGD_ALGO_PUSH : LASGD_ALGO_ONESHOT;
+  if (P == 2) return bytes >= ((size_t)32 << 20) ? LASGD_ALGO_PUSH : LASGD_ALGO_ONESHOT;
   const int a = resolve_algo(algo, P, bytes);
   return a == LASGD_ALGO_TWOSHOT ? LASGD_ALGO_PUSH : a;
 }

@@ -53,7 +53,7 @@ def _w_allreduce(rank, world, port):
         for n in (3, 1001, 65_537, 4_000_037):
             comm = L.P2PCommunicator(n, dtype=dtype, nblocks=24, timeout_s=20.0)
             ar = comm.resolve_algo(N.ALGO_AUTO)
-            big = world == 2 and n * dtype.itemsize >= (1 << 20)
+            big = world == 2 and n * dtype.itemsize >= (32 << 20)
             assert comm.resolve_fused_algo(N.ALGO_AUTO) == (N.ALGO_PUSH if ar == N.ALGO_TWOSHOT or big else ar)
             assert comm.resolve_fused_algo(N.ALGO_TWOSHOT) == N.ALGO_TWOSHOT
             if world >= 3 and n * dtype.itemsize > (4 << 20):
