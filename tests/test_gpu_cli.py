@@ -57,6 +57,18 @@ def test_cli_run_single_gpu(tmp_path):
     assert cli.main(["plotdata", outs["sgd_ar"], outs["lasgd"], "--out", str(tmp_path / "p.csv")]) == 0
 
 
+def test_cli_run_image_model(tmp_path):
+    """problem.kind = resnet18 (synthetic CIFAR-shaped batch, bf16 autocast fwd/bwd)."""
+    from paper_2203_13085_b200 import cli
+
+    out = str(tmp_path / "r18")
+    cfg = _cfg(str(tmp_path), "r18", problem={"kind": "resnet18", "batch": 16}, steps=6,
+               lasgd={"tau_max": 2, "pipeline": "fused"}, sgd={"momentum": 0.9, "nesterov": True})
+    assert cli.main(["run", "--config", cfg, "--out", out]) == 0
+    s = json.load(open(os.path.join(out, "summary.json")))
+    assert s["rounds"] == 3 and s["n_params"] == 11_181_642 and s["final_loss"] == s["final_loss"]
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
