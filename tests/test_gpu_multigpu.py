@@ -238,6 +238,40 @@ def _w_full_size(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_ragged(rank, world, port):
+    """Fused rounds through the communicator at tiny / ragged n (empty chunks when n < P,
+    packs straddling chunk bounds) for every fused algorithm, bit-exact vs the oracle."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+
+    _init(rank, world, port)
+    steps = 4
+    mom = L.SgdConfig(0.9, 0.0, 1e-4, True)
+    for n in (1, 3, 5, 7, 33, 4099):
+        x0 = _vec(n + 1, n)
+        grads = np.stack([np.stack([_vec(1000 * n + 10 * t + r, n) for r in range(world)]) for t in range(steps)])
+        for algo in (1, 2, 3):
+            comm = L.P2PCommunicator(n, nblocks=8, timeout_s=20.0)
+            x = torch.from_numpy(x0.copy()).cuda()
+            g = torch.empty_like(x)
+            w = L.LASGDWorker(x, g, comm=comm, sync_period=1, alpha=0.5, sgd=mom, lr=0.05, mode="pull",
+                              pipeline="fused", algo=algo)
+            for t in range(steps):
+                g.copy_(torch.from_numpy(grads[t, rank]))
+                w.step()
+            w.drain()
+            torch.cuda.synchronize()
+            xs, _, _, _ = O.run_lasgd_pull(x0, grads, np.full(steps, 0.05), world, 1, 0.5,
+                                           sgd=O.SgdConfig(0.05, 0.9, 0.0, 1e-4, True))
+            assert _same_bits(x.cpu().numpy(), xs[rank]), (n, algo, rank)
+            dist.barrier()
+            w.close()
+            comm.close()
+    dist.destroy_process_group()
+
+
 def _w_fault(rank, world, port):
     import torch.distributed as dist
 
@@ -289,6 +323,11 @@ def test_sgd_ar_worker_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_fused_auto_full_resnet50_size_bit_exact():
     _spawn(_w_full_size)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_fused_rounds_ragged_sizes_bit_exact():
+    _spawn(_w_ragged)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
