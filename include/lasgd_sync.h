@@ -139,7 +139,7 @@ typedef struct {
   int threads;          /* threads per CTA (multiple of 32 in [64, 256]; <= 128 regs each)     */
   double timeout_s;     /* watchdog for a peer flag (→ CollectiveFailure), e.g. 30.0          */
   long long fault_seq;  /* TEST KNOB: skip this rank's flag writes in launch #fault_seq (-1 off) */
-  int fault_phase;      /* 0 entry barrier, 1 mid barrier                                     */
+  int fault_phase;      /* 0 entry barrier, 1 mid barrier, 2 end-of-round signal              */
 } lasgd_comm_config;
 
 /* Allocates this rank's IPC-exportable region: signal pad + snapshot slot 0/1

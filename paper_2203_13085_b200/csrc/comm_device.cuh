@@ -250,7 +250,9 @@ __device__ void rank_signal(const CommArgs& a, int kind, unsigned* ctr, int rank
   }
   __syncthreads();
   const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)kind * kMaxR;
-  if (s_last && threadIdx.x < P && !(kind == 0 && a.skip_signal_phase == 1)) {
+  // fault injection (test knob): phase 1 drops the mid signal, phase 2 the end signal
+  if (s_last && threadIdx.x < P && !(kind == 0 && a.skip_signal_phase == 1) &&
+      !(kind == 1 && a.skip_signal_phase == 2)) {
     __threadfence_system();
     st_release_sys(a.pad[threadIdx.x] + slot + rank, a.epoch);
   }
@@ -267,7 +269,7 @@ __device__ bool rank_wait(const CommArgs& a, int kind, uint32_t epoch, int b, in
     const unsigned long long t0 = globaltimer();
     while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) {
       if ((long long)(globaltimer() - t0) > a.timeout_ns) {
-        report_failure(a, ERR_TIMEOUT, q, 1, b, rank);
+        report_failure(a, ERR_TIMEOUT, q, kind + 1, b, rank);  // phase 1 mid, 2 end, 3 gate
         ok = 0;
         break;
       }

@@ -874,7 +874,8 @@ extern "C" int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len) {
   if (!c || !buf || !len) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
   const uint32_t* st = c->status_host;
   const unsigned long long fs = (unsigned long long)st[ST_SEQ_LO] | ((unsigned long long)st[ST_SEQ_HI] << 32);
-  const char* phase = st[ST_PHASE] == 0 ? "entry" : "mid";
+  static const char* const kPhaseName[] = {"entry", "mid", "end-of-round", "launch gate"};
+  const char* phase = st[ST_PHASE] < 4 ? kPhaseName[st[ST_PHASE]] : "unknown";
   switch (st[ST_ERR]) {
     case ERR_NONE: snprintf(buf, len, "ok"); break;
     case ERR_TIMEOUT:

@@ -298,6 +298,34 @@ def _w_fault(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_fault_end_signal(rank, world, port):
+    """A rank that never raises its end-of-round signal (fault phase 2) in a fused push /
+    mirror round: the next round's entry wait trips the watchdog and every rank's worker
+    raises CollectiveFailure instead of hanging."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+
+    _init(rank, world, port)
+    n = 4099
+    comm = L.P2PCommunicator(n, nblocks=8, timeout_s=1.0, fault_seq=3 if rank == 1 else -1, fault_phase=2)
+    x = torch.randn(n, device="cuda")
+    g = torch.randn(n, device="cuda")
+    w = L.LASGDWorker(x, g, comm=comm, sync_period=1, lr=0.01, pipeline="fused", algo=3)
+    with pytest.raises(L.CollectiveFailure):
+        for _ in range(6):  # launch 1 stages the snapshot, 2.. are rounds; rank 1 skips end(3)
+            w.step()
+        torch.cuda.synchronize()  # in-flight rounds time out after 1 s
+        w.step()
+    torch.cuda.synchronize()
+    diag = comm.diagnostic()
+    assert ("end-of-round" in diag and "timed out" in diag) or "injected" in diag, diag
+    dist.barrier()
+    w.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def _spawn(fn):
     import torch.multiprocessing as mp
 
@@ -328,6 +356,11 @@ def test_fused_auto_full_resnet50_size_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_fused_rounds_ragged_sizes_bit_exact():
     _spawn(_w_ragged)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_watchdog_missing_end_signal_fails_every_rank():
+    _spawn(_w_fault_end_signal)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
