@@ -262,7 +262,9 @@ size_t elem_bytes(int dtype) { return dtype == LASGD_F64 ? 8 : 4; }
 int resolve_algo(int algo, int P, size_t bytes) {
   if (algo != LASGD_ALGO_AUTO) return algo;
   if (P <= 2) return LASGD_ALGO_ONESHOT;
-  const size_t cutoff = P <= 4 ? (size_t)2 << 20 : (size_t)1 << 20;
+  // P <= 4: one-shot still wins at 4 MB (42 vs 53 us all-reduce, 43 vs 48 us fused),
+  // two-shot / push from 16 MB (profiles/allreduce_sweep_r01_v2_p4.jsonl)
+  const size_t cutoff = P <= 4 ? (size_t)8 << 20 : (size_t)1 << 20;
   return bytes <= cutoff ? LASGD_ALGO_ONESHOT : LASGD_ALGO_TWOSHOT;
 }
 

@@ -56,7 +56,7 @@ def _w_allreduce(rank, world, port):
             big = world == 2 and n * dtype.itemsize >= (32 << 20)
             assert comm.resolve_fused_algo(N.ALGO_AUTO) == (N.ALGO_PUSH if ar == N.ALGO_TWOSHOT or big else ar)
             assert comm.resolve_fused_algo(N.ALGO_TWOSHOT) == N.ALGO_TWOSHOT
-            if world >= 3 and n * dtype.itemsize > (4 << 20):
+            if world >= 3 and n * dtype.itemsize > (8 << 20):
                 assert ar == N.ALGO_TWOSHOT
             for rnd in range(4):
                 for algo in (N.ALGO_ONESHOT, N.ALGO_TWOSHOT):

@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--threads", type=int, default=256)
+    ap.add_argument("--fused-algos", default="auto,oneshot,push",
+                    help="fused-round algorithms to time per size ('' to skip)")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -86,6 +88,44 @@ def main():
                                       "nvlink_gbs": nv / (ar_ms * 1e-3) / 1e9,
                                       "busbw_gbs": 2 * (world - 1) / world * 4 * n / (ar_ms * 1e-3) / 1e9,
                                       "round_ms": round_ms}), flush=True)
+        # the fused round (K7 / K8: local step + mean + pull + next snapshot in one kernel)
+        # against the same work as separate kernels (K5, K1, K2/K3, K4)
+        if a.fused_algos:
+            g = torch.randn(n, device=dev) * 1e-3
+            m = torch.zeros(n, device=dev)
+            fk = dict(m=m, momentum=0.9, weight_decay=1e-4, nesterov=True, alpha=0.5, stream=s)
+            fcodes = {"auto": N.ALGO_AUTO, "oneshot": N.ALGO_ONESHOT, "twoshot": N.ALGO_TWOSHOT, "push": N.ALGO_PUSH}
+            for alg in a.fused_algos.split(","):
+                code = fcodes[alg]
+                with torch.cuda.stream(s):
+                    for i in range(a.warmup):
+                        comm.fused_round(i % 2, x, g, 1e-3, algo=code, **fk)
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(s)
+                    for i in range(a.reps):
+                        comm.fused_round(i % 2, x, g, 1e-3, algo=code, **fk)
+                    e1.record(s)
+                    torch.cuda.synchronize()
+                    f_ms = tmax(e0.elapsed_time(e1) / a.reps)
+                    dist.barrier()
+                    e0.record(s)
+                    for i in range(a.reps):
+                        K.sgd_step(x, g, 1e-3, m=m, momentum=0.9, weight_decay=1e-4, nesterov=True, stream=s)
+                        K.snapshot(comm.snapshots[i % 2], x, stream=s)
+                        comm.allreduce(i % 2, N.ALGO_AUTO, stream=s)
+                        K.elastic_pull(x, comm.snapshots[i % 2], comm.xbar, 0.5, stream=s)
+                    e1.record(s)
+                    torch.cuda.synchronize()
+                    sep_ms = tmax(e0.elapsed_time(e1) / a.reps)
+                if rank == 0:
+                    print(json.dumps({"P": world, "MB": 4 * n / 1e6, "n": n, "fused_algo": alg,
+                                      "resolved": comm.resolve_fused_algo(code), "fused_round_ms": f_ms,
+                                      "separate_kernels_ms": sep_ms, "speedup": sep_ms / f_ms,
+                                      "busbw_equiv_gbs": 2 * (world - 1) / world * 4 * n / (f_ms * 1e-3) / 1e9}),
+                          flush=True)
+            del g, m
         # NCCL all-reduce (sum) of the same buffer, for context (not on the product path)
         y = x.clone()
         for _ in range(a.warmup):
