@@ -166,6 +166,9 @@ int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, u
  *   mode 0 (pull):     x = x + (-alpha)*(snap_own + (-1)*xbar)
  *   mode 1 (finalize): x = xbar + delta            (optimizer.py:171; delta then resets)
  *   snapshot slot 1-snap_slot = x.
+ *   mode 2 (SGD-AR, optimizer.py:214-242): the slots hold gradients; x = K5(x, mean of
+ *   every rank's slot `snap_slot`) with the rate/momentum of `sgd` — g and delta unused,
+ *   no slot written; one-shot or two-shot only (AUTO as for the all-reduce).
  * Bit-identical to lasgd_sgd_step -> lasgd_comm_allreduce -> lasgd_elastic_pull /
  * lasgd_finalize under the same schedule; launched on `stream` with `nblocks` CTAs
  * (<= 0: the communicator's budget), `algo` one-shot (every peer's whole snapshot) or
@@ -226,7 +229,8 @@ int lasgd_comm_peers_ahead(lasgd_comm* c, unsigned long long seq);
  * all-reduce never holds a CTA per SM while a late peer catches up (which would
  * starve the compute stream).  Collective setting: every rank must use the same. */
 int lasgd_comm_set_gate(lasgd_comm* c, int on);
-/* The caller rewrote a snapshot slot outside the push round: the next push round
+/* The caller rewrote a snapshot slot outside the fused rounds (also resets the chain of
+ * end-of-round signals the next K7 would otherwise enter on).  The next push round
  * re-stages the current snapshot first. */
 int lasgd_comm_invalidate_staging(lasgd_comm* c);
 /* Number of launches this rank has issued on the communicator (its current sequence number). */

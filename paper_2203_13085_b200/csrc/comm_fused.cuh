@@ -29,7 +29,7 @@ struct FusedRound {
   T* snap_next[kMaxR];
   SgdCoef<T> c;
   T neg_alpha;
-  int mode;  // 0 pull, 1 reference finalize (delta)
+  int mode;  // 0 pull, 1 reference finalize (delta), 2 SGD-AR (step with the mean of the slots)
 };
 
 template <typename T, int P, bool VIRTUAL, int U>
@@ -63,6 +63,12 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
     const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
     const bool store_d = f.c.use_delta && (P == 1 || f.mode == 0);  // finalize resets delta
     auto element = [&](T& xv, T gv, T& mv, T& dv, const T (&lane)[P], int cidx) -> T {
+      if constexpr (P > 1) {
+        if (f.mode == 2) {  // SGD-AR: the local step with the ring-order mean of the gradients
+          bad += sgd_elem(f.c, xv, mean_div<T, P>(rot_sum<T, P>(lane, cidx)), mv, dv);
+          return xv;
+        }
+      }
       unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
       if constexpr (P > 1) {
         const T zb = mean_div<T, P>(rot_sum<T, P>(lane, cidx));
@@ -88,7 +94,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
         if (pu < p1) {
           const size_t j = pu * W;
           vx[u] = ld_stream(x + j);
-          vg[u] = ld_stream(g + j);
+          if (f.mode != 2) vg[u] = ld_stream(g + j);
           if (load_m) vm[u] = ld_stream(m + j);
           if (load_d) vd[u] = ld_stream(dl + j);
           if constexpr (P > 1) {
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
           st_stream(x + j0, vx[u]);
           if (f.c.use_mom) st_stream(m + j0, vm[u]);
           if (store_d) st_stream(dl + j0, vd[u]);
-          st_stream(sn + j0, vx[u]);
+          if (f.mode != 2) st_stream(sn + j0, vx[u]);
         }
       }
     }
@@ -126,11 +132,11 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
 #pragma unroll
         for (int q = 0; q < P; ++q) lane[q] = (P > 1) ? src[q][j] : T(0);
         T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-        element(xv, g[j], mv, dv, lane, chunk_of<P>(j, bnd));
+        element(xv, f.mode == 2 ? T(0) : g[j], mv, dv, lane, chunk_of<P>(j, bnd));
         x[j] = xv;
         if (f.c.use_mom) m[j] = mv;
         if (store_d) dl[j] = dv;
-        sn[j] = xv;
+        if (f.mode != 2) sn[j] = xv;
       }
     }
   }
@@ -166,6 +172,10 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
   const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
   const bool store_d = f.c.use_delta && f.mode == 0;
   auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
+    if (f.mode == 2) {  // SGD-AR: the local step with the mean gradient
+      bad += sgd_elem(f.c, xv, zb, mv, dv);
+      return;
+    }
     unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
     if (f.mode == 0) {
       bb += pull_elem(f.neg_alpha, xv, sv, zb);
@@ -200,7 +210,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
 #pragma unroll
               for (int q = 0; q < P; ++q) v[u][q] = ld_cg(src[q] + j);
               vx[u] = ld_stream(x + j);
-              vg[u] = ld_stream(g + j);
+              if (f.mode != 2) vg[u] = ld_stream(g + j);
               if (load_m) vm[u] = ld_stream(m + j);
               if (load_d) vd[u] = ld_stream(dl + j);
             }
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
               st_stream(x + j, vx[u]);
               if (f.c.use_mom) st_stream(m + j, vm[u]);
               if (store_d) st_stream(dl + j, vd[u]);
-              st_stream(sn + j, vx[u]);
+              if (f.mode != 2) st_stream(sn + j, vx[u]);
             }
           }
         }
@@ -238,11 +248,11 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
           const T zb = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
           own[j] = zb;
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, snap_own[j], zb);
+          element(xv, f.mode == 2 ? T(0) : g[j], mv, dv, snap_own[j], zb);
           x[j] = xv;
           if (f.c.use_mom) m[j] = mv;
           if (store_d) dl[j] = dv;
-          sn[j] = xv;
+          if (f.mode != 2) sn[j] = xv;
         };
         for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
         for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
                 const size_t j = pu * W;
                 vz[u] = ld_cg(zc + j);
                 vx[u] = ld_stream(x + j);
-                vg[u] = ld_stream(g + j);
+                if (f.mode != 2) vg[u] = ld_stream(g + j);
                 if (load_m) vm[u] = ld_stream(m + j);
                 if (load_d) vd[u] = ld_stream(dl + j);
                 if (f.mode == 0) vs[u] = ld_stream(snap_own + j);
@@ -282,18 +292,19 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
                 st_stream(x + j, vx[u]);
                 if (f.c.use_mom) st_stream(m + j, vm[u]);
                 if (store_d) st_stream(dl + j, vd[u]);
-                st_stream(sn + j, vx[u]);
+                if (f.mode != 2) st_stream(sn + j, vx[u]);
               }
             }
           }
         },
         [&](int c, size_t j) {
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
-          element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), reinterpret_cast<const T*>(a.xbar[c])[j]);
+          element(xv, f.mode == 2 ? T(0) : g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0),
+                  reinterpret_cast<const T*>(a.xbar[c])[j]);
           x[j] = xv;
           if (f.c.use_mom) m[j] = mv;
           if (store_d) dl[j] = dv;
-          sn[j] = xv;
+          if (f.mode != 2) sn[j] = xv;
         });
     }
   }

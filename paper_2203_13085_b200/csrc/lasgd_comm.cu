@@ -133,7 +133,8 @@ FusedRound<T> make_fused(int nr, void* const* x, const void* const* g, void* con
 int check_fused_args(int nr, void* const* x, const void* const* g, void* const* m, void* const* delta,
                      void* const* snap_next, const lasgd_sgd_params* sgd, double alpha, int mode) {
   if (!sgd) return fail(LASGD_ERR_INVALID_ARGUMENT, "null sgd params");
-  if (mode != 0 && mode != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "mode %d (0 pull, 1 finalize)", mode);
+  if (mode < 0 || mode > 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "mode %d (0 pull, 1 finalize, 2 SGD-AR)", mode);
+  if (mode == 2 && delta && delta[0]) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round has no delta");
   if (mode == 0 && !(alpha > 0.0 && alpha <= 1.0)) return fail(LASGD_ERR_INVALID_ARGUMENT, "alpha must be in (0, 1], got %g", alpha);
   if (mode == 1 && (!delta || !delta[0])) return fail(LASGD_ERR_INVALID_ARGUMENT, "finalize mode needs the delta buffer");
   if (sgd->momentum != 0.0 && !m) return fail(LASGD_ERR_INVALID_ARGUMENT, "momentum needs m");
@@ -340,6 +341,7 @@ extern "C" int lasgd_fused_round_virtual(int P, int algo, void* const* x, const 
   if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
   int rc = check_fused_args(P, x, g, m, delta, snap_next, sgd, alpha, mode);
   if (rc) return rc;
+  if (mode == 2 && P < 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round needs P >= 2");
   if (P == 1)  // no peers: the streaming local step with the snapshot store fused in
     return sgd_step_snapshot(dtype, x[0], g[0], m ? m[0] : nullptr, delta ? delta[0] : nullptr, snap_next[0], n, sgd,
                              nonfinite, stream);
@@ -647,6 +649,7 @@ extern "C" int lasgd_comm_peers_ahead(lasgd_comm* c, unsigned long long seq) {
 extern "C" int lasgd_comm_invalidate_staging(lasgd_comm* c) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   c->push_slot = -1;
+  c->end_seq = 0;  // a slot was rewritten outside the rounds: the next K7 uses the entry barrier
   return LASGD_OK;
 }
 
@@ -761,7 +764,11 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
                                       void* delta, const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                                       unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
-  algo = resolve_fused_algo(algo, c->world, c->n * c->elem);
+  // SGD-AR (mode 2) averages gradients that backward wrote into the slots, so there is
+  // nothing to push ahead: one-shot or two-shot, chosen like the all-reduce
+  if (mode == 2 && c->world < 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round needs P >= 2");
+  if (mode == 2 && algo == LASGD_ALGO_PUSH) return fail(LASGD_ERR_INVALID_ARGUMENT, "no push form of the SGD-AR round");
+  algo = mode == 2 ? resolve_algo(algo, c->world, c->n * c->elem) : resolve_fused_algo(algo, c->world, c->n * c->elem);
   const bool push = algo == LASGD_ALGO_PUSH;
   if (!push && algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT)
     return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
@@ -819,14 +826,17 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
   if (rc) return rc;
   a.nblocks = nblocks;
   a.nonfinite = nonfinite;
-  if (algo == LASGD_ALGO_ONESHOT && c->end_seq != 0 && c->end_seq + 1 == s) a.prev_end = (uint32_t)c->end_seq;
+  // (not for SGD-AR: its inputs are written by backward after the previous round ended)
+  if (algo == LASGD_ALGO_ONESHOT && mode != 2 && c->end_seq != 0 && c->end_seq + 1 == s)
+    a.prev_end = (uint32_t)c->end_seq;
   c->push_slot = -1;  // this round writes the next snapshot without staging it
   if (c->dtype == LASGD_F32)
     rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, algo);
   else
     rc = launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, algo);
   if (rc) return rc;
-  c->end_seq = algo == LASGD_ALGO_ONESHOT ? s : 0;  // the one-shot K7 raises end signals
+  // the one-shot K7 raises end signals that certify its next snapshot; SGD-AR writes none
+  c->end_seq = (algo == LASGD_ALGO_ONESHOT && mode != 2) ? s : 0;
   LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
   if (seq) *seq = s;
   return LASGD_OK;

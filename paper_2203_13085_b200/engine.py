@@ -255,11 +255,11 @@ class SGDARWorker:
     """SGD-AR baseline (optimizer.py:214-242, ``sync_allreduce_sgd_round``) per process.
 
     Backward writes the gradient straight into one of the communicator's registered
-    snapshot slots (``grad_buffer``), ``step()`` then launches the NVLink mean
-    all-reduce of the gradients (K2/K3, the reference ring's per-chunk order, so the
-    mean and therefore every replica's model stay bit-identical) and K5 with the mean
-    gradient, both on the compute stream: the synchronous data-parallel step LASGD is
-    compared against (Table 4).
+    snapshot slots (``grad_buffer``); ``step()`` then runs ONE fused kernel on the compute
+    stream (K7 mode 2): the ring-order mean of every rank's gradient slot over NVLink
+    (one-shot or two-shot; the reference ring's per-chunk order, so the mean and therefore
+    every replica's model stay bit-identical) and K5 with the mean gradient — the
+    synchronous data-parallel step LASGD is compared against (Table 4).
 
     The slots alternate per step: peers may still be reading this step's slot while
     this rank runs the next backward; the slot is rewritten two steps later, after the
@@ -302,17 +302,21 @@ class SGDARWorker:
     def step(self) -> None:
         """Mean of every rank's ``grad_buffer`` then ``x = K5(x, mean)`` (call on the
         compute stream after backward; every rank must call it the same number of times)."""
-        g = self.grad_buffer
-        if self.comm is not None:
-            self.comm.allreduce(self._slot, self.algo, stream=self.compute)
-            self.launches["allreduce"] += 1
-            g = self.comm.xbar
-            self._slot ^= 1
         s = self.sgd
-        K.sgd_step(self.x, g, self.current_lr(), m=self.m, momentum=s.momentum, dampening=s.dampening,
-                   weight_decay=s.weight_decay, nesterov=s.nesterov, first_step=self.local_clock == 0,
-                   nonfinite=self._finite.counter, stream=self.compute)
-        self.launches["sgd_step"] += 1
+        if self.comm is not None:
+            # one fused pass (K7 mode 2): ring-order mean of every rank's gradient slot
+            # (over NVLink) and the local step with it
+            self.comm.fused_round(self._slot, self.x, self.x, self.current_lr(), m=self.m, momentum=s.momentum,
+                                  dampening=s.dampening, weight_decay=s.weight_decay, nesterov=s.nesterov,
+                                  first_step=self.local_clock == 0, mode=2, algo=self.algo,
+                                  nonfinite=self._finite.counter, stream=self.compute)
+            self.launches["fused_round"] += 1
+            self._slot ^= 1
+        else:
+            K.sgd_step(self.x, self.grad_buffer, self.current_lr(), m=self.m, momentum=s.momentum,
+                       dampening=s.dampening, weight_decay=s.weight_decay, nesterov=s.nesterov,
+                       first_step=self.local_clock == 0, nonfinite=self._finite.counter, stream=self.compute)
+            self.launches["sgd_step"] += 1
         self.local_clock += 1
         if self.flat is not None and self.comm is not None:
             self.flat.bind_grads(self.grad_buffer)

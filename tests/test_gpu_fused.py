@@ -169,3 +169,38 @@ def test_push_round_finalize_mode():
     ref, _, _, _ = O.run_lasgd_delta(x0, grads, [0.03, 0.03], P, 1)
     for r in range(P):
         assert same_bits(xs[r].cpu().numpy(), ref[r])
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("algo", [1, 2])
+@pytest.mark.parametrize("n", [7, 4099, 100_003])
+def test_sgd_ar_round_bit_exact(P, algo, n):
+    """K7 mode 2 (SGD-AR, optimizer.py:214-242): one pass = ring-order mean of every
+    rank's gradient slot + the momentum/Nesterov/wd step with it, bit-exact against the
+    oracle's SGD-AR loop; the next-snapshot buffers are not written."""
+    rng = np.random.default_rng(P * 7 + n % 13 + algo)
+    steps = 3
+    x0 = rng.standard_normal(n).astype(np.float32)
+    grads = rng.standard_normal((steps, P, n)).astype(np.float32)
+    xs = [dev(x0.copy()) for _ in range(P)]
+    ms = [torch.zeros(n, device="cuda") for _ in range(P)]
+    xbars = [torch.zeros(n, device="cuda") for _ in range(P)]
+    untouched = [torch.full((n,), 7.0, device="cuda") for _ in range(P)]
+    etas = [0.1, 0.05, 0.2]
+    for t in range(steps):
+        slots = [dev(grads[t, r]) for r in range(P)]
+        K.fused_round_virtual(xs, xs, slots, untouched, etas[t], ms=ms, xbars=xbars, momentum=0.9, weight_decay=1e-4,
+                              nesterov=True, first_step=(t == 0), mode=2, algo=algo, nblocks=7)
+    torch.cuda.synchronize()
+    ref, _ = O.run_sgd_ar(x0, grads, etas, P, sgd=O.SgdConfig(1.0, 0.9, 0.0, 1e-4, True))
+    for r in range(P):
+        assert same_bits(xs[r].cpu().numpy(), ref), (P, algo, n, r)
+        assert bool((untouched[r] == 7.0).all())
+
+
+def test_sgd_ar_round_rejects_bad_arguments():
+    x = torch.zeros(64, device="cuda")
+    with pytest.raises(ValueError):  # needs peers
+        K.fused_round_virtual([x], [x], [x], [x], 0.1, mode=2)
+    with pytest.raises(ValueError):  # no delta bookkeeping in SGD-AR
+        K.fused_round_virtual([x, x.clone()], [x, x], [x, x], [x, x], 0.1, deltas=[x, x], mode=2)
