@@ -178,7 +178,10 @@ int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, u
  * peer; the next snapshot's chunks are pushed to their owners; the first push round
  * after any other use of the slots adds one staging launch); AUTO = see
  * lasgd_comm_resolve_fused_algo.  A launch like lasgd_comm_allreduce (same
- * sequence numbers, query / wait / stream_wait apply). */
+ * sequence numbers, query / wait / stream_wait apply).  The rounds own the snapshot
+ * slots: a caller that writes a slot between rounds must call
+ * lasgd_comm_invalidate_staging first (consecutive rounds enter on the previous round's
+ * end-of-round signals, which only certify what the rounds themselves wrote). */
 int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, void* x, const void* g, void* m, void* delta,
                            const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                            unsigned long long* nonfinite, void* stream, unsigned long long* seq);

@@ -406,6 +406,12 @@ class P2PCommunicator:
     def set_trace(self, on: bool) -> None:
         N.check(N.lib().lasgd_comm_set_trace(self._h, int(bool(on))))
 
+    def invalidate_staging(self) -> None:
+        """Call after writing a snapshot slot outside the fused rounds (e.g. loading a
+        checkpoint into it): the next round re-stages / re-enters through the per-CTA
+        barrier instead of trusting the previous round's end-of-round signals."""
+        N.check(N.lib().lasgd_comm_invalidate_staging(self._h))
+
     def set_gate(self, on: bool) -> None:
         """Gate every all-reduce behind a one-warp wait for all peers (collective setting)."""
         N.check(N.lib().lasgd_comm_set_gate(self._h, int(bool(on))))
