@@ -9,6 +9,7 @@
 // All GPUs run the same variant at once (all-to-all traffic).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mix_probe tools/mix_probe.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x)                                                                   \
@@ -63,14 +64,16 @@ __global__ void __launch_bounds__(256) k_mixed(Args a) {
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   int P = 0;
   cudaGetDeviceCount(&P);
   if (P < 2) {
     printf("need >= 2 GPUs\n");
     return 0;
   }
-  const size_t push_bytes = 51ull << 20, hbm_bytes = 146ull << 20;
+  // defaults: the P = 4 staged push round; argv: push source MB, MB per local stream
+  const size_t push_bytes = (argc > 1 ? (size_t)atoi(argv[1]) : 51ull) << 20;
+  const size_t hbm_bytes = (argc > 2 ? (size_t)atoi(argv[2]) : 146ull) << 20;
   Args args[8];
   cudaStream_t s0[8], s1[8];
   cudaEvent_t e0[8], e1[8];
