@@ -11,8 +11,9 @@ ids — and builds the trace:
 
     round, time_s, node_tau_0..P-1, loss, eta, grad_evals, bytes_sent
 
-* ``time_s``: device time since the start event, max over ranks (measured, not
-  simulated: the reference SPEC's ``sim_time_s`` column);
+* ``time_s``: device time since the start event by which every rank that closed the
+  round had closed it (max over ranks, non-decreasing; measured, not simulated: the
+  reference SPEC's ``sim_time_s`` column);
 * ``loss``: mean over ranks of the minibatch training loss at each rank's closing
   step (free: the forward pass computed it);
 * ``grad_evals``: cumulative local steps over all ranks at their k-th close;
@@ -105,6 +106,7 @@ class RunTrace:
     def rows(self) -> List[dict]:
         rows = []
         last_clock = [0] * self.P  # a rank that closed fewer rounds keeps its last count
+        t_done = 0.0  # round k is complete no earlier than round k-1 (ranks drop out at the end)
         for k in range(self.rounds):
             recs = [rs[k] if k < len(rs) else None for rs in self.per_rank]
             present = [r for r in recs if r is not None]
@@ -112,9 +114,10 @@ class RunTrace:
             for i, r in enumerate(recs):
                 if r is not None:
                     last_clock[i] = r.local_clock
+            t_done = max(t_done, max(r.time_s for r in present))
             rows.append({
                 "round": k + 1,
-                "time_s": max(r.time_s for r in present),
+                "time_s": t_done,
                 "node_tau": [r.tau if r is not None else None for r in recs],
                 "loss": sum(losses) / len(losses) if losses else None,
                 "eta": present[0].eta,
@@ -124,7 +127,12 @@ class RunTrace:
         return rows
 
     def validate(self) -> None:
-        """RunTrace invariants: rounds strictly increasing, cumulative counters nondecreasing."""
+        """RunTrace invariants: rounds strictly increasing, cumulative counters nondecreasing
+        (per rank in the raw records, and in the merged rows)."""
+        for i, recs in enumerate(self.per_rank):
+            for a, b in zip(recs, recs[1:]):
+                if b.time_s < a.time_s or b.local_clock <= a.local_clock:
+                    raise ValueError(f"rank {i}: time / local clock decreased at round {b.round}")
         prev = None
         for row in self.rows():
             if prev is not None:
