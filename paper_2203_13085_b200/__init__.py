@@ -29,6 +29,9 @@ from .engine import LASGDWorker, SGDARWorker  # noqa: E402
 from .graphs import GraphedStep  # noqa: E402
 from .flat import FlatParams  # noqa: E402
 from .optimizer import (  # noqa: E402
+    easgd_round_robin_exchange,
+    elastic_center_step,
+    elastic_local_step,
     HyperParamError,
     HyperParams,
     ModelDivergenceError,
@@ -40,13 +43,14 @@ from .optimizer import (  # noqa: E402
     sgd_local_step,
     sync_allreduce_sgd_round,
 )
-from .params import ChunkSpec, as_device_vector, blend, partition_chunks, require_same_dim  # noqa: E402
+from .params import ChunkSpec, as_device_vector, blend, mean_of_vectors, partition_chunks, require_same_dim  # noqa: E402
 from .problems import LrSchedule, lr_at  # noqa: E402
 
 __all__ = [
     "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
     "DimensionMismatchError", "FlatParams", "GraphedStep", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "ModelDivergenceError",
     "NodeState", "NonFiniteError", "P2PCommunicator", "SGDARWorker", "SgdConfig", "Status", "TickAction", "TransportFault",
-    "all_reduce_average", "as_device_vector", "blend", "bytes_per_node", "lasgd_finalize_round", "lasgd_node_tick",
+    "all_reduce_average", "as_device_vector", "blend", "bytes_per_node", "easgd_round_robin_exchange",
+    "elastic_center_step", "elastic_local_step", "mean_of_vectors", "lasgd_finalize_round", "lasgd_node_tick",
     "lr_at", "partition_chunks", "poll", "require_same_dim", "ring_schedule", "sgd_local_step", "sync_allreduce_sgd_round",
 ]

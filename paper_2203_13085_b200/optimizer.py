@@ -34,7 +34,7 @@ import torch
 from . import kernels as K
 from ._native import NonFiniteError
 from .collective import CollectiveHandle
-from .params import as_device_vector
+from .params import as_device_vector, blend, mean_of_vectors, require_same_dim, vector_dtype
 from .problems import LrSchedule, lr_at
 
 
@@ -266,6 +266,46 @@ def lasgd_finalize_round(state: NodeState, z, num_nodes: int,
 
 class ModelDivergenceError(RuntimeError):
     """optimizer.py:210-211: synchronous replicas stopped being bit-identical."""
+
+
+def elastic_local_step(x, z, g, eta: float, alpha: float) -> torch.Tensor:
+    """optimizer.py:113-122: ``alpha*z + (1-alpha)*x - eta*g`` as two K0 blends, in the
+    reference's order (new device vector)."""
+    if not 0.0 <= alpha <= 1.0:
+        raise HyperParamError(f"alpha must be in [0, 1], got {alpha}")
+    if eta <= 0:
+        raise HyperParamError(f"eta must be positive, got {eta}")
+    dt = vector_dtype(x)
+    x, z, g = (as_device_vector(v, dtype=dt) for v in (x, z, g))
+    pulled = blend(alpha, z, 1.0 - alpha, x)
+    return blend(1.0, pulled, -eta, g, out=pulled)
+
+
+def elastic_center_step(z, xs, beta: float) -> torch.Tensor:
+    """optimizer.py:125-133: ``(1-beta)*z + beta*mean(xs)`` (ascending-order mean)."""
+    xs = list(xs)
+    if not xs:
+        raise ValueError("need at least one local model")
+    if not 0.0 <= beta <= 1.0:
+        raise HyperParamError(f"beta must be in [0, 1], got {beta}")
+    dt = vector_dtype(z)
+    z = as_device_vector(z, dtype=dt)
+    xs = [as_device_vector(v, dtype=dt) for v in xs]
+    for v in xs:
+        require_same_dim(z, v)
+    return blend(1.0 - beta, z, beta, mean_of_vectors(xs))
+
+
+def easgd_round_robin_exchange(x, z, alpha: float):
+    """optimizer.py:245-259: symmetric elastic pull between one node and the center,
+    ``x' = x - alpha*(x - z)``, ``z' = z + alpha*(x - z)`` (three K0 blends)."""
+    if not 0.0 < alpha < 1.0:
+        raise HyperParamError(f"round-robin exchange needs 0 < alpha < 1, got {alpha}")
+    dt = vector_dtype(x)
+    x, z = as_device_vector(x, dtype=dt), as_device_vector(z, dtype=dt)
+    require_same_dim(x, z)
+    diff = blend(1.0, x, -1.0, z)
+    return blend(1.0, x, -alpha, diff), blend(1.0, z, alpha, diff)
 
 
 def sync_allreduce_sgd_round(states, grads, eta: float, transport=None, round_id: int = 0) -> torch.Tensor:

@@ -44,6 +44,14 @@ def as_device_vector(v, dtype: torch.dtype = torch.float32, device=None) -> torc
     return t
 
 
+def vector_dtype(v) -> torch.dtype:
+    """The element type a vector argument computes in: f64 for f64 inputs (e.g. the
+    reference's ParamVector, bit-exact with it), f32 otherwise."""
+    if isinstance(v, torch.Tensor):
+        return torch.float64 if v.dtype == torch.float64 else torch.float32
+    return torch.float64 if np.asarray(getattr(v, "data", v)).dtype == np.float64 else torch.float32
+
+
 def require_same_dim(u: torch.Tensor, v: torch.Tensor) -> None:
     """params.py:75-77."""
     if u.numel() != v.numel():
@@ -112,3 +120,22 @@ def partition_chunks(d: int, num_chunks: int) -> ChunkSpec:
     arr = (ctypes.c_size_t * (num_chunks + 1))()
     N.check(N.lib().lasgd_partition_chunks(d, num_chunks, arr), "partition_chunks")
     return ChunkSpec(num_chunks=num_chunks, bounds=tuple((int(arr[i]), int(arr[i + 1])) for i in range(num_chunks)))
+
+
+def mean_of_vectors(vectors) -> torch.Tensor:
+    """params.py:150-158: the mean in fixed ascending-index order (``acc += v`` then
+    ``acc / len``) — NOT the ring order of the all-reduce.  Sums with the K0 blend
+    (``1*acc + 1*v`` is exact in the rounding contract); the division is a true
+    division by a device scalar tensor (a Python-scalar divisor would be turned into a
+    reciprocal multiply)."""
+    vectors = list(vectors)
+    if not vectors:
+        raise ValueError("need at least one vector")
+    dt = vector_dtype(vectors[0])
+    vs = [as_device_vector(v, dtype=dt) for v in vectors]
+    acc = vs[0].clone()
+    for v in vs[1:]:
+        require_same_dim(vs[0], v)
+        blend(1.0, acc, 1.0, v, out=acc)
+    return acc / torch.tensor(float(len(vs)), dtype=acc.dtype, device=acc.device)
+

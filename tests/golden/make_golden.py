@@ -281,9 +281,39 @@ def main_sgd_ar():
     print("sgd_ar fixture written")
 
 
+def gen_easgd(n=1003, seed=41):
+    """elastic_local_step / elastic_center_step / easgd_round_robin_exchange
+    (optimizer.py:113-133, 245-259) and mean_of_vectors (params.py:150-158), reference."""
+    rng = np.random.default_rng(seed)
+    x, z, g = (rng.standard_normal(n) for _ in range(3))
+    xs = rng.standard_normal((5, n))
+    out = {"x": x, "z": z, "g": g, "xs": xs}
+    for i, (eta, alpha) in enumerate([(0.1, 0.5), (0.03, 0.0), (0.2, 1.0), (0.07, 0.3)]):
+        out[f"els_{i}"] = O.elastic_local_step(PR.ParamVector(x), PR.ParamVector(z), PR.ParamVector(g), eta, alpha).data
+        out[f"els_{i}_args"] = np.array([eta, alpha])
+    for i, beta in enumerate([0.0, 0.25, 0.9, 1.0]):
+        out[f"ecs_{i}"] = O.elastic_center_step(PR.ParamVector(z), [PR.ParamVector(v) for v in xs[: 2 + i]], beta).data
+        out[f"ecs_{i}_args"] = np.array([beta, 2 + i])
+    for i, alpha in enumerate([0.1, 0.5, 0.9]):
+        nx, nz = O.easgd_round_robin_exchange(PR.ParamVector(x), PR.ParamVector(z), alpha)
+        out[f"rr_{i}_x"], out[f"rr_{i}_z"] = nx.data, nz.data
+        out[f"rr_{i}_args"] = np.array([alpha])
+    for k in (1, 2, 3, 5):
+        out[f"mean_{k}"] = PR.mean_of_vectors([PR.ParamVector(v) for v in xs[:k]]).data
+    return out
+
+
+def main_easgd():
+    np.savez_compressed(os.path.join(HERE, "easgd.npz"), **gen_easgd())
+    print("easgd fixture written")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "sgd_ar":
         main_sgd_ar()
+    elif len(sys.argv) > 1 and sys.argv[1] == "easgd":
+        main_easgd()
     else:
         main()
         main_sgd_ar()
+        main_easgd()

@@ -198,3 +198,23 @@ def test_config1_trajectory_f32_within_1e4(golden_config1, alpha):
     losses, _ = _config1_oracle(np.float32, alpha)
     rel = np.abs(losses - golden_config1[tag + "losses"]) / np.abs(golden_config1[tag + "losses"])
     assert rel.max() < 1e-4, rel.max()
+
+
+def test_easgd_templates_bit_exact_f64():
+    """elastic_local_step / elastic_center_step / easgd_round_robin_exchange /
+    mean_of_vectors restated in the oracle vs the reference (tests/golden/easgd.npz)."""
+    import os
+
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "easgd.npz")))
+    x, z, gr, xs = g["x"], g["z"], g["g"], g["xs"]
+    for i in range(4):
+        eta, alpha = g[f"els_{i}_args"]
+        assert np.array_equal(O.elastic_local_step(x, z, gr, float(eta), float(alpha)), g[f"els_{i}"]), i
+    for i in range(4):
+        beta, k = g[f"ecs_{i}_args"]
+        assert np.array_equal(O.elastic_center_step(z, list(xs[: int(k)]), float(beta)), g[f"ecs_{i}"]), i
+    for i in range(3):
+        nx, nz = O.easgd_round_robin_exchange(x, z, float(g[f"rr_{i}_args"][0]))
+        assert np.array_equal(nx, g[f"rr_{i}_x"]) and np.array_equal(nz, g[f"rr_{i}_z"]), i
+    for k in (1, 2, 3, 5):
+        assert np.array_equal(O.naive_mean(list(xs[:k])), g[f"mean_{k}"]), k
