@@ -15,6 +15,7 @@ _native.lib()  # fail loudly at import time when the CUDA library is absent
 
 from ._native import CollectiveFailure, DimensionMismatchError, NonFiniteError, TransportFault  # noqa: E402
 from .collective import (  # noqa: E402
+    AllReduceOutcome,
     CollectiveHandle,
     CudaLoopbackTransport,
     CudaP2PTransport,
@@ -22,6 +23,7 @@ from .collective import (  # noqa: E402
     Status,
     all_reduce_average,
     bytes_per_node,
+    execute_allreduce,
     poll,
     ring_schedule,
 )
@@ -50,7 +52,7 @@ __all__ = [
     "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
     "DimensionMismatchError", "FlatParams", "GraphedStep", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "ModelDivergenceError",
     "NodeState", "NonFiniteError", "P2PCommunicator", "SGDARWorker", "SgdConfig", "Status", "TickAction", "TransportFault",
-    "all_reduce_average", "as_device_vector", "blend", "bytes_per_node", "easgd_round_robin_exchange",
+    "AllReduceOutcome", "all_reduce_average", "as_device_vector", "execute_allreduce", "blend", "bytes_per_node", "easgd_round_robin_exchange",
     "elastic_center_step", "elastic_local_step", "mean_of_vectors", "lasgd_finalize_round", "lasgd_node_tick",
     "lr_at", "partition_chunks", "poll", "require_same_dim", "ring_schedule", "sgd_local_step", "sync_allreduce_sgd_round",
 ]

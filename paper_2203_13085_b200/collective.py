@@ -32,7 +32,7 @@ import torch
 from . import _native as N
 from . import kernels as K
 from ._native import CollectiveFailure, DimensionMismatchError, TransportFault  # noqa: F401 (collective.py:22-27)
-from .params import as_device_vector, partition_chunks
+from .params import ChunkSpec, as_device_vector, partition_chunks
 
 
 # ---------------------------------------------------------------- ring plan (host replica)
@@ -250,6 +250,67 @@ class CudaLoopbackTransport:
         del self._pending[round_id]
         del self._handles[round_id]
         self._done.add(round_id)
+
+
+@dataclass
+class AllReduceOutcome:
+    """collective.py:147-151."""
+
+    per_rank: list  # mean vector per rank (device tensors), bit-identical
+    bytes_sent: list  # exact bytes each rank's ring schedule transmits
+    peak_step_bytes: int  # largest single-step payload any rank sends
+
+
+def execute_allreduce(vectors, chunks: Optional[ChunkSpec] = None, schedule: Optional[RingSchedule] = None,
+                      on_step=None) -> AllReduceOutcome:
+    """collective.py:154-203 on the device: the ring-order mean of P contributions held
+    on one GPU, computed by the one-shot mean kernel (K2 over virtual ranks), which
+    writes the P bit-identical per-rank results in one launch.
+
+    Byte accounting is the exact replay of the ring schedule (``bytes_sent``,
+    ``peak_step_bytes``).  ``on_step(step_index, step_bytes)`` is called for every step
+    with the reference's payload sizes, in step order, BEFORE the kernel runs: a
+    ``TransportFault`` raised there aborts the collective with no result, as in the
+    reference.  f64 inputs compute in f64 (bit-exact with the reference), others in
+    f32.  Only the default partition and schedule are supported (the kernels implement
+    exactly that order); anything else raises ``NotImplementedError``."""
+    from .params import vector_dtype
+
+    vectors = list(vectors)
+    P = len(vectors)
+    if P == 0:
+        raise ValueError("need at least one contribution")
+    dt = vector_dtype(vectors[0])
+    vs = [as_device_vector(v, dtype=dt) for v in vectors]
+    d = vs[0].numel()
+    for v in vs:
+        if v.numel() != d:
+            raise DimensionMismatchError(f"contribution dims differ: {v.numel()} vs {d}")
+    if P == 1:
+        return AllReduceOutcome(per_rank=[vs[0]], bytes_sent=[0], peak_step_bytes=0)
+    default_chunks = partition_chunks(d, P)
+    if chunks is not None and tuple(map(tuple, chunks.bounds)) != tuple(map(tuple, default_chunks.bounds)):
+        raise NotImplementedError("the device ring mean implements the default partition_chunks(d, P) only")
+    if schedule is not None and schedule != ring_schedule(P):
+        raise NotImplementedError("the device ring mean implements the default ring_schedule(P) only")
+    bpe = vs[0].element_size()
+    sizes = [default_chunks.size(c) * bpe for c in range(P)]
+    peak = 0
+    for step_index, step in enumerate(ring_schedule(P).steps):
+        step_bytes = [0] * P
+        for entry in step:  # rank entry.recv_from sends chunk entry.recv_chunk
+            step_bytes[entry.recv_from] = sizes[entry.recv_chunk]
+        peak = max(peak, max(step_bytes))
+        if on_step is not None:
+            on_step(step_index, step_bytes)
+    outs = [torch.empty_like(vs[0]) for _ in range(P)]
+    nf = torch.zeros(1, dtype=torch.int64, device=vs[0].device)
+    K.mean_virtual(outs, vs, algo=N.ALGO_ONESHOT, nonfinite=nf)
+    bad = int(nf.item())
+    if bad:
+        raise N.NonFiniteError(f"all-reduce result: {bad} non-finite entries out of {d * P}")
+    return AllReduceOutcome(per_rank=outs, bytes_sent=[bytes_per_node(d, P, bpe, r) for r in range(P)],
+                            peak_step_bytes=peak)
 
 
 def all_reduce_average(contributions, transport=None, round_id: int = 0) -> CollectiveHandle:

@@ -68,3 +68,37 @@ def test_f32_bit_exact_vs_oracle_and_errors():
         L.elastic_center_step(dz, [], 0.5)
     with pytest.raises(L.DimensionMismatchError):
         L.easgd_round_robin_exchange(dx, dz[:100], 0.5)
+
+
+def test_execute_allreduce_matches_reference(golden_prims):
+    """collective.py:154-203 on the device: per-rank means bit-exact (f64) against the
+    reference's outputs, exact byte accounting, on_step abort, default plan only."""
+    import paper_2203_13085_b200 as L
+
+    for P in range(1, 9):
+        for d in (1, 5, 7, 1000, 1001, 4099):
+            vecs = list(golden_prims[f"mean_in_{P}_{d}"])
+            out = L.execute_allreduce(vecs)
+            ref = golden_prims[f"mean_out_{P}_{d}"]
+            assert len(out.per_rank) == P
+            for r in range(P):
+                assert np.array_equal(out.per_rank[r].cpu().numpy(), ref if P > 1 else vecs[0]), (P, d, r)
+            assert out.bytes_sent == ([O.bytes_per_node(d, P, 8, r) for r in range(P)] if P > 1 else [0])
+            sizes = [e - s for s, e in O.partition_chunks(d, P)]
+            assert out.peak_step_bytes == (8 * max(sizes) if P > 1 else 0)
+    vecs = list(golden_prims["mean_in_4_1001"])
+    seen = []
+
+    def on_step(i, step_bytes):
+        seen.append((i, list(step_bytes)))
+        if i == 2:
+            raise L.TransportFault("injected at step 2")
+
+    with pytest.raises(L.TransportFault):
+        L.execute_allreduce(vecs, on_step=on_step)
+    assert [i for i, _ in seen] == [0, 1, 2] and all(len(b) == 4 for _, b in seen)
+    custom = L.ChunkSpec(4, ((0, 500), (500, 600), (600, 700), (700, 1001)))
+    with pytest.raises(NotImplementedError):
+        L.execute_allreduce(vecs, chunks=custom)
+    with pytest.raises(L.DimensionMismatchError):
+        L.execute_allreduce([vecs[0], vecs[1][:10]])
