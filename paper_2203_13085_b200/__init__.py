@@ -20,6 +20,8 @@ from .collective import (  # noqa: E402
     CudaLoopbackTransport,
     CudaP2PTransport,
     P2PCommunicator,
+    RingSchedule,
+    RingStep,
     Status,
     all_reduce_average,
     bytes_per_node,
@@ -51,7 +53,7 @@ from .problems import LrSchedule, lr_at  # noqa: E402
 __all__ = [
     "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
     "DimensionMismatchError", "FlatParams", "GraphedStep", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "ModelDivergenceError",
-    "NodeState", "NonFiniteError", "P2PCommunicator", "SGDARWorker", "SgdConfig", "Status", "TickAction", "TransportFault",
+    "NodeState", "NonFiniteError", "P2PCommunicator", "RingSchedule", "RingStep", "SGDARWorker", "SgdConfig", "Status", "TickAction", "TransportFault",
     "AllReduceOutcome", "all_reduce_average", "as_device_vector", "execute_allreduce", "blend", "bytes_per_node", "easgd_round_robin_exchange",
     "elastic_center_step", "elastic_local_step", "mean_of_vectors", "lasgd_finalize_round", "lasgd_node_tick",
     "lr_at", "partition_chunks", "poll", "require_same_dim", "ring_schedule", "sgd_local_step", "sync_allreduce_sgd_round",
