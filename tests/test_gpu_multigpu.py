@@ -298,6 +298,44 @@ def _w_fault(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_adaptive_laggard(rank, world, port):
+    """Adaptive schedule with the last rank much slower: the fast ranks take up to
+    tau_max local steps per round while the laggard closes its rounds early (peers
+    already ahead), i.e. the dynamic rate of the paper's Table 3.  Measured on B200:
+    mean tau 3.8 on the fast ranks, 2.4 on the laggard (P=2 and P=4)."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+
+    _init(rank, world, port)
+    n = 100_003
+    comm = L.P2PCommunicator(n, nblocks=16, timeout_s=30.0)
+    x = torch.randn(n, device="cuda")
+    g = torch.randn(n, device="cuda") * 1e-3
+    w = L.LASGDWorker(x, g, comm=comm, sync_period=4, lr=0.01, mode="pull", adaptive=True, tau_max=4)
+    for _ in range(40):
+        if rank == world - 1:
+            torch.cuda._sleep(3_000_000)  # ~1.5 ms per step on the laggard
+        w.step()
+    w.drain()
+    torch.cuda.synchronize()
+    hist = dict(w.tau_hist)
+    mean_tau = sum(k * v for k, v in hist.items()) / max(1, sum(hist.values()))
+    allm = [None] * world
+    dist.all_gather_object(allm, mean_tau)
+    assert np.isfinite(x.cpu().numpy()).all()
+    if rank == 0:
+        # fast ranks run ahead (several local steps per round); the laggard closes as soon
+        # as it sees its peers ahead, which its host learns at most max_host_lead (2)
+        # steps late, so its rounds last at most ~1 + 2 steps
+        assert all(m >= allm[world - 1] + 1.0 for m in allm[:-1]), allm
+        assert allm[world - 1] <= 3.0, allm
+    dist.barrier()
+    w.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def _w_fault_end_signal(rank, world, port):
     """A rank that never raises its end-of-round signal (fault phase 2) in a fused push /
     mirror round: the next round's entry wait trips the watchdog and every rank's worker
@@ -356,6 +394,11 @@ def test_fused_auto_full_resnet50_size_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_fused_rounds_ragged_sizes_bit_exact():
     _spawn(_w_ragged)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_adaptive_fast_ranks_run_ahead_of_a_laggard():
+    _spawn(_w_adaptive_laggard)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
