@@ -7,12 +7,16 @@
 //   stream waits for the previous launch (event), applies K4 (pull or reference
 //   finalize, writing the next snapshot slot) and hands the snapshot to the side
 //   stream, where K2/K3 runs while the next minibatches proceed.
-// pipeline FUSED (deterministic only): the boundary step is one K7 launch (local step
-//   + NVLink mean + pull + next snapshot); other steps are K5.
+// pipeline FUSED (deterministic only): the boundary step is one fused launch (local
+//   step + NVLink mean + pull + next snapshot: K7, or the K8 push round — mirror form at
+//   P = 2, staged form at P >= 3 — as lasgd_comm_resolve_fused_algo picks); other steps
+//   are K5.
 // adaptive: a round closes as soon as the host-mapped completion flag of the
-//   in-flight launch is set, or when tau_max local steps have been taken (then the
-//   compute stream waits on the event; the host never blocks except for the optional
-//   run-ahead throttle that bounds how far the host's view runs ahead of the GPU).
+//   in-flight launch is set, when the peers are already ahead (this rank is the
+//   round's laggard, lasgd_comm_peers_ahead), or when tau_max local steps have been
+//   taken (then the compute stream waits on the event; the host never blocks except
+//   for the bounded run-ahead throttle).  Side-stream all-reduces are gated (k_gate)
+//   so they do not hold SMs while a late peer catches up.
 #include <string.h>
 #include <time.h>
 

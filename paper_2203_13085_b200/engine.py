@@ -14,14 +14,16 @@ that step, so the host keeps well ahead of the GPU.
   stream (low priority, bounded CTA budget), where the NVLink P2P mean
   all-reduce (K2/K3 with K6 flags) overlaps the next minibatches;
 * ``pipeline="fused"`` (deterministic only): the boundary step is ONE kernel
-  (K7) that applies the local step, reads every peer's snapshot over NVLink,
-  forms the ring-order mean, pulls and writes the next snapshot — bit-identical
-  results, HBM and NVLink streamed concurrently.
+  that applies the local step, forms the ring-order mean of every rank's snapshot,
+  pulls and writes the next snapshot — K7 (peers' snapshots read over NVLink) or the
+  K8 push round (data moved by remote stores: the peer's snapshot mirrored at P=2,
+  staged chunks at P>=3); bit-identical results, HBM and NVLink streamed concurrently.
 
 Round boundaries are deterministic (exactly ``sync_period`` local steps per
 round — the parity schedule) or adaptive (finalize as soon as the host-mapped
-completion flag says the mean landed, or make the compute stream wait when
-``tau_max`` steps have been taken — the paper's dynamic rate, Table 3).
+completion flag says the mean landed or the peers are already ahead, or make the
+compute stream wait when ``tau_max`` steps have been taken — the paper's dynamic
+rate, Table 3).
 """
 
 from __future__ import annotations
