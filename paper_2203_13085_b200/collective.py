@@ -414,9 +414,11 @@ class P2PCommunicator:
                     momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False, first_step=False,
                     delta_reset=False, alpha: float = 1.0, mode: int = 0, algo: int = N.ALGO_AUTO, nblocks: int = 0,
                     nonfinite=None, stream=None) -> int:
-        """K7: local step + mean of snapshot slot ``slot`` over all ranks (NVLink) + pull
-        (mode 0) / finalize (mode 1) + write snapshot slot ``1 - slot``, one launch on
-        ``stream`` (default: the current stream)."""
+        """One fused round on ``stream`` (default: the current stream): local step + mean of
+        snapshot slot ``slot`` over all ranks (NVLink) + pull (mode 0) / finalize (mode 1)
+        + write snapshot slot ``1 - slot`` — K7, or the K8 push round for ``ALGO_PUSH``
+        (what AUTO picks for large buffers).  Mode 2 = one SGD-AR round: the slots hold
+        gradients and x takes the local step with their mean (K7 one-/two-shot only)."""
         K._check(x, g, m, delta, self.snapshots[0])
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         p = K.sgd_params(lr, momentum, dampening, weight_decay, nesterov, first_step, delta_reset)

@@ -393,6 +393,7 @@ extern "C" int lasgd_fused_push_virtual(int P, void* const* x, const void* const
   if (!x || !g || !snaps || !snap_next || !xbars || !stages) return fail(LASGD_ERR_INVALID_ARGUMENT, "null pointer array");
   if (dtype != LASGD_F32 && dtype != LASGD_F64) return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
   if (cur != 0 && cur != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "parity %d", cur);
+  if (mode == 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "no push form of the SGD-AR round");
   int rc = check_fused_args(P, x, g, m, delta, snap_next, sgd, alpha, mode);
   if (rc) return rc;
   if (n == 0) return LASGD_OK;

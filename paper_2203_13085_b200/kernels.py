@@ -107,7 +107,9 @@ def fused_round_virtual(xs, gs, snaps, snap_nexts, lr: float, *, ms=None, deltas
                         nonfinite=None, stream=None) -> None:
     """K7 for P ranks on one device: local step + ring-order mean of ``snaps`` + pull
     (mode 0) or finalize (mode 1) + next snapshot, one pass (two launches for the
-    two-shot form, which needs per-rank ``xbars`` scratch)."""
+    two-shot form, which needs per-rank ``xbars`` scratch).  Mode 2 (SGD-AR): ``snaps``
+    hold the gradients, x = local step with their mean; ``gs`` unused, nothing else
+    written."""
     P = len(xs)
     flat = list(xs) + list(gs) + list(snaps) + list(snap_nexts) + list(ms or []) + list(deltas or []) + list(xbars or [])
     code, n = _check(*flat)

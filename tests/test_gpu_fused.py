@@ -204,3 +204,6 @@ def test_sgd_ar_round_rejects_bad_arguments():
         K.fused_round_virtual([x], [x], [x], [x], 0.1, mode=2)
     with pytest.raises(ValueError):  # no delta bookkeeping in SGD-AR
         K.fused_round_virtual([x, x.clone()], [x, x], [x, x], [x, x], 0.1, deltas=[x, x], mode=2)
+    st = [torch.zeros(2 * 2 * K.push_stage_elems(64, 2), device="cuda") for _ in range(2)]
+    with pytest.raises(ValueError):  # no push form of the SGD-AR round
+        K.fused_push_virtual([x, x.clone()], [x, x], [x, x], [x, x], [x, x], st, 0, True, 0.1, mode=2)
