@@ -88,12 +88,16 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
     if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
     trace_mark(a, b, 1);
     if (ok) {
-      const T* src[P];
-#pragma unroll
-      for (int q = 0; q < P; ++q) src[q] = q == rank ? snap_own : stage_ptr<T>(a, rank, cur, q, P);
       size_t cs, ce, cp0, cp1;
       chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
       const size_t base = cs / W * W;  // staging offset origin of the own chunk
+      // contribution of rank q to the own chunk: the own snapshot, or q's staged copy
+      // (addresses computed per use: P pointers would cost 2P registers at large P)
+      const T* const stage0 = stage_ptr<T>(a, rank, cur, 0, P);
+      const size_t selems = a.stage_elems;
+      auto src = [&](int q, size_t j) -> const T* {
+        return q == rank ? snap_own + j : stage0 + (size_t)q * selems + (j - base);
+      };
       tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
         for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
           Pack<T> v[U][P], vx[U], vg[U], vm[U], vd[U];
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
             if (pu < p1) {
               const size_t j = pu * W;
 #pragma unroll
-              for (int q = 0; q < P; ++q) v[u][q] = ld_stream(src[q] + (q == rank ? j : j - base));
+              for (int q = 0; q < P; ++q) v[u][q] = ld_stream(src(q, j));
               vx[u] = ld_stream(x + j);
               vg[u] = ld_stream(g + j);
               if (load_m) vm[u] = ld_stream(m + j);
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
         auto scalar = [&](size_t j) {
           T lane[P];
 #pragma unroll
-          for (int q = 0; q < P; ++q) lane[q] = src[q][q == rank ? j : j - base];
+          for (int q = 0; q < P; ++q) lane[q] = *src(q, j);
           const T zb = mean_div<T, P>(rot_sum<T, P>(lane, rank));
 #pragma unroll
           for (int q = 0; q < P; ++q)
