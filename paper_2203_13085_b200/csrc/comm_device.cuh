@@ -113,7 +113,7 @@ __device__ __forceinline__ T mean_div(T s) {
   }
 }
 
-__device__ void report_failure(const CommArgs& a, int code, int peer, int phase, int block, int rank) {
+__device__ inline void report_failure(const CommArgs& a, int code, int peer, int phase, int block, int rank) {
   if (atomicCAS(&a.status[ST_ERR], 0u, (uint32_t)code) == 0u) {
     a.status[ST_PEER] = peer;
     a.status[ST_PHASE] = phase;
@@ -153,7 +153,7 @@ __device__ bool cta_barrier(const CommArgs& a, int phase, int b, int rank) {
 }
 
 // Last CTA of a launch publishes the sequence number to host-mapped memory.
-__device__ void publish_done(const CommArgs& a) {
+__device__ inline void publish_done(const CommArgs& a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();

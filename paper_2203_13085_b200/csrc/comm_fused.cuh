@@ -4,7 +4,7 @@
 #ifndef LASGD_COMM_FUSED_CUH
 #define LASGD_COMM_FUSED_CUH
 
-#include "comm_device.cuh"
+#include "comm_allreduce.cuh"  // chunk_tiles, ordered_sum, tile loops
 
 namespace lasgd {
 
@@ -313,10 +313,6 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
   if (!VIRTUAL) publish_done(a);
 }
 
-// Launch `kernel` normally, or cooperatively (all CTAs co-resident, required by the
-// rank-level barrier of the P2P two-shot kernels).  A cooperative grid is clamped to
-// what fits on the device — every rank computes the same clamp on the same GPU type,
-// so the per-CTA flag slots still line up.
 
 }  // namespace lasgd
 

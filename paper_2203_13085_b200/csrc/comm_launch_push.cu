@@ -1,0 +1,48 @@
+// Dispatch of the push round kernels (K8: mirror form at P = 2, staged form at P >= 3).
+// Separate translation unit: see comm_launch.cuh.
+#include "comm_push.cuh"
+#include "comm_launch.cuh"
+
+namespace lasgd {
+
+template <typename T, bool VIRTUAL>
+int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s) {
+#define LASGD_PCASE(PP)                                                                             \
+  case PP: {                                                                                        \
+    auto kern = k_push_round<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)>;                                    \
+    CommArgs aa = a;                                                                                \
+    if (!VIRTUAL) {                                                                                 \
+      const int cap = coop_capacity(kern, threads);                                                 \
+      if ((int)grid.x > cap) grid.x = cap;                                                          \
+      aa.nblocks = grid.x;                                                                          \
+    }                                                                                               \
+    return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                  \
+  }
+  if (P == 2) {  // mirror form
+    auto kern = k_push_mirror<T, VIRTUAL, 2>;
+    CommArgs aa = a;
+    if (!VIRTUAL) {
+      const int cap = coop_capacity(kern, threads);
+      if ((int)grid.x > cap) grid.x = cap;
+      aa.nblocks = grid.x;
+    }
+    return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);
+  }
+  switch (P) {
+    LASGD_PCASE(3)
+    LASGD_PCASE(4)
+    LASGD_PCASE(5)
+    LASGD_PCASE(6)
+    LASGD_PCASE(7)
+    LASGD_PCASE(8)
+    default: return fail(LASGD_ERR_UNSUPPORTED, "push round needs 2 <= P <= %d, got %d", kMaxR, P);
+  }
+#undef LASGD_PCASE
+}
+
+template int launch_push<float, false>(int, const CommArgs&, const FusedRound<float>&, dim3, int, cudaStream_t);
+template int launch_push<float, true>(int, const CommArgs&, const FusedRound<float>&, dim3, int, cudaStream_t);
+template int launch_push<double, false>(int, const CommArgs&, const FusedRound<double>&, dim3, int, cudaStream_t);
+template int launch_push<double, true>(int, const CommArgs&, const FusedRound<double>&, dim3, int, cudaStream_t);
+
+}  // namespace lasgd

@@ -38,79 +38,10 @@
 #include <mutex>
 #include <utility>
 
-#include "comm_allreduce.cuh"
-#include "comm_device.cuh"
-#include "comm_fused.cuh"
-#include "comm_push.cuh"
+#include "comm_launch.cuh"
 #include "lasgd_common.cuh"
 
 namespace lasgd {
-
-template <typename... Args>
-int launch_kernel(bool coop, void (*kernel)(Args...), dim3 grid, int threads, cudaStream_t s, Args... args) {
-  if (!coop) {
-    kernel<<<grid, threads, 0, s>>>(args...);
-    LASGD_CUDA_TRY(cudaGetLastError());
-    return LASGD_OK;
-  }
-  void* kargs[] = {(void*)&args...};
-  LASGD_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kernel, grid, dim3(threads), kargs, 0, s));
-  return LASGD_OK;
-}
-
-template <typename... Args>
-int coop_capacity(void (*kernel)(Args...), int threads) {
-  // cached per (kernel, threads): an occupancy query per launch costs host time every step
-  static std::mutex mu;
-  static std::map<std::pair<const void*, int>, int> cache;
-  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), threads);
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  const int cap = per_sm * num_sms();
-  std::lock_guard<std::mutex> lk(mu);
-  cache[key] = cap;
-  return cap;
-}
-
-template <typename T, bool VIRTUAL>
-int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s,
-                 int algo = LASGD_ALGO_ONESHOT) {
-  static_assert(sizeof(CommArgs) + sizeof(FusedRound<T>) < 4000, "kernel parameters");
-#define LASGD_FCASE(PP)                                                                             \
-  case PP:                                                                                          \
-    if (algo == LASGD_ALGO_TWOSHOT && PP > 1) {                                                     \
-      auto kern = k_fused_twoshot<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)>;                               \
-      CommArgs aa = a;                                                                              \
-      if (!VIRTUAL) {                                                                               \
-        const int cap = coop_capacity(kern, threads);                                               \
-        if ((int)grid.x > cap) grid.x = cap;                                                        \
-        aa.nblocks = grid.x;                                                                        \
-      }                                                                                             \
-      return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                \
-    }                                                                                               \
-    return launch_kernel(false, k_fused_round<T, PP, VIRTUAL, (PP <= 2 ? 2 : 1)>, grid, threads, s, \
-                         a, f);
-  switch (P) {
-    LASGD_FCASE(1)
-    LASGD_FCASE(2)
-    LASGD_FCASE(3)
-    LASGD_FCASE(4)
-    LASGD_FCASE(5)
-    LASGD_FCASE(6)
-    LASGD_FCASE(7)
-    LASGD_FCASE(8)
-    default: return fail(LASGD_ERR_UNSUPPORTED, "world size %d > %d", P, kMaxR);
-  }
-#undef LASGD_FCASE
-  LASGD_CUDA_TRY(cudaGetLastError());
-  return LASGD_OK;
-}
 
 template <typename T>
 FusedRound<T> make_fused(int nr, void* const* x, const void* const* g, void* const* m, void* const* delta,
@@ -147,79 +78,6 @@ int check_fused_args(int nr, void* const* x, const void* const* g, void* const* 
     if (sgd->momentum != 0.0 && !m[r]) return fail(LASGD_ERR_INVALID_ARGUMENT, "momentum needs m");
   }
   return LASGD_OK;
-}
-
-// ------------------------------------------------------------------ dispatch
-template <int P>
-constexpr int unroll_for() { return P <= 2 ? 8 : (P <= 4 ? 4 : 2); }
-template <int P>
-constexpr int oneshot_unroll() { return P <= 2 ? 4 : (P <= 4 ? 2 : 1); }  // <= 128 regs, no spills
-
-template <typename T, bool VIRTUAL>
-int launch_allreduce(int algo, int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
-#define LASGD_CASE(PP)                                                                                    \
-  case PP:                                                                                                \
-    if (algo == LASGD_ALGO_ONESHOT) return launch_kernel(false, k_oneshot<T, PP, VIRTUAL, oneshot_unroll<PP>()>, \
-                                                         grid, threads, s, a);                            \
-    {                                                                                                     \
-      auto kern = k_twoshot<T, PP, VIRTUAL, unroll_for<PP>(), 8>;                                         \
-      CommArgs aa = a;                                                                                    \
-      if (!VIRTUAL) {                                                                                     \
-        const int cap = coop_capacity(kern, threads);                                                     \
-        if ((int)grid.x > cap) grid.x = cap;                                                              \
-        aa.nblocks = grid.x;                                                                              \
-      }                                                                                                   \
-      return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa);                                         \
-    }
-  switch (P) {
-    LASGD_CASE(1)
-    LASGD_CASE(2)
-    LASGD_CASE(3)
-    LASGD_CASE(4)
-    LASGD_CASE(5)
-    LASGD_CASE(6)
-    LASGD_CASE(7)
-    LASGD_CASE(8)
-    default: return fail(LASGD_ERR_UNSUPPORTED, "world size %d > %d", P, kMaxR);
-  }
-#undef LASGD_CASE
-  LASGD_CUDA_TRY(cudaGetLastError());
-  return LASGD_OK;
-}
-
-template <typename T, bool VIRTUAL>
-int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s) {
-#define LASGD_PCASE(PP)                                                                             \
-  case PP: {                                                                                        \
-    auto kern = k_push_round<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)>;                                    \
-    CommArgs aa = a;                                                                                \
-    if (!VIRTUAL) {                                                                                 \
-      const int cap = coop_capacity(kern, threads);                                                 \
-      if ((int)grid.x > cap) grid.x = cap;                                                          \
-      aa.nblocks = grid.x;                                                                          \
-    }                                                                                               \
-    return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                  \
-  }
-  if (P == 2) {  // mirror form
-    auto kern = k_push_mirror<T, VIRTUAL, 2>;
-    CommArgs aa = a;
-    if (!VIRTUAL) {
-      const int cap = coop_capacity(kern, threads);
-      if ((int)grid.x > cap) grid.x = cap;
-      aa.nblocks = grid.x;
-    }
-    return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);
-  }
-  switch (P) {
-    LASGD_PCASE(3)
-    LASGD_PCASE(4)
-    LASGD_PCASE(5)
-    LASGD_PCASE(6)
-    LASGD_PCASE(7)
-    LASGD_PCASE(8)
-    default: return fail(LASGD_ERR_UNSUPPORTED, "push round needs 2 <= P <= %d, got %d", kMaxR, P);
-  }
-#undef LASGD_PCASE
 }
 
 size_t elem_bytes(int dtype);
