@@ -1,12 +1,15 @@
 // NVLink P2P communicator of the LASGD sync path: the C-ABI entry points, launch
 // dispatch, virtual-rank test paths and the communicator lifecycle (IPC region,
-// signal pad, work queues, host-mapped status).  The kernels live in headers of this
-// one translation unit:
+// signal pad, work queues, host-mapped status).  The kernels live in headers:
 //   comm_device.cuh    CommArgs, system-scope flags, per-CTA / rank-level barriers,
 //                      launch gate (K9), completion word, tile work queues
 //   comm_allreduce.cuh K2 one-shot and K3 two-shot mean all-reduce
-//   comm_fused.cuh     K7 fused round (local step + mean + pull + next snapshot)
+//   comm_fused.cuh     K7 fused round (local step + mean + pull + next snapshot;
+//                      mode 2 = one SGD-AR round)
 //   comm_push.cuh      K8 push round (staged chunks for P >= 3, mirror for P = 2)
+//   comm_launch.cuh    launch helpers and the dispatcher declarations
+// and are instantiated in their own translation units (comm_launch_allreduce.cu,
+// comm_launch_fused.cu, comm_launch_push.cu), compiled in parallel.
 //
 // Replaces collective.py:154-203 (`execute_allreduce`) and the
 // LoopbackTransport round (collective.py:229-287).  The arithmetic reproduces the
