@@ -26,7 +26,6 @@ from dataclasses import dataclass
 from enum import Enum
 from typing import Optional
 
-import numpy as np
 import torch
 
 from . import _native as N

@@ -4,7 +4,6 @@ the LASGDWorker round protocol (double-buffered snapshots, side stream) bit-exac
 against the oracle's deterministic-k loop, and the watchdog turning a missing
 peer flag into CollectiveFailure on every rank.  Skipped with < 2 GPUs."""
 
-import os
 import socket
 
 import numpy as np

@@ -18,7 +18,6 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2203_13085_b200 as L  # noqa: E402
-from paper_2203_13085_b200 import _native as N  # noqa: E402
 
 
 def summarise(tr):
