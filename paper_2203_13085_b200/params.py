@@ -32,7 +32,10 @@ def as_device_vector(v, dtype: torch.dtype = torch.float32, device=None) -> torc
         arr = getattr(v, "data", v)
         if isinstance(arr, memoryview):
             arr = np.asarray(v)
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(arr)))
+        arr = np.asarray(arr)
+        if arr.ndim == 0:  # np.ascontiguousarray would promote a scalar to shape (1,)
+            raise ValueError(f"parameter vector must be 1-D, got shape {arr.shape}")
+        t = torch.from_numpy(np.ascontiguousarray(arr))
     if t.dim() != 1:
         if t.dim() == 0:
             raise ValueError(f"parameter vector must be 1-D, got shape {tuple(t.shape)}")

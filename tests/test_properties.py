@@ -99,3 +99,22 @@ def test_ring_mean_order_property():
         for k in range(1, P):
             acc = acc + vecs[(c + k) % P][s:e]
         assert np.array_equal(got[s:e], acc / np.float32(P))
+
+
+def test_degenerate_inputs_raise_like_the_reference():
+    """params.py:39,55,136-139: zero-dimension vectors and zero chunk counts are
+    ValueErrors; d < num_chunks gives trailing empty ranges at offset d."""
+    import pytest
+    import torch
+
+    from paper_2203_13085_b200.params import as_device_vector
+
+    with pytest.raises(ValueError, match="positive dimension"):
+        as_device_vector(np.zeros(0), device=torch.device("cpu"))
+    with pytest.raises(ValueError, match="1-D"):
+        as_device_vector(np.float64(1.0), device=torch.device("cpu"))
+    with pytest.raises(ValueError, match="d must be positive"):
+        partition_chunks(0, 3)
+    with pytest.raises(ValueError, match="num_chunks must be positive"):
+        partition_chunks(5, 0)
+    assert [tuple(b) for b in partition_chunks(2, 5).bounds] == [(0, 1), (1, 2), (2, 2), (2, 2), (2, 2)]
