@@ -237,6 +237,47 @@ def _w_full_size(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_max_size(rank, world, port):
+    """BASELINE configs[4]'s largest buffer (1 GiB of fp32, ragged: 2^28 + 5 elements)
+    through the fused AUTO round, checked by a size-independent property: contributions
+    are small integers, so every summation order is exact; with zero gradients and
+    α = 1 each rank must end on x + (-1)·(x + (-1)·sum/P) (K4a's rounding order,
+    optimizer.py:113-133), which is sum/P itself when P is a power of two — then a
+    second round must leave it unchanged."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+
+    _init(rank, world, port)
+    n = (1 << 28) + 5
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+
+    def contrib(r):
+        return ((idx * 7 + 13 * r + (idx >> 11)) % 4096).to(torch.float32)
+
+    want = contrib(0)
+    for r in range(1, world):
+        want += contrib(r)
+    want /= world
+    x = contrib(rank)
+    del idx
+    want = x - (x - want)  # separately rounded ops, as the kernel (exact when P is a power of two)
+    rounds = 2 if world & (world - 1) == 0 else 1
+    g = torch.zeros_like(x)
+    comm = L.P2PCommunicator(n, timeout_s=60.0)
+    w = L.LASGDWorker(x, g, comm=comm, sync_period=1, alpha=1.0, sgd=L.SgdConfig(0.0, 0.0, 0.0, False), lr=0.1,
+                      mode="pull", pipeline="fused")
+    for _ in range(rounds):
+        w.step()
+    w.drain()
+    torch.cuda.synchronize()
+    assert torch.equal(x.view(torch.int32), want.view(torch.int32)), (world, rank, rounds)
+    dist.barrier()
+    w.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def _w_ragged(rank, world, port):
     """Fused rounds through the communicator at tiny / ragged n (empty chunks when n < P,
     packs straddling chunk bounds) for every fused algorithm, bit-exact vs the oracle."""
@@ -389,6 +430,11 @@ def test_sgd_ar_worker_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_fused_auto_full_resnet50_size_bit_exact():
     _spawn(_w_full_size)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_fused_auto_1gib_exact_mean():
+    _spawn(_w_max_size)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
