@@ -207,3 +207,36 @@ def test_sgd_ar_round_rejects_bad_arguments():
     st = [torch.zeros(2 * 2 * K.push_stage_elems(64, 2), device="cuda") for _ in range(2)]
     with pytest.raises(ValueError):  # no push form of the SGD-AR round
         K.fused_push_virtual([x, x.clone()], [x, x], [x, x], [x, x], [x, x], st, 0, True, 0.1, mode=2)
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_push_round_1gib_exact_mean(P):
+    """BASELINE configs[4]'s largest buffer (2^28 + 5 fp32 per rank) through K8 over
+    virtual ranks (mirror form at P=2, staged form at P=8), checked by a size-independent
+    property: small-integer contributions make every summation order exact, so with zero
+    gradients and α = 1 every rank holds exactly sum/P (collective.py:200) after the
+    first round, and the second round leaves it unchanged."""
+    n = (1 << 28) + 5
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    xs = [((idx * 7 + 13 * r + (idx >> 11)) % 4096).to(torch.float32) for r in range(P)]
+    del idx
+    want = torch.zeros(n, device="cuda")
+    for x in xs:
+        want += x
+    want /= P
+    zero = torch.zeros(n, device="cuda")
+    snaps = [[x.clone() for x in xs], [torch.empty(n, device="cuda") for _ in range(P)]]
+    xbars = [torch.empty(n, device="cuda") for _ in range(P)]
+    se = K.push_stage_elems(n, P)
+    stages = [torch.empty(2 * P * se, device="cuda") for _ in range(P)]
+    cur = 0
+    for t in range(2):
+        K.fused_push_virtual(xs, [zero] * P, snaps[cur], snaps[1 - cur], xbars, stages, cur, t == 0, 0.1,
+                             alpha=1.0)
+        cur = 1 - cur
+        torch.cuda.synchronize()
+        for r in range(P):
+            assert torch.equal(xs[r].view(torch.int32), want.view(torch.int32)), (P, t, r)
+            assert torch.equal(snaps[cur][r].view(torch.int32), want.view(torch.int32)), (P, t, r)
+    del xs, snaps, xbars, stages
+    torch.cuda.empty_cache()
