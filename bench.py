@@ -106,6 +106,12 @@ class ClockSampler:
                                        "-i", str(gpu), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+            return
+        # nvidia-smi's NVML start-up contends with kernel launches in this process: wait
+        # for its first sample so that start-up stays outside the timed region.
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 10.0 and self.p.poll() is None and os.path.getsize(self.f.name) == 0:
+            time.sleep(0.01)
 
     def stop(self):
         if self.p is None:
@@ -353,8 +359,8 @@ def main():
         run_sync_path(w, args.warmup, lambda t: grads[t % 2])
         w.drain()
     torch.cuda.synchronize()
-    barrier()
     clocks = ClockSampler(local) if rank == 0 else None
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w.reset_records()
     with torch.cuda.stream(compute):
@@ -425,6 +431,7 @@ def main():
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(compute):
         f0.record(compute)
+        copy_stream.wait_event(f0)  # the first H2D starts inside the timed region
         e2e_loop(we, args.steps)
         f1.record(compute)
     torch.cuda.synchronize()
