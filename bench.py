@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--no-graphs", action="store_true", help="training leg: eager fwd/bwd instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernels-only", action="store_true", help="short run for ncu: sync path only")
+    ap.add_argument("--no-virtual", action="store_true", help="skip the virtual-rank (P=2/4/8 on one GPU) kernels")
+    ap.add_argument("--no-sync-graph", action="store_true",
+                    help="N=1: issue the timed steps one by one instead of replaying them as one CUDA graph")
     return ap.parse_args()
 
 
@@ -142,6 +145,24 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- helpers
+class Hold:
+    """lasgd_hold: a one-thread kernel that holds a stream until released, so a whole
+    timed region is enqueued before the device starts it (bounded: 30 s)."""
+
+    def __init__(self, N):
+        import ctypes
+
+        self._N, self._c = N, ctypes
+        self._h = ctypes.c_void_p()
+        N.check(N.lib().lasgd_hold_create(ctypes.byref(self._h)), "lasgd_hold_create")
+
+    def enqueue(self, stream):
+        self._N.check(self._N.lib().lasgd_hold_enqueue(self._h, self._c.c_void_p(stream.cuda_stream), 30.0))
+
+    def release(self):
+        self._N.check(self._N.lib().lasgd_hold_release(self._h))
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -186,6 +207,75 @@ def kernel_bytes(name, n, world, comm, algo_code, sgd_momentum=True):
     if name == "allreduce":
         return comm.bytes_per_node(algo_code), "nvlink"
     return 0, "hbm"
+
+
+def virtual_rank_kernels(n, dev, stream, hbm_peak, traffic, reps=10):
+    """The multi-rank kernels in their virtual-rank form (P ranks' buffers on this one
+    GPU, the same device code minus the flag barriers, which stream order replaces):
+    K8 mirror push (P=2), K8 staged push (P=4, 8), K3 two-shot mean (P=2, 4, 8), K2
+    one-shot mean (P=2).  Every byte a rank would move over NVLink moves through this
+    GPU's HBM instead, so the roofline is HBM.  Algorithmic bytes per round (all ranks;
+    B = 4n): push P*(7B + 4(P-1)/P*B) (local step + pull + next snapshot, staged
+    contributions read, mean pushed, peers' means read, next-snapshot chunks pushed);
+    two-shot P*(3B - B/P); one-shot 2P*B (each source read once, each mean written)."""
+    import torch
+
+    from paper_2203_13085_b200 import _native as N
+    from paper_2203_13085_b200 import kernels as K
+
+    B = 4 * n
+    out = {}
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    def entry(name, ms, byt, launches):
+        ach = byt / (ms * 1e-3) / 1e9
+        out[name] = {"avg_ms": ms, "bytes_per_round": byt, "bound": "hbm", "achieved_gbs": ach, "peak_gbs": hbm_peak,
+                     "frac": ach / hbm_peak, "launches_per_round": launches, "traffic": traffic.get(name)}
+
+    gen = torch.Generator(device=dev)
+    with torch.cuda.stream(stream):
+        for P in (2, 4, 8):
+            gen.manual_seed(77 + P)
+            xs = [torch.randn(n, device=dev, generator=gen) * 0.02 for _ in range(P)]
+            gs = [torch.randn(n, device=dev, generator=gen) * 1e-2 for _ in range(P)]
+            ms_ = [torch.zeros(n, device=dev) for _ in range(P)]
+            snaps = [[x.clone() for x in xs], [torch.empty(n, device=dev) for _ in range(P)]]
+            xbars = [torch.empty(n, device=dev) for _ in range(P)]
+            # K8 push round (mirror at P=2, staged at P>=3); the staging launch runs once
+            se = K.push_stage_elems(n, P)
+            stages = [torch.zeros(2 * P * se, device=dev) for _ in range(P)]
+            state = {"cur": 0, "init": True}
+            fk = dict(ms=ms_, momentum=0.9, weight_decay=1e-4, nesterov=True, alpha=1.0, stream=stream)
+
+            def push():
+                c = state["cur"]
+                K.fused_push_virtual(xs, gs, snaps[c], snaps[1 - c], xbars, stages, c, state["init"], 0.1,
+                                     first_step=state["init"], **fk)
+                state["cur"], state["init"] = 1 - c, False
+
+            push()
+            name = "push_mirror_virtual_p2" if P == 2 else f"push_staged_virtual_p{P}"
+            entry(name, timeit(push), P * (7 * B + 4 * (P - 1) * B // P), 2)
+            entry(f"twoshot_virtual_p{P}",
+                  timeit(lambda: K.mean_virtual(xbars, snaps[0], algo=N.ALGO_TWOSHOT, stream=stream)),
+                  P * (3 * B - B // P), 2)
+            if P == 2:
+                entry("oneshot_virtual_p2",
+                      timeit(lambda: K.mean_virtual(xbars, snaps[0], algo=N.ALGO_ONESHOT, stream=stream)),
+                      2 * P * B, 1)
+            del xs, gs, ms_, snaps, xbars, stages
+            torch.cuda.empty_cache()
+    return out
 
 
 def cpu_reference_run(n_full, P, k, steps, warmup, threads, target_step_s=1.0):
@@ -353,23 +443,37 @@ def main():
             worker.g = gsrc(t)
             worker.step()
 
-    # ---------------- value: HBM-resident gradients, device-timed
+    hold = Hold(N)
+
+    # ---------------- value: HBM-resident gradients, device-timed.  One rank: the K steps
+    # replay as ONE CUDA graph (LASGDWorker.capture: the deterministic loop reads its
+    # per-round scalars from the device round descriptor).  Every N: the timed region is
+    # enqueued behind a hold kernel and released at once, so host jitter cannot open gaps.
     with torch.cuda.stream(compute):
         w = make_worker(False)
         run_sync_path(w, args.warmup, lambda t: grads[t % 2])
         w.drain()
+        graph = None
+        if world == 1 and not args.no_sync_graph:
+            graph = w.capture([grads[t % 2] for t in range(args.steps)])
+            graph.replay()  # graph upload; one more untimed pass
     torch.cuda.synchronize()
     clocks = ClockSampler(local) if rank == 0 else None
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w.reset_records()
     with torch.cuda.stream(compute):
+        hold.enqueue(compute)
         e0.record(compute)
         h0 = time.perf_counter()
-        run_sync_path(w, args.steps, lambda t: grads[t % 2])
+        if graph is not None:
+            graph.replay()
+        else:
+            run_sync_path(w, args.steps, lambda t: grads[t % 2])
         host_issue_ms = (time.perf_counter() - h0) * 1e3
         w.drain()
         e1.record(compute)
+        hold.release()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1))
     host_issue_ms = max_over_ranks(host_issue_ms)
@@ -430,10 +534,12 @@ def main():
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(compute):
+        hold.enqueue(compute)
         f0.record(compute)
         copy_stream.wait_event(f0)  # the first H2D starts inside the timed region
         e2e_loop(we, args.steps)
         f1.record(compute)
+        hold.release()
     torch.cuda.synchronize()
     ms_e2e = max_over_ranks(f0.elapsed_time(f1))
     barrier()
@@ -485,6 +591,11 @@ def main():
             iso["fused_round"] = timeit(lambda: K.fused_round_virtual(
                 [x], [grads[0]], [s0], [s1], lr, ms=[m], **{k: v for k, v in fk.items() if k != "m"}))
     barrier()
+
+    # ---------------- multi-rank kernels in virtual-rank form (one GPU: the N=1 record)
+    vkernels = None
+    if world == 1 and not args.no_virtual:
+        vkernels = virtual_rank_kernels(n, dev, compute, peaks()[0], ncu_traffic())
 
     # ---------------- real training: ResNet-50 fwd/bwd + LASGD vs no-sync ceiling
     training = None
@@ -552,8 +663,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "host_issue_ms_per_step": host_issue_ms / args.steps,
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": config_dict(args, world, {1: "oneshot", 2: "twoshot", 3: "push"}.get(
+            "config": dict(config_dict(args, world, {1: "oneshot", 2: "twoshot", 3: "push"}.get(
                 comm.resolve_fused_algo(algo_code) if comm is not None else 1)),
+                timed_region=("one CUDA-graph replay of the K steps (LASGDWorker.capture), behind a hold kernel"
+                              if graph is not None else "K worker steps issued one by one, behind a hold kernel")),
             "roofline": roofline,
             "cpu_baseline": cpu_base,
             "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,
@@ -562,6 +675,7 @@ def main():
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "sync_kernels": kernels,
+            "virtual_rank_kernels": vkernels,
             "training": training,
         }
         print(json.dumps(line), flush=True)

@@ -102,6 +102,8 @@ int lasgd_elastic_pull(void* x, void* snap_next, const void* snap, const void* x
                        double alpha, unsigned long long* nonfinite, void* stream);
 
 /* K4b: reference finalize new = 1*z + 1*delta; x = new; snap_next = new (nullable).
+ * delta may be NULL: the accumulator is zero (no local step since the previous
+ * finalize reset it, optimizer.py:174), so new = z + 0.
  * Replaces optimizer.py:170-174 (`lasgd_finalize_round`, P > 1 branch). */
 int lasgd_finalize(void* x, void* snap_next, const void* z, const void* delta, size_t n, int dtype,
                    unsigned long long* nonfinite, void* stream);
@@ -240,6 +242,8 @@ int lasgd_comm_invalidate_staging(lasgd_comm* c);
 int lasgd_comm_launches(lasgd_comm* c, unsigned long long* out);
 /* rank, world size and the mean buffer of a communicator (any pointer may be NULL). */
 int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar);
+/* Element count and element type of the communicator's buffers (either pointer may be NULL). */
+int lasgd_comm_shape(lasgd_comm* c, size_t* n, int* dtype);
 
 /* ---- native per-rank worker: the round protocol (optimizer.py:181-207) ---- */
 
@@ -291,6 +295,44 @@ int lasgd_worker_set_timing(lasgd_worker* w, int on);
 int lasgd_worker_timings(lasgd_worker* w, int kind, float* out_ms, int max);
 int lasgd_worker_reset_stats(lasgd_worker* w);
 int lasgd_worker_destroy(lasgd_worker* w);
+
+/* ---- graph replay of the deterministic schedule (optimizer.py:181-207 with
+ * collective_complete = (tau_i == k)) ------------------------------------------
+ * The per-launch scalars of a worker step (learning rate, first_step, delta reset,
+ * snapshot slot) live in a device round descriptor that every captured launch reads
+ * at entry and its last CTA advances, so `steps` worker steps captured once replay as
+ * ONE CUDA graph launch, any number of times, with results bit-identical to the same
+ * steps issued one by one.  Single rank (comm NULL) for now; both pipelines (a round
+ * boundary is the local step with the next snapshot fused in). */
+typedef struct lasgd_graph lasgd_graph;
+/* Learning rate per local clock (lr_at of problems.py:355 for clocks 0..len-1); len 1 =
+ * a constant rate.  A replay that would read past a longer table fails with
+ * LASGD_ERR_STATE.  Synchronises the compute stream. */
+int lasgd_worker_set_lr_table(lasgd_worker* w, const double* lr, size_t len);
+/* Capture `steps` steps (a whole number of rounds) reading gradient g[t] at step t.  Nothing
+ * runs and the worker's state is unchanged until lasgd_graph_launch. */
+int lasgd_worker_graph_capture(lasgd_worker* w, int steps, const void* const* g, lasgd_graph** out);
+/* Capture worker steps into the caller's own stream capture (e.g. forward + backward +
+ * step in one graph): call with the compute stream capturing, issue the steps, then
+ * lasgd_worker_capture_end.  The returned lasgd_graph holds no executable: before each
+ * replay of the caller's graph on the compute stream, call lasgd_graph_launch (it
+ * refreshes the device descriptor when needed and advances the worker's state). */
+int lasgd_worker_capture_begin(lasgd_worker* w, lasgd_graph** out);
+int lasgd_worker_capture_end(lasgd_graph* gr);
+/* Replay on the worker's compute stream and advance the worker's state by the captured
+ * steps; LASGD_ERR_STATE if the worker is not at the round position of the capture. */
+int lasgd_graph_launch(lasgd_graph* gr);
+int lasgd_graph_destroy(lasgd_graph* gr);
+
+/* ---- measurement aid ------------------------------------------------------ */
+/* One thread that holds `stream` until lasgd_hold_release (or `timeout_s` passes): the
+ * host enqueues a whole timed region behind it, then releases it, so host-side jitter
+ * cannot open gaps in the region.  Destroy only after the stream has drained. */
+typedef struct lasgd_hold lasgd_hold;
+int lasgd_hold_create(lasgd_hold** out);
+int lasgd_hold_enqueue(lasgd_hold* h, void* stream, double timeout_s);
+int lasgd_hold_release(lasgd_hold* h);
+int lasgd_hold_destroy(lasgd_hold* h);
 
 /* ---- host utilities ------------------------------------------------------ */
 

@@ -29,7 +29,7 @@ from .collective import (  # noqa: E402
     poll,
     ring_schedule,
 )
-from .engine import LASGDWorker, SGDARWorker  # noqa: E402
+from .engine import LASGDWorker, SGDARWorker, SyncGraph  # noqa: E402
 from .graphs import GraphedStep  # noqa: E402
 from .flat import FlatParams  # noqa: E402
 from .optimizer import (  # noqa: E402
@@ -52,7 +52,7 @@ from .problems import LrSchedule, lr_at  # noqa: E402
 
 __all__ = [
     "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
-    "DimensionMismatchError", "FlatParams", "GraphedStep", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "ModelDivergenceError",
+    "DimensionMismatchError", "FlatParams", "GraphedStep", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "SyncGraph", "ModelDivergenceError",
     "NodeState", "NonFiniteError", "P2PCommunicator", "RingSchedule", "RingStep", "SGDARWorker", "SgdConfig", "Status", "TickAction", "TransportFault",
     "AllReduceOutcome", "all_reduce_average", "as_device_vector", "execute_allreduce", "blend", "bytes_per_node", "easgd_round_robin_exchange",
     "elastic_center_step", "elastic_local_step", "mean_of_vectors", "lasgd_finalize_round", "lasgd_node_tick",

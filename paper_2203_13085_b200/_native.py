@@ -153,6 +153,7 @@ SIGNATURES = {
     "lasgd_comm_read_trace": (_I, [_P, _P, _I]),
     "lasgd_comm_destroy": (_I, [_P]),
     "lasgd_comm_info": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_P)]),
+    "lasgd_comm_shape": (_I, [_P, ctypes.POINTER(_SZ), ctypes.POINTER(_I)]),
     "lasgd_comm_peer_max_seq": (_I, [_P, _ULLP]),
     "lasgd_comm_launches": (_I, [_P, _ULLP]),
     "lasgd_comm_invalidate_staging": (_I, [_P]),
@@ -168,6 +169,16 @@ SIGNATURES = {
     "lasgd_worker_timings": (_I, [_P, _I, ctypes.POINTER(ctypes.c_float), _I]),
     "lasgd_worker_reset_stats": (_I, [_P]),
     "lasgd_worker_destroy": (_I, [_P]),
+    "lasgd_worker_set_lr_table": (_I, [_P, ctypes.POINTER(ctypes.c_double), _SZ]),
+    "lasgd_worker_graph_capture": (_I, [_P, _I, _P, ctypes.POINTER(_P)]),
+    "lasgd_worker_capture_begin": (_I, [_P, ctypes.POINTER(_P)]),
+    "lasgd_worker_capture_end": (_I, [_P]),
+    "lasgd_graph_launch": (_I, [_P]),
+    "lasgd_graph_destroy": (_I, [_P]),
+    "lasgd_hold_create": (_I, [ctypes.POINTER(_P)]),
+    "lasgd_hold_enqueue": (_I, [_P, _P, _D]),
+    "lasgd_hold_release": (_I, [_P]),
+    "lasgd_hold_destroy": (_I, [_P]),
     "lasgd_partition_chunks": (_I, [_SZ, _I, ctypes.POINTER(_SZ)]),
     "lasgd_bytes_per_node": (ctypes.c_ulonglong, [_SZ, _I, _I, _I]),
 }

@@ -164,6 +164,16 @@ class _EventHandle(CollectiveHandle):
     def __init__(self, round_id: int):
         super().__init__(round_id)
         self._event: Optional[torch.cuda.Event] = None
+        self._nf_host: Optional[torch.Tensor] = None  # pinned copy of the mean's non-finite count
+
+    @property
+    def result(self) -> torch.Tensor:
+        out = super().result
+        # collective.py:201-202 checks the mean; the fused counter landed with the event
+        bad = int(self._nf_host.item()) if self._nf_host is not None else 0
+        if bad:
+            raise N.NonFiniteError(f"all-reduce result: {bad} non-finite entries out of {out.numel()}")
+        return out
 
     def _probe(self) -> Status:
         if self._status is Status.IN_FLIGHT and self._event is not None and self._event.query():
@@ -236,8 +246,12 @@ class CudaLoopbackTransport:
             handle._result = vectors[0]  # collective.py:174-175: input unchanged
         else:
             out = torch.empty_like(vectors[0])
-            K.mean_virtual([out], vectors, algo=N.ALGO_ONESHOT if self.algo == N.ALGO_AUTO else self.algo)
+            nf = torch.zeros(1, dtype=torch.int64, device=out.device)
+            K.mean_virtual([out], vectors, algo=N.ALGO_ONESHOT if self.algo == N.ALGO_AUTO else self.algo,
+                           nonfinite=nf)
             handle._result = out
+            handle._nf_host = torch.empty(1, dtype=torch.int64, pin_memory=True)
+            handle._nf_host.copy_(nf, non_blocking=True)
         handle._event = torch.cuda.Event()
         handle._event.record()
         bpe = vectors[0].element_size()

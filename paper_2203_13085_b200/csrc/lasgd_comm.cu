@@ -317,6 +317,8 @@ struct lasgd_comm {
   bool trace_on = false;
   bool gate = false;           // launch k_gate ahead of every all-reduce (side-stream use)
   unsigned long long seq = 0;  // launches issued
+  uint32_t* epoch_host = nullptr;      // pinned readback of the peers' entry flags (read_peer_epochs)
+  cudaStream_t epoch_stream = nullptr;  // on this communicator's device
   cudaEvent_t ev[kEvents];
   int nev = 0;
 };
@@ -453,11 +455,14 @@ extern "C" int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo) {
 // non-blocking stream, so it never waits behind the caller's (possibly stalled)
 // streams.  out[q] = epoch of peer q's latest launch (u32, wrapping compare).
 static int read_peer_epochs(lasgd_comm* c, int rows, uint32_t* out) {
-  static thread_local uint32_t* host = nullptr;
-  static thread_local cudaStream_t s = nullptr;
+  // per-communicator pinned buffer and stream, created on c->device (the caller holds a
+  // DeviceGuard) and freed by lasgd_comm_destroy
   const size_t entry_words = (size_t)kMaxB * kMaxR;
-  if (!host) LASGD_CUDA_TRY(cudaHostAlloc((void**)&host, (entry_words + kMaxR) * sizeof(uint32_t), cudaHostAllocDefault));
-  if (!s) LASGD_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  if (!c->epoch_host)
+    LASGD_CUDA_TRY(cudaHostAlloc((void**)&c->epoch_host, (entry_words + kMaxR) * sizeof(uint32_t), cudaHostAllocDefault));
+  if (!c->epoch_stream) LASGD_CUDA_TRY(cudaStreamCreateWithFlags(&c->epoch_stream, cudaStreamNonBlocking));
+  uint32_t* host = c->epoch_host;
+  cudaStream_t s = c->epoch_stream;
   const size_t gate_word = (size_t)2 * kMaxB * kMaxR + (size_t)2 * kMaxR;  // k_gate's rank-level slots
   LASGD_CUDA_TRY(cudaMemcpyAsync(host, c->base, (size_t)rows * kMaxR * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   LASGD_CUDA_TRY(cudaMemcpyAsync(host + entry_words, c->base + gate_word * sizeof(uint32_t), kMaxR * sizeof(uint32_t),
@@ -481,10 +486,12 @@ extern "C" int lasgd_comm_peer_max_seq(lasgd_comm* c, unsigned long long* out) {
   uint32_t ep[kMaxR];
   int rc = read_peer_epochs(c, kMaxB, ep);
   if (rc) return rc;
-  uint32_t best = 0;
+  // epochs are the low 32 bits of the sequence numbers: wrapping compare, like peers_ahead
+  uint32_t best = (uint32_t)c->seq;
   for (int q = 0; q < c->world; ++q)
-    if (q != c->rank && ep[q] > best) best = ep[q];
-  *out = best;
+    if (q != c->rank && (int32_t)(ep[q] - best) > 0) best = ep[q];
+  // extend to 64 bits around this rank's own sequence number
+  *out = c->seq + (unsigned long long)(int64_t)(int32_t)(best - (uint32_t)c->seq);
   return LASGD_OK;
 }
 
@@ -526,6 +533,13 @@ extern "C" int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar
   if (rank) *rank = c->rank;
   if (world) *world = c->world;
   if (xbar) *xbar = c->base + c->off_xbar;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_comm_shape(lasgd_comm* c, size_t* n, int* dtype) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (n) *n = c->n;
+  if (dtype) *dtype = c->dtype;
   return LASGD_OK;
 }
 
@@ -785,6 +799,8 @@ extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
   if (c->end_ctr) cudaFree(c->end_ctr);
   if (c->trace_buf) cudaFree(c->trace_buf);
   if (c->status_host) cudaFreeHost(c->status_host);
+  if (c->epoch_host) cudaFreeHost(c->epoch_host);
+  if (c->epoch_stream) cudaStreamDestroy(c->epoch_stream);
   if (c->base) cudaFree(c->base);
   delete c;
   return LASGD_OK;

@@ -25,6 +25,11 @@ int num_sms();  // SM count of the current device (cached per device)
 // K5 with the next snapshot written in the same pass (lasgd_elementwise.cu).
 int sgd_step_snapshot(int dtype, void* x, const void* g, void* m, void* delta, void* snap, size_t n,
                       const lasgd_sgd_params* p, unsigned long long* nf, void* s);
+struct RoundAdv;
+// K5 with the per-launch scalars read from the device round descriptor (graph replay);
+// snaps != nullptr also writes the next snapshot slot snaps[1 - cur] (P = 1 round).
+int sgd_step_dyn(int dtype, void* x, const void* g, void* m, void* delta, void* const* snaps, size_t n,
+                 const lasgd_sgd_params* p, unsigned long long* nf, void* s, const RoundAdv& adv);
 
 // ---------------------------------------------------------------- arithmetic
 // Separately rounded ops (the reference's numpy never contracts a*b+c).
@@ -130,6 +135,83 @@ __device__ __forceinline__ unsigned pull_elem(T neg_alpha, T& xv, T sv, T zv) {
   const T diff = add_rn(sv, mul_rn(T(-1), zv));
   xv = add_rn(xv, mul_rn(neg_alpha, diff));
   return !finite(diff) + !finite(xv);
+}
+
+// ---------------------------------------------------------------- device round descriptor
+// The per-launch scalars of the deterministic schedule (optimizer.py:181-207 with
+// collective_complete = (tau_i == k)) live in device memory so that a captured loop of
+// worker steps replays as one CUDA graph: every CTA of a launch reads the learning
+// rate (table indexed by the local clock, problems.py:322-365), first_step, the delta
+// reset flag and the snapshot slot at entry, and the last CTA to finish advances the
+// descriptor for the next launch (RoundAdv says how: baked into the graph node, the
+// same on every replay because a graph holds a whole number of rounds).
+struct DevRound {
+  unsigned long long clock;         // local steps taken (NodeState.local_clock)
+  unsigned long long seq;           // communicator launches issued (epoch of the next one - 1)
+  const double* lr;                 // learning rate per local clock
+  unsigned long long lr_len;        // clock >= lr_len reads the last entry
+  int snap_idx;                     // current snapshot slot
+  int mom_started;                  // momentum buffer initialised (first_step = !mom_started)
+  int delta_fresh;                  // delta is logically zero (reset at the last finalize)
+  unsigned int arrive;              // CTAs of the running launch that have finished
+};
+
+struct RoundAdv {
+  DevRound* rd;   // nullptr: static launch arguments (eager path)
+  int steps;      // local steps this launch takes (0 or 1)
+  int close;      // this launch closes a round (snapshot slot flips, delta reset)
+  int has_mom;    // momentum buffer in use
+  int has_delta;  // delta accumulator in use
+  int seq_inc;    // communicator launches this kernel counts as
+};
+
+struct DynView {
+  double lr;
+  int first, reset, cur;
+};
+
+// Every thread reads the descriptor (one L2 line, written by the previous kernel).
+__device__ __forceinline__ DynView dyn_read(const DevRound* r) {
+  DynView v;
+  const unsigned long long k = __ldcg(&r->clock);
+  const unsigned long long len = __ldcg(&r->lr_len);
+  const double* lr = (const double*)__ldcg((const unsigned long long*)&r->lr);
+  v.lr = __ldcg(lr + (k < len ? k : len - 1));
+  v.first = !__ldcg(&r->mom_started);
+  v.reset = __ldcg(&r->delta_fresh);
+  v.cur = __ldcg(&r->snap_idx);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ void dyn_coef(SgdCoef<T>& c, const DynView& v) {
+  c.neg_lr = (T)(-v.lr);  // the host's (T)(-lr) of make_sgd_coef
+  c.first = v.first != 0;
+  c.reset = c.use_delta && v.reset != 0;
+}
+
+// Last CTA of the launch (of `total` CTAs) advances the descriptor.  Every CTA read it
+// at entry, before counting itself in, so the update cannot race a reader.
+__device__ __forceinline__ void dyn_advance(const RoundAdv& ad, unsigned total) {
+  if (ad.rd == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    DevRound* r = ad.rd;
+    if (atomicAdd(&r->arrive, 1u) == total - 1u) {
+      r->arrive = 0u;
+      r->clock += (unsigned long long)ad.steps;
+      r->seq += (unsigned long long)ad.seq_inc;
+      if (ad.steps && ad.has_mom) r->mom_started = 1;
+      if (ad.close) {
+        r->snap_idx ^= 1;
+        r->delta_fresh = ad.has_delta;
+      } else if (ad.steps) {
+        r->delta_fresh = 0;
+      }
+      __threadfence();
+    }
+  }
 }
 
 // CTAs per SM of the streaming kernels (tunable, lasgd_set_stream_ctas_per_sm).  The

@@ -25,7 +25,7 @@ constexpr int kThreads = 256;
 // near 32 registers (<= 64 total under __launch_bounds__(256, 4), no spills).
 
 template <typename T, typename Op, int U>
-__global__ void __launch_bounds__(kThreads, 4) k_stream(Op op, size_t n, unsigned long long* nonfinite) {
+__device__ __forceinline__ void stream_body(Op& op, size_t n, unsigned long long* nonfinite) {
   constexpr int W = Pack<T>::W;
   const size_t npack = n / W;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -46,6 +46,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_stream(Op op, size_t n, unsigne
   const size_t t = npack * W + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) bad += op.scalar(t);
   report_nonfinite(nonfinite, bad);
+}
+
+template <typename T, typename Op, int U>
+__global__ void __launch_bounds__(kThreads, 4) k_stream(Op op, size_t n, unsigned long long* nonfinite) {
+  stream_body<T, Op, U>(op, n, nonfinite);
 }
 
 // Fallback for buffers that are not 16-byte aligned (e.g. arbitrary views).
@@ -205,7 +210,12 @@ struct FinalizeOp {
   struct Loaded { Pack<T> z, d; };
   __device__ __forceinline__ void load(Loaded& L, size_t j) const {
     L.z = ld_stream(z + j);
-    L.d = ld_stream(delta + j);
+    if (delta) {
+      L.d = ld_stream(delta + j);
+    } else {
+#pragma unroll
+      for (int k = 0; k < Pack<T>::W; ++k) L.d.v[k] = T(0);
+    }
   }
   __device__ __forceinline__ unsigned compute_store(Loaded& L, size_t j) const {
     Pack<T> o;
@@ -220,7 +230,7 @@ struct FinalizeOp {
     return bad;
   }
   __device__ __forceinline__ unsigned scalar(size_t j) const {
-    T o = add_rn(z[j], delta[j]);
+    T o = add_rn(z[j], delta ? delta[j] : T(0));
     x[j] = o;
     if (snap_next) snap_next[j] = o;
     return !finite(o);
@@ -265,6 +275,53 @@ int sgd_step_snapshot(int dtype, void* x, const void* g, void* m, void* delta, v
   return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
 }
 
+// K5 (and the P = 1 round: K5 + next snapshot) with lr / first_step / delta reset /
+// snapshot slot from the device round descriptor: the graph-replayable form.
+template <typename T, int U>
+__global__ void __launch_bounds__(kThreads, 4) k_sgd_dyn(SgdOp<T> op, T* snap0, T* snap1, size_t n,
+                                                        unsigned long long* nonfinite, RoundAdv adv, bool aligned) {
+  const DynView v = dyn_read(adv.rd);
+  dyn_coef(op.c, v);
+  op.snap = snap0 == nullptr ? nullptr : (v.cur ? snap0 : snap1);  // next slot = 1 - cur
+  if (aligned)
+    stream_body<T, SgdOp<T>, U>(op, n, nonfinite);
+  else {  // unaligned views: the scalar loop
+    unsigned bad = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+      bad += op.scalar(i);
+    report_nonfinite(nonfinite, bad);
+  }
+  dyn_advance(adv, gridDim.x);
+}
+
+template <typename T>
+int sgd_dyn_t(void* x, const void* g, void* m, void* delta, void* const* snaps, size_t n, const lasgd_sgd_params* p,
+              unsigned long long* nf, void* s, const RoundAdv& adv) {
+  SgdOp<T> op;
+  op.x = (T*)x;
+  op.g = (const T*)g;
+  op.m = (T*)m;
+  op.delta = (T*)delta;
+  op.snap = nullptr;
+  op.c = make_sgd_coef<T>(p, delta != nullptr);
+  const size_t npack = n / Pack<T>::W;
+  const size_t work = npack > (size_t)kThreads ? npack : (size_t)kThreads;
+  const bool al = aligned16(x) && aligned16(g) && (!op.c.use_mom || aligned16(m)) &&
+                  (!op.c.use_delta || aligned16(delta)) && (!snaps || (aligned16(snaps[0]) && aligned16(snaps[1])));
+  k_sgd_dyn<T, SgdOp<T>::U><<<stream_grid(work, kThreads), kThreads, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      op, snaps ? (T*)snaps[0] : nullptr, snaps ? (T*)snaps[1] : nullptr, n, nf, adv, al);
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
+
+int sgd_step_dyn(int dtype, void* x, const void* g, void* m, void* delta, void* const* snaps, size_t n,
+                 const lasgd_sgd_params* p, unsigned long long* nf, void* s, const RoundAdv& adv) {
+  if (!adv.rd) return fail(LASGD_ERR_INVALID_ARGUMENT, "sgd_step_dyn: no round descriptor");
+  if (dtype == LASGD_F32) return sgd_dyn_t<float>(x, g, m, delta, snaps, n, p, nf, s, adv);
+  if (dtype == LASGD_F64) return sgd_dyn_t<double>(x, g, m, delta, snaps, n, p, nf, s, adv);
+  return fail(LASGD_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+}
+
 template <typename T>
 int pull_t(void* x, void* snap_next, const void* snap, const void* xbar, size_t n, double alpha,
            unsigned long long* nf, void* s) {
@@ -277,7 +334,7 @@ template <typename T>
 int finalize_t(void* x, void* snap_next, const void* z, const void* delta, size_t n, unsigned long long* nf,
                void* s) {
   FinalizeOp<T> op{(T*)x, (T*)snap_next, (const T*)z, (const T*)delta};
-  bool al = aligned16(x) && aligned16(z) && aligned16(delta) && (!snap_next || aligned16(snap_next));
+  bool al = aligned16(x) && aligned16(z) && (!delta || aligned16(delta)) && (!snap_next || aligned16(snap_next));
   return launch<T>(op, n, al, nf, s);
 }
 
@@ -329,7 +386,9 @@ extern "C" int lasgd_elastic_pull(void* x, void* snap_next, const void* snap, co
 
 extern "C" int lasgd_finalize(void* x, void* snap_next, const void* z, const void* delta, size_t n, int dtype,
                               unsigned long long* nonfinite, void* stream) {
-  if (n && (!x || !z || !delta)) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_finalize: null buffer");
+  // delta == NULL: the accumulator is zero (no local step since the last finalize,
+  // optimizer.py:174), so new = z + 0 without reading it
+  if (n && (!x || !z)) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_finalize: null buffer");
   DISPATCH_DTYPE(dtype, finalize_t<float>(x, snap_next, z, delta, n, nonfinite, stream),
                  finalize_t<double>(x, snap_next, z, delta, n, nonfinite, stream));
 }

@@ -109,3 +109,68 @@ extern "C" unsigned long long lasgd_bytes_per_node(size_t d, int P, int bpe, int
   }
   return best;
 }
+
+// ---------------------------------------------------------------- stream hold
+// Measurement aid (the "blocking kernel" of GPU benchmarking practice): one thread
+// spins on a host-mapped flag so that the host can enqueue a whole timed region behind
+// it and release it at once — the device then runs the region back to back and host
+// jitter before or during enqueueing (driver locks taken by NVML queries, the GIL)
+// cannot open gaps in it.  Bounded: the kernel exits by itself after `timeout_ns`.
+struct lasgd_hold {
+  volatile unsigned int* host = nullptr;
+  unsigned int* dev = nullptr;
+};
+
+namespace lasgd {
+__global__ void k_hold(const volatile unsigned int* flag, long long timeout_ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0u) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if ((long long)(t - t0) > timeout_ns) break;
+    __nanosleep(1000);
+  }
+}
+}  // namespace lasgd
+
+extern "C" int lasgd_hold_create(lasgd_hold** out) {
+  if (!out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null out");
+  lasgd_hold* h = new lasgd_hold();
+  unsigned int* p = nullptr;
+  cudaError_t e = cudaHostAlloc((void**)&p, sizeof(unsigned int), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&h->dev, p, 0);
+  if (e != cudaSuccess) {
+    if (p) cudaFreeHost(p);
+    delete h;
+    return cuda_fail(e, "cudaHostAlloc(hold flag)");
+  }
+  h->host = p;
+  *h->host = 0u;
+  *out = h;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_hold_enqueue(lasgd_hold* h, void* stream, double timeout_s) {
+  if (!h) return fail(LASGD_ERR_INVALID_ARGUMENT, "null hold");
+  *h->host = 0u;
+  __sync_synchronize();
+  k_hold<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(h->dev, (long long)(timeout_s * 1e9));
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_hold_release(lasgd_hold* h) {
+  if (!h) return fail(LASGD_ERR_INVALID_ARGUMENT, "null hold");
+  __sync_synchronize();
+  *h->host = 1u;
+  __sync_synchronize();
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_hold_destroy(lasgd_hold* h) {
+  if (!h) return LASGD_OK;
+  *h->host = 1u;
+  cudaFreeHost((void*)h->host);
+  delete h;
+  return LASGD_OK;
+}

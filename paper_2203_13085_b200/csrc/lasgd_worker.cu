@@ -58,6 +58,14 @@ struct lasgd_worker {
   std::vector<cudaEvent_t> lead;  // adaptive run-ahead throttle ring
   size_t lead_pos = 0;
   long long lead_count = 0;
+  // graph replay (deterministic schedule): the device round descriptor the captured
+  // launches read and advance, and the learning-rate table it indexes
+  DevRound* rd = nullptr;
+  double* lr_dev = nullptr;
+  size_t lr_len = 0;
+  bool dyn = false;       // issuing into a capture: launches take their scalars from rd
+  cudaStream_t cap_stream = nullptr;  // lasgd_worker_graph_capture records here
+  bool rd_dirty = true;   // eager launches ran since rd was last written
   // instrumentation
   bool timed = false;
   std::vector<TimingRec> recs;
@@ -158,12 +166,36 @@ static int close_round(lasgd_worker* w) {
   return LASGD_OK;
 }
 
+static RoundAdv make_adv(const lasgd_worker* w, int close) {
+  RoundAdv a;
+  a.rd = w->rd;
+  a.steps = 1;
+  a.close = close;
+  a.has_mom = w->m != nullptr;
+  a.has_delta = w->delta != nullptr;
+  a.seq_inc = 0;
+  return a;
+}
+
+// Graph capture, one rank: the local step, with the next snapshot fused in when the
+// step closes a round (K7 at P = 1, optimizer.py:168-169 — both pipelines).
+static int dyn_step(lasgd_worker* w, const void* g, int close) {
+  lasgd_sgd_params p = sgd_params(w, 0.0);  // lr, first_step, delta_reset come from rd
+  void* snaps[2] = {w->snap[0], w->snap[1]};
+  return issue(w, close ? K_FUSED : K_SGD, w->compute, [&] {
+    return sgd_step_dyn(w->dtype, w->x, g, w->m, w->delta, close ? snaps : nullptr, w->n, &p, w->nonfinite,
+                        (void*)w->compute, make_adv(w, close));
+  });
+}
+
 static int fused_step(lasgd_worker* w, const void* g, double lr) {
   const int cur = w->snap_idx, nxt = 1 - cur;
   lasgd_sgd_params p = sgd_params(w, lr);
   const int mode = finalize_mode(w) ? 1 : 0;
   int rc;
-  if (w->world == 1) {
+  if (w->dyn) {
+    rc = dyn_step(w, g, 1);
+  } else if (w->world == 1) {
     void* xs[1] = {w->x};
     const void* gs[1] = {g};
     void* ms[1] = {w->m};
@@ -221,6 +253,19 @@ extern "C" int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* del
       delete w;
       return wr;
     }
+    // the kernels stream the caller's n over the communicator's buffers (and comm->n
+    // over the caller's): a mismatch would read and write out of bounds, peers included
+    size_t cn = 0;
+    int cdt = -1;
+    if ((wr = lasgd_comm_shape(comm, &cn, &cdt)) != 0) {
+      delete w;
+      return wr;
+    }
+    if (cn != n || cdt != dtype) {
+      delete w;
+      return fail(LASGD_ERR_DIMENSION, "communicator holds %zu elements of type %d, the worker %zu of type %d", cn,
+                  cdt, n, dtype);
+    }
     if (lasgd_comm_buffer(comm, 0, &w->snap[0]) || lasgd_comm_buffer(comm, 1, &w->snap[1])) {
       delete w;
       return LASGD_ERR_INVALID_ARGUMENT;
@@ -256,9 +301,11 @@ extern "C" int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* del
 
 extern "C" int lasgd_worker_step(lasgd_worker* w, const void* g, double lr) {
   if (!w || !g) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
-  if (w->cfg.pipeline == 1 && w->cfg.sync && w->tau + 1 == w->cfg.sync_period) return fused_step(w, g, lr);
+  if (!w->dyn) w->rd_dirty = true;
+  const bool closes = w->cfg.sync && !w->cfg.adaptive && w->tau + 1 == w->cfg.sync_period;
+  if ((w->cfg.pipeline == 1 || (w->dyn && w->world == 1)) && closes) return fused_step(w, g, lr);
   lasgd_sgd_params p = sgd_params(w, lr);
-  int rc = issue(w, K_SGD, w->compute, [&] {
+  int rc = w->dyn ? dyn_step(w, g, 0) : issue(w, K_SGD, w->compute, [&] {
     return lasgd_sgd_step(w->x, g, w->m, w->delta, w->n, w->dtype, &p, w->nonfinite, (void*)w->compute);
   });
   if (rc) return rc;
@@ -371,10 +418,219 @@ extern "C" int lasgd_worker_reset_stats(lasgd_worker* w) {
   return LASGD_OK;
 }
 
+// ---------------------------------------------------------------- graph replay
+// Host mirror of the protocol state, saved at capture begin and put back at the end:
+// the captured launches advance it as they are issued; a replay applies that advance.
+struct lasgd_graph_saved {
+  int tau, snap_idx;
+  long long clock, gclock;
+  bool mom, dfresh;
+  long long launches[K_KINDS], hist[LASGD_TAU_HIST];
+};
+
+struct lasgd_graph {
+  lasgd_worker* w = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int steps = 0, tau0 = 0;
+  lasgd_graph_saved saved;
+  // what one replay does to the host mirror of the protocol state
+  long long d_clock = 0, d_rounds = 0;
+  bool mom_after = false, delta_fresh_after = false;
+  long long d_launches[K_KINDS] = {0};
+  long long d_tau_hist[LASGD_TAU_HIST] = {0};
+};
+
+namespace lasgd {
+__global__ void k_round_set(DevRound* r, unsigned long long clock, unsigned long long seq, const double* lr,
+                            unsigned long long lr_len, int snap_idx, int mom_started, int delta_fresh) {
+  r->clock = clock;
+  r->seq = seq;
+  r->lr = lr;
+  r->lr_len = lr_len;
+  r->snap_idx = snap_idx;
+  r->mom_started = mom_started;
+  r->delta_fresh = delta_fresh;
+  r->arrive = 0u;
+}
+}  // namespace lasgd
+
+extern "C" int lasgd_worker_set_lr_table(lasgd_worker* w, const double* lr, size_t len) {
+  if (!w || !lr || len == 0) return fail(LASGD_ERR_INVALID_ARGUMENT, "null or empty learning-rate table");
+  for (size_t i = 0; i < len; ++i)
+    if (!(lr[i] > 0.0)) return fail(LASGD_ERR_INVALID_ARGUMENT, "learning rate %zu is %g, must be positive", i, lr[i]);
+  // the old table may still be read by queued replays
+  LASGD_CUDA_TRY(cudaStreamSynchronize(w->compute));
+  if (w->lr_dev) cudaFree(w->lr_dev);
+  w->lr_dev = nullptr;
+  w->lr_len = 0;
+  if (!w->rd) LASGD_CUDA_TRY(cudaMalloc(&w->rd, sizeof(DevRound)));  // (no allocation may happen inside a capture)
+  LASGD_CUDA_TRY(cudaMalloc(&w->lr_dev, len * sizeof(double)));
+  LASGD_CUDA_TRY(cudaMemcpy(w->lr_dev, lr, len * sizeof(double), cudaMemcpyHostToDevice));
+  w->lr_len = len;
+  w->rd_dirty = true;
+  return LASGD_OK;
+}
+
+static int capture_check(lasgd_worker* w) {
+  if (w->cfg.adaptive) return fail(LASGD_ERR_UNSUPPORTED, "graph replay needs the deterministic schedule");
+  if (w->world > 1) return fail(LASGD_ERR_UNSUPPORTED, "graph replay of multi-rank rounds is not built");
+  if (w->timed) return fail(LASGD_ERR_STATE, "per-launch timing cannot be captured");
+  if (w->dyn) return fail(LASGD_ERR_STATE, "a capture is already open on this worker");
+  if (!w->lr_dev || !w->rd)
+    return fail(LASGD_ERR_STATE, "set the learning-rate table first (lasgd_worker_set_lr_table)");
+  return LASGD_OK;
+}
+
+static void capture_open(lasgd_worker* w, lasgd_graph* gr) {
+  lasgd_graph_saved& v = gr->saved;
+  gr->w = w;
+  gr->tau0 = w->tau;
+  v.tau = w->tau;
+  v.snap_idx = w->snap_idx;
+  v.clock = w->local_clock;
+  v.gclock = w->global_clock;
+  v.mom = w->mom_started;
+  v.dfresh = w->delta_fresh;
+  memcpy(v.launches, w->launches, sizeof(v.launches));
+  memcpy(v.hist, w->tau_hist, sizeof(v.hist));
+  w->dyn = true;
+}
+
+// Close the capture: record what the captured steps did, put the mirror back.
+static int capture_close(lasgd_worker* w, lasgd_graph* gr) {
+  const lasgd_graph_saved& v = gr->saved;
+  w->dyn = false;
+  gr->steps = (int)(w->local_clock - v.clock);
+  gr->d_clock = w->local_clock - v.clock;
+  gr->d_rounds = w->global_clock - v.gclock;
+  gr->mom_after = w->mom_started;
+  gr->delta_fresh_after = w->delta_fresh;
+  const int tau_end = w->tau;
+  for (int k = 0; k < K_KINDS; ++k) gr->d_launches[k] = w->launches[k] - v.launches[k];
+  for (int t = 0; t < LASGD_TAU_HIST; ++t) gr->d_tau_hist[t] = w->tau_hist[t] - v.hist[t];
+  w->tau = v.tau;
+  w->snap_idx = v.snap_idx;
+  w->local_clock = v.clock;
+  w->global_clock = v.gclock;
+  w->mom_started = v.mom;
+  w->delta_fresh = v.dfresh;
+  memcpy(w->launches, v.launches, sizeof(v.launches));
+  memcpy(w->tau_hist, v.hist, sizeof(v.hist));
+  if (w->cfg.sync && tau_end != gr->tau0)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "a graph holds whole rounds: %d steps, sync period %d", gr->steps,
+                w->cfg.sync_period);
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_worker_graph_capture(lasgd_worker* w, int steps, const void* const* g, lasgd_graph** out) {
+  if (!w || !g || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (steps < 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "steps must be >= 1");
+  for (int t = 0; t < steps; ++t)
+    if (!g[t]) return fail(LASGD_ERR_INVALID_ARGUMENT, "gradient %d is null", t);
+  if (w->cfg.sync && steps % w->cfg.sync_period)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "a graph holds whole rounds: %d steps, sync period %d", steps,
+                w->cfg.sync_period);
+  int rc = capture_check(w);
+  if (rc) return rc;
+  // capture on a private stream (the compute stream may be the legacy default stream,
+  // which cannot be captured); the graph is launched on the compute stream
+  if (!w->cap_stream) LASGD_CUDA_TRY(cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking));
+  lasgd_graph* gr = new lasgd_graph();
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(w->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    delete gr;
+    return cuda_fail(e, "cudaStreamBeginCapture");
+  }
+  cudaStream_t compute = w->compute;
+  w->compute = w->cap_stream;
+  capture_open(w, gr);
+  for (int t = 0; t < steps && rc >= 0; ++t) rc = lasgd_worker_step(w, g[t], 0.0);
+  const int rc_close = capture_close(w, gr);
+  w->compute = compute;
+  e = cudaStreamEndCapture(w->cap_stream, &graph);
+  if (rc >= 0) rc = rc_close;
+  if (rc >= 0 && e != cudaSuccess) rc = cuda_fail(e, "cudaStreamEndCapture");
+  if (rc >= 0) {
+    e = cudaGraphInstantiate(&gr->exec, graph, 0);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphInstantiate");
+  }
+  if (graph) cudaGraphDestroy(graph);
+  if (rc < 0) {
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    delete gr;
+    return rc;
+  }
+  *out = gr;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_worker_capture_begin(lasgd_worker* w, lasgd_graph** out) {
+  if (!w || !out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  LASGD_CUDA_TRY(cudaStreamIsCapturing(w->compute, &st));
+  if (st != cudaStreamCaptureStatusActive)
+    return fail(LASGD_ERR_STATE, "the worker's compute stream is not being captured");
+  int rc = capture_check(w);
+  if (rc) return rc;
+  lasgd_graph* gr = new lasgd_graph();
+  capture_open(w, gr);
+  *out = gr;
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_worker_capture_end(lasgd_graph* gr) {
+  if (!gr || !gr->w || !gr->w->dyn) return fail(LASGD_ERR_STATE, "no capture open");
+  return capture_close(gr->w, gr);
+}
+
+extern "C" int lasgd_graph_launch(lasgd_graph* gr) {
+  if (!gr) return fail(LASGD_ERR_INVALID_ARGUMENT, "null graph");
+  lasgd_worker* w = gr->w;
+  if (w->tau != gr->tau0)
+    return fail(LASGD_ERR_STATE, "graph captured at local step %d of a round, worker is at step %d", gr->tau0, w->tau);
+  if (w->lr_len > 1 && (unsigned long long)(w->local_clock + gr->d_clock) > w->lr_len)
+    return fail(LASGD_ERR_STATE, "learning-rate table holds %zu clocks, the replay needs %lld", w->lr_len,
+                w->local_clock + gr->d_clock);
+  if (w->rd_dirty) {
+    k_round_set<<<1, 1, 0, w->compute>>>(w->rd, (unsigned long long)w->local_clock, w->seq, w->lr_dev,
+                                         (unsigned long long)w->lr_len, w->snap_idx, w->mom_started ? 1 : 0,
+                                         w->delta_fresh ? 1 : 0);
+    LASGD_CUDA_TRY(cudaGetLastError());
+    w->rd_dirty = false;
+  }
+  if (gr->exec) LASGD_CUDA_TRY(cudaGraphLaunch(gr->exec, w->compute));  // else the caller replays its own graph next
+  w->local_clock += gr->d_clock;
+  w->global_clock += gr->d_rounds;
+  if (gr->d_rounds & 1) w->snap_idx ^= 1;
+  if (gr->d_clock) {
+    w->mom_started = gr->mom_after;
+    w->delta_fresh = gr->delta_fresh_after;
+  }
+  for (int k = 0; k < K_KINDS; ++k) w->launches[k] += gr->d_launches[k];
+  for (int t = 0; t < LASGD_TAU_HIST; ++t) w->tau_hist[t] += gr->d_tau_hist[t];
+  return LASGD_OK;
+}
+
+extern "C" int lasgd_graph_destroy(lasgd_graph* gr) {
+  if (!gr) return LASGD_OK;
+  if (gr->exec) {
+    cudaStreamSynchronize(gr->w->compute);
+    cudaGraphExecDestroy(gr->exec);
+  }
+  delete gr;
+  return LASGD_OK;
+}
+
 extern "C" int lasgd_worker_destroy(lasgd_worker* w) {
   if (!w) return LASGD_OK;
   cudaStreamSynchronize(w->compute);
   if (w->side) cudaStreamSynchronize(w->side);
+  if (w->rd) cudaFree(w->rd);
+  if (w->lr_dev) cudaFree(w->lr_dev);
+  if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   for (auto& r : w->recs) {
     cudaEventDestroy(r.e0);
     cudaEventDestroy(r.e1);

@@ -102,6 +102,8 @@ class LASGDWorker:
         sgd = sgd or SgdConfig()
         sgd.validate()
         K._check(x, g)
+        if comm is not None and (comm.n != x.numel() or comm.dtype != x.dtype):
+            raise ValueError("communicator buffers do not match x")
         self.comm = comm
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
@@ -111,6 +113,8 @@ class LASGDWorker:
         self.adaptive = adaptive
         self.algo = algo
         self.timed = timed
+        self.sync = bool(sync)
+        self._graphs: list = []  # SyncGraphs point into the native worker: closed with it
         self.g = g
         self.compute = compute_stream if compute_stream is not None else torch.cuda.current_stream(x.device)
         self._local_clock = 0
@@ -154,6 +158,8 @@ class LASGDWorker:
         self._local_clock += 1
         if self._check_mode == "eager":
             self.state.check_finite()
+        if getattr(self, "_capturing", False):
+            return rc == 1  # inside a stream capture: the replay does the bookkeeping
         if rc == 1:
             self._rounds += 1
             if self._check_mode == "lazy" and self._rounds % self._check_every == 0:
@@ -161,6 +167,70 @@ class LASGDWorker:
                     self.state._finite.poll(self.state.x_local.numel())
             return True
         return False
+
+    # ------------------------------------------------------------------ graph replay
+    def _ensure_lr_table(self, clock_end: int) -> None:
+        """Device learning-rate table covering local clocks [0, clock_end)."""
+        if self.schedule is None:
+            if getattr(self, "_lr_len", 0) != 1:
+                table = (ctypes.c_double * 1)(float(self.lr))
+                N.check(N.lib().lasgd_worker_set_lr_table(self._h, table, 1), "lasgd_worker_set_lr_table")
+                self._lr_len = 1
+            return
+        if getattr(self, "_lr_len", 0) >= clock_end:
+            return
+        n = max(clock_end, 2 * getattr(self, "_lr_len", 0), 1024)
+        table = (ctypes.c_double * n)(*[lr_at(self.schedule, t) for t in range(n)])
+        N.check(N.lib().lasgd_worker_set_lr_table(self._h, table, n), "lasgd_worker_set_lr_table")
+        self._lr_len = n
+
+    def capture(self, grads, steps: Optional[int] = None) -> "SyncGraph":
+        """Capture ``steps`` local steps (default ``len(grads)``; a whole number of rounds),
+        step t reading gradient ``grads[t % len(grads)]``, as one CUDA graph.  Nothing runs
+        until ``replay()``; each replay advances the worker exactly as ``steps`` calls of
+        ``step()`` would, with bit-identical results (deterministic schedule, one rank)."""
+        grads = list(grads)
+        steps = len(grads) if steps is None else int(steps)
+        for t in grads:
+            K._check(self.state.x_local, t)
+        self._ensure_lr_table(self._local_clock + steps)
+        arr = (ctypes.c_void_p * steps)(*[grads[t % len(grads)].data_ptr() for t in range(steps)])
+        h = ctypes.c_void_p()
+        N.check(N.lib().lasgd_worker_graph_capture(self._h, steps, arr, ctypes.byref(h)), "lasgd_worker_graph_capture")
+        gr = SyncGraph(self, h, steps, grads)
+        self._graphs.append(gr)
+        return gr
+
+    def capture_with(self, fn, steps: int = 1, pool=None) -> "SyncGraph":
+        """Capture ``steps`` iterations of ``fn(t)`` (forward + backward writing the
+        gradient into ``self.g``) followed by ``step()`` into ONE CUDA graph on the compute
+        stream: the whole training step — minibatch compute, local step and round
+        boundary — replays as a single launch.  ``fn`` must have run eagerly before
+        (cuDNN autotuning, allocator warm-up) and must not synchronise with the host."""
+        self._ensure_lr_table(self._local_clock + steps)
+        graph = torch.cuda.CUDAGraph()
+        h = ctypes.c_void_p()
+        self._capturing = True
+        try:
+            with torch.cuda.graph(graph, stream=self.compute, pool=pool):
+                N.check(N.lib().lasgd_worker_capture_begin(self._h, ctypes.byref(h)), "lasgd_worker_capture_begin")
+                try:
+                    for t in range(steps):
+                        fn(t)
+                        self.step()
+                finally:
+                    rc_end = N.lib().lasgd_worker_capture_end(h)
+            N.check(rc_end, "lasgd_worker_capture_end")
+        except BaseException:
+            if h:
+                N.lib().lasgd_graph_destroy(h)
+            raise
+        finally:
+            self._capturing = False
+            self._local_clock -= steps  # step() advanced the Python clock during capture
+        gr = SyncGraph(self, h, steps, [self.g], external=graph)
+        self._graphs.append(gr)
+        return gr
 
     def drain(self, group=None) -> None:
         """Order the compute stream after the in-flight all-reduce.
@@ -242,8 +312,50 @@ class LASGDWorker:
         N.check(N.lib().lasgd_worker_reset_stats(self._h))
 
     def close(self) -> None:
+        for gr in getattr(self, "_graphs", ()):
+            gr.close()
         if getattr(self, "_h", None):
             N.lib().lasgd_worker_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SyncGraph:
+    """A captured run of worker steps (``LASGDWorker.capture``): ``replay()`` is one graph
+    launch on the worker's compute stream."""
+
+    def __init__(self, worker: LASGDWorker, handle, steps: int, grads, external=None):
+        self.worker = worker
+        self._h = handle
+        self.steps = steps
+        self.rounds = steps // worker.k if worker.sync else 0
+        self._keep = grads  # the captured gradient buffers
+        self.external = external  # capture_with: the torch graph holding fwd/bwd + the steps
+
+    def replay(self) -> None:
+        w = self.worker
+        w._ensure_lr_table(w._local_clock + self.steps)
+        N.check(N.lib().lasgd_graph_launch(self._h), "lasgd_graph_launch")
+        if self.external is not None:
+            with torch.cuda.stream(w.compute):
+                self.external.replay()
+        w._local_clock += self.steps
+        before = w._rounds
+        w._rounds += self.rounds
+        if w._check_mode == "eager":
+            w.state.check_finite()
+        elif w._check_mode == "lazy" and w._rounds // w._check_every != before // w._check_every:
+            with torch.cuda.stream(w.compute):
+                w.state._finite.poll(w.state.x_local.numel())
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.lib().lasgd_graph_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -88,7 +88,8 @@ def elastic_pull(x, snap, xbar, alpha: float, snap_next=None, nonfinite=None, st
 
 
 def finalize(x, z, delta, snap_next=None, nonfinite=None, stream=None) -> torch.Tensor:
-    """K4b: ``x = z + delta`` (optimizer.py:171), optional fused ``snap_next = x``."""
+    """K4b: ``x = z + delta`` (optimizer.py:171), optional fused ``snap_next = x``;
+    ``delta=None`` is a zero accumulator (x = z + 0)."""
     code, n = _check(x, z, delta, snap_next)
     N.check(N.lib().lasgd_finalize(_ptr(x), _ptr(snap_next), _ptr(z), _ptr(delta), n, code, _ptr(nonfinite),
                                    _stream(stream)), "finalize")

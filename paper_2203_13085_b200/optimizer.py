@@ -147,7 +147,7 @@ class NodeState:
         self.x_local = x_local
         self.snapshots = list(snapshots)
         self.snap_idx = 0
-        self.delta = delta
+        self._delta_buf = delta
         self.tau_i = 0
         self.local_clock = 0
         self.global_clock = 0
@@ -165,6 +165,16 @@ class NodeState:
     @property
     def x_snapshot(self) -> torch.Tensor:
         return self.snapshots[self.snap_idx]
+
+    @property
+    def delta(self) -> Optional[torch.Tensor]:
+        """The delta accumulator (optimizer.py:84).  A finalize resets it to zero
+        (optimizer.py:174) lazily: the next local step overwrites instead of adding, so
+        the reset costs no pass of its own.  Reading it here materialises the zeros."""
+        if self._delta_buf is not None and self._delta_fresh:
+            self._delta_buf.zero_()
+            self._delta_fresh = False
+        return self._delta_buf
 
     @property
     def nonfinite_counter(self) -> Optional[torch.Tensor]:
@@ -214,7 +224,7 @@ def sgd_local_step(state: NodeState, g, eta: float, tau_max: int) -> NodeState:
     g = g if isinstance(g, torch.Tensor) and g.is_cuda else as_device_vector(g, state.x_local.dtype,
                                                                              state.x_local.device)
     c = state.sgd
-    K.sgd_step(state.x_local, g.reshape(-1), eta, m=state.momentum_buf, delta=state.delta, momentum=c.momentum,
+    K.sgd_step(state.x_local, g.reshape(-1), eta, m=state.momentum_buf, delta=state._delta_buf, momentum=c.momentum,
                dampening=c.dampening, weight_decay=c.weight_decay, nesterov=c.nesterov,
                first_step=not state._momentum_started, delta_reset=state._delta_fresh,
                nonfinite=state.nonfinite_counter)
@@ -247,8 +257,11 @@ def lasgd_finalize_round(state: NodeState, z, num_nodes: int,
         if z is None:
             raise ValueError("collective reported complete but no center vector supplied")
         z = z if isinstance(z, torch.Tensor) and z.is_cuda else as_device_vector(z, x.dtype, x.device)
-        if state.delta is not None and (alpha is None or alpha == 1.0):
-            K.finalize(x, z, state.delta, snap_next=state.snapshots[nxt], nonfinite=state.nonfinite_counter)
+        if state._delta_buf is not None and (alpha is None or alpha == 1.0):
+            # no local step since the last finalize: delta is logically zero (optimizer.py:174),
+            # so new = z + 0 — the kernel reads no delta at all
+            d = None if state._delta_fresh else state._delta_buf
+            K.finalize(x, z, d, snap_next=state.snapshots[nxt], nonfinite=state.nonfinite_counter)
         else:
             a = 1.0 if alpha is None else float(alpha)
             if not 0.0 < a <= 1.0:
@@ -256,7 +269,7 @@ def lasgd_finalize_round(state: NodeState, z, num_nodes: int,
             K.elastic_pull(x, state.x_snapshot, z, a, snap_next=state.snapshots[nxt],
                            nonfinite=state.nonfinite_counter)
     state.snap_idx = nxt
-    state._delta_fresh = state.delta is not None
+    state._delta_fresh = state._delta_buf is not None
     state.tau_i = 0
     state.global_clock += 1
     state._after_op(boundary=True)

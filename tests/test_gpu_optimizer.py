@@ -200,3 +200,41 @@ def test_config1_loss_trajectory_within_1e4(golden_config1, alpha):
     ref = golden_config1[f"a{int(alpha * 100)}_losses"]
     rel = np.abs(losses - ref) / np.abs(ref)
     assert rel.max() < 1e-4, rel.max()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_finalize_twice_without_a_step_uses_zero_delta(dtype):
+    """optimizer.py:171-174: finalize resets delta to zero, so a second finalize with no
+    local step in between computes new = z + 0 (the poll-driven lasgd_node_tick loop hits
+    this when a round is already complete at the next tick), and delta reads back as 0."""
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    rng = np.random.default_rng(5)
+    n = 4099
+    x0 = rng.standard_normal(n).astype(dtype)
+    g = rng.standard_normal(n).astype(dtype)
+    z1 = rng.standard_normal(n).astype(dtype)
+    z2 = rng.standard_normal(n).astype(dtype)
+    st = L.NodeState.fresh(0, x0, mode="delta", dtype=tdt)
+    L.sgd_local_step(st, torch.from_numpy(g).cuda(), 0.1, tau_max=4)
+    L.lasgd_finalize_round(st, torch.from_numpy(z1).cuda(), 2)
+    L.lasgd_finalize_round(st, torch.from_numpy(z2).cuda(), 2)  # no step in between
+    torch.cuda.synchronize()
+    want = z2 + np.zeros(n, dtype)  # blend(1, z, 1, zeros) == z + 0
+    assert same_bits(st.x_local.cpu().numpy(), want)
+    assert same_bits(st.x_snapshot.cpu().numpy(), want)
+    assert not st.delta.cpu().numpy().any()
+    # the accumulator is live again after the next step: delta = 0 + (-eta)*g
+    L.sgd_local_step(st, torch.from_numpy(g).cuda(), 0.1, tau_max=4)
+    torch.cuda.synchronize()
+    assert same_bits(st.delta.cpu().numpy(), np.zeros(n, dtype) + dtype(-0.1) * g)
+
+
+def test_worker_rejects_communicator_of_another_shape():
+    comm = L.P2PCommunicator(1000)
+    x = torch.zeros(999, device="cuda")
+    with pytest.raises(ValueError, match="communicator"):
+        L.LASGDWorker(x, torch.zeros_like(x), comm=comm, lr=0.1)
+    xd = torch.zeros(1000, device="cuda", dtype=torch.float64)
+    with pytest.raises(ValueError, match="communicator"):
+        L.LASGDWorker(xd, torch.zeros_like(xd), comm=comm, lr=0.1)
+    comm.close()
