@@ -278,11 +278,30 @@ def virtual_rank_kernels(n, dev, stream, hbm_peak, traffic, reps=10):
     return out
 
 
-def cpu_reference_run(n_full, P, k, steps, warmup, threads, target_step_s=1.0):
-    """The reference algorithm on the host (oracle/ C port, f64 like the reference):
-    per step every worker runs sgd_local_step (x and delta, optimizer.py:145-146);
-    every k steps the ring mean of the P snapshots (collective.py:154-203) and P
-    finalizes new = z + delta (optimizer.py:171).  Returns (seconds/step, sample n)."""
+def fused_algo_name(P, n):
+    """The fused-round algorithm our arm runs at world size P for n fp32 parameters
+    (lasgd_comm_resolve_fused_algo, csrc/lasgd_comm.cu), so both arms record one config."""
+    if P <= 1:
+        return "oneshot"
+    b = 4 * n
+    if P == 2:
+        return "push" if b >= (32 << 20) else "oneshot"
+    cutoff = (8 << 20) if P <= 4 else (1 << 20)
+    return "oneshot" if b <= cutoff else "push"
+
+
+def cpu_reference_run(n_full, P, k, steps, warmup, threads, target_step_s=1.0, rule="matched", alpha=1.0):
+    """The LASGD sync path on the host through the C restatement in oracle/ (f64 like the
+    reference, pinned to its outputs by tests/test_c_oracle.py), P workers in-process like
+    LoopbackTransport, on a bounded sample of the parameter vector.
+
+    rule "matched": the GPU arm's per-step work — every worker's local step with Nesterov
+      momentum 0.9 and weight decay 1e-4 (oracle_sgd_momentum); every k steps the ring
+      mean of the P snapshots (collective.py:154-203), the elastic pull writing the next
+      snapshot (P > 1) or the snapshot copy (P = 1, optimizer.py:168-169).
+    rule "reference": the reference's own rule — sgd_local_step on x and delta
+      (optimizer.py:145-146), every k steps the ring mean and new = z + delta (:171).
+    Returns (seconds per step, sample n)."""
     import numpy as np
 
     from oracle import c_oracle as C
@@ -293,36 +312,59 @@ def cpu_reference_run(n_full, P, k, steps, warmup, threads, target_step_s=1.0):
     xa, xb, da, db, g = (np.random.default_rng(i).standard_normal(probe_n) for i in range(5))
     t0 = time.perf_counter()
     for _ in range(3):
-        C.sgd_delta(xb, db, xa, da, g, 0.1)
+        if rule == "matched":
+            C.sgd_momentum(xa, g, da, 0.1, 0.9, 0.0, 1e-4, True, False)
+        else:
+            C.sgd_delta(xb, db, xa, da, g, 0.1)
     per_elem = (time.perf_counter() - t0) / 3 / probe_n
-    per_step_elem = per_elem * P * (1.0 + 1.5 / k)  # sgd + amortised mean/finalize
+    per_step_elem = per_elem * P * (1.0 + 1.5 / k)  # local step + amortised mean / pull
     n = int(min(n_full, max(1 << 16, target_step_s / per_step_elem)))
     mem = _mem_available()
     if mem:
-        n = int(min(n, mem * 0.5 / (8 * (5 * P + 2))))
+        n = int(min(n, mem * 0.5 / (8 * (6 * P + 2))))
     rng = np.random.default_rng(0)
     g = rng.standard_normal(n) * 1e-2
-    xs = [[rng.standard_normal(n) * 0.1, np.empty(n)] for _ in range(P)]
-    ds = [[np.zeros(n), np.empty(n)] for _ in range(P)]
-    snaps = [x[0].copy() for x in xs]
     z = np.empty(n)
-    cur = [0] * P
-    reset = [True] * P
+    if rule == "matched":
+        xs = [rng.standard_normal(n) * 0.1 for _ in range(P)]
+        ms = [np.zeros(n) for _ in range(P)]
+        snaps = [[x.copy() for x in xs], [np.empty(n) for _ in range(P)]]
+        st = {"cur": 0, "first": True}
 
-    def one_step(t):
-        for r in range(P):
-            c = cur[r]
-            C.sgd_delta(xs[r][1 - c], ds[r][1 - c], xs[r][c], ds[r][c], g, 0.1, delta_reset=reset[r])
-            cur[r] = 1 - c
-            reset[r] = False
-        if (t + 1) % k == 0:
-            if P > 1:
-                C.ring_mean([z], snaps)
-                for r in range(P):
-                    C.finalize(xs[r][cur[r]], z, ds[r][cur[r]])
-                    snaps[r] = xs[r][cur[r]]  # x_local = x_snapshot = new (aliased, optimizer.py:172-173)
+        def one_step(t):
             for r in range(P):
-                reset[r] = True
+                C.sgd_momentum(xs[r], g, ms[r], 0.1, 0.9, 0.0, 1e-4, True, st["first"])
+            st["first"] = False
+            if (t + 1) % k == 0:
+                c = st["cur"]
+                if P > 1:
+                    C.ring_mean([z], snaps[c])
+                    for r in range(P):
+                        C.pull(xs[r], snaps[1 - c][r], snaps[c][r], z, alpha)
+                else:
+                    C.copy(snaps[1 - c][0], xs[0])
+                st["cur"] = 1 - c
+    else:
+        xs = [[rng.standard_normal(n) * 0.1, np.empty(n)] for _ in range(P)]
+        ds = [[np.zeros(n), np.empty(n)] for _ in range(P)]
+        snaps = [x[0].copy() for x in xs]
+        cur = [0] * P
+        reset = [True] * P
+
+        def one_step(t):
+            for r in range(P):
+                c = cur[r]
+                C.sgd_delta(xs[r][1 - c], ds[r][1 - c], xs[r][c], ds[r][c], g, 0.1, delta_reset=reset[r])
+                cur[r] = 1 - c
+                reset[r] = False
+            if (t + 1) % k == 0:
+                if P > 1:
+                    C.ring_mean([z], snaps)
+                    for r in range(P):
+                        C.finalize(xs[r][cur[r]], z, ds[r][cur[r]])
+                        snaps[r] = xs[r][cur[r]]  # x_local = x_snapshot = new (aliased, optimizer.py:172-173)
+                for r in range(P):
+                    reset[r] = True
 
     for t in range(warmup):
         one_step(t)
@@ -331,6 +373,38 @@ def cpu_reference_run(n_full, P, k, steps, warmup, threads, target_step_s=1.0):
         one_step(warmup + t)
     dt = (time.perf_counter() - t0) / steps
     return dt, n
+
+
+def stock_reference_run(n_full, target_s=10.0):
+    """The UNMODIFIED reference package (pip-installed into baseline/_ref, single-threaded
+    numpy like the reference) timing its own sgd_local_step + lasgd_finalize_round
+    (optimizer.py:136-178) for one worker at P = 1 on a bounded sample.  Returns
+    (seconds per step at the full size, sample n) or None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "lasgd")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import numpy as np
+    from lasgd.optimizer import NodeState, lasgd_finalize_round, sgd_local_step
+    from lasgd.params import ParamVector
+
+    n = min(n_full, 1 << 22)
+    rng = np.random.default_rng(0)
+    st = NodeState.fresh(0, ParamVector(rng.standard_normal(n) * 0.1))
+    g = ParamVector(rng.standard_normal(n) * 1e-2)
+    sgd_local_step(st, g, 0.1, tau_max=1)  # warm-up
+    lasgd_finalize_round(st, None, 1)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        sgd_local_step(st, g, 0.1, tau_max=1)
+        lasgd_finalize_round(st, None, 1)
+        reps += 1
+        if time.perf_counter() - t0 > target_s / 4 or reps >= 50:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return dt * n_full / n, n
 
 
 def _mem_available():
@@ -355,26 +429,41 @@ def cpu_model():
 
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """The reference's algorithm on the host cores, on our arm's workload and config: the
+    work-matched rule (value) and the reference's own plain-SGD + delta rule (extra)."""
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
     P = world
     full = MODELS[args.model]["params"]
-    dt, n = cpu_reference_run(full, P, args.sync_period, max(1, args.steps), max(1, args.warmup), threads)
+    dt, n = cpu_reference_run(full, P, args.sync_period, max(1, args.steps), max(1, args.warmup), threads,
+                              rule="matched", alpha=args.alpha)
     scale = n / full  # elementwise work is linear in n: full-size step time = dt / scale
     value = P * args.batch / (dt / scale)
-    sample = (f"reference algorithm (f64, delta bookkeeping, ring-order mean, {P} workers in-process) on "
-              f"{n} of {full} parameters per step, scaled linearly to the full vector; "
-              "the reference has no momentum, so its local step is the plain sgd_local_step; "
-              f"{args.steps} timed steps after {args.warmup} warm-up; host: {cpu_model()}")
+    dt_r, n_r = cpu_reference_run(full, P, args.sync_period, max(1, args.steps // 4), 1, threads, rule="reference",
+                                  target_step_s=0.5)
+    sample = (f"oracle/ C port (f64, pinned to the reference by tests/test_c_oracle.py), {P} workers in-process, "
+              f"{threads} threads: per step every worker's Nesterov/weight-decay local step, every "
+              f"{args.sync_period} steps the ring-order mean + elastic pull + next snapshot (the GPU arm's work); "
+              f"{n} of {full} parameters per step, scaled linearly; {args.steps} timed steps after {args.warmup} "
+              f"warm-up; host {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / scale * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, world),
+        "config": config_dict(args, world, fused_algo_name(world, full)),
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "port", "sample": sample},
+        "reference_rule": {"value": P * args.batch / (dt_r * full / n_r), "unit": "images/s", "cores": threads,
+                           "sample": f"the reference's own rule (plain sgd_local_step + delta, finalize z + delta), "
+                                     f"{n_r} of {full} parameters, scaled"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    stock = stock_reference_run(full)
+    if stock is not None:
+        line["stock_reference"] = {
+            "value": args.batch / stock[0], "unit": "images/s", "cores": 1,
+            "sample": f"unmodified reference package (baseline/_ref) sgd_local_step + lasgd_finalize_round, one "
+                      f"worker, numpy single-threaded, {stock[1]} of {full} parameters, scaled"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -651,11 +740,12 @@ def main():
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        dt, ns = cpu_reference_run(n, 1, args.sync_period, 10, 2, threads, target_step_s=0.5)
+        dt, ns = cpu_reference_run(n, 1, args.sync_period, 10, 2, threads, target_step_s=0.5, alpha=args.alpha)
         scale = ns / n
         cpu_base = {"value": args.batch / (dt / scale), "unit": "images/s", "cores": threads, "kind": "port",
-                    "sample": f"reference algorithm (f64 C port of oracle/, 1 worker, sgd_local_step + finalize) on "
-                              f"{ns} of {n} parameters, 10 steps, scaled linearly; host {cpu_model()}"}
+                    "sample": f"oracle/ C port (f64, pinned by tests/test_c_oracle.py), 1 worker, the GPU arm's "
+                              f"work (Nesterov/wd local step + next snapshot) on {ns} of {n} parameters, 10 steps, "
+                              f"scaled linearly; host {cpu_model()}"}
 
     if rank == 0:
         line = {
@@ -663,10 +753,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "host_issue_ms_per_step": host_issue_ms / args.steps,
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(config_dict(args, world, {1: "oneshot", 2: "twoshot", 3: "push"}.get(
+            "config": config_dict(args, world, {1: "oneshot", 2: "twoshot", 3: "push"}.get(
                 comm.resolve_fused_algo(algo_code) if comm is not None else 1)),
-                timed_region=("one CUDA-graph replay of the K steps (LASGDWorker.capture), behind a hold kernel"
-                              if graph is not None else "K worker steps issued one by one, behind a hold kernel")),
+            "timed_region": ("one CUDA-graph replay of the K steps (LASGDWorker.capture), behind a hold kernel"
+                             if graph is not None else "K worker steps issued one by one, behind a hold kernel"),
             "roofline": roofline,
             "cpu_baseline": cpu_base,
             "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,

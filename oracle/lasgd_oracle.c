@@ -1,6 +1,7 @@
 /*
  * CPU ORACLE (C restatement) of the LASGD parameter-synchronisation path.
- * TEST INFRASTRUCTURE ONLY: used by tests/ as a second checker and by bench.py
+ * TEST INFRASTRUCTURE ONLY: pinned by tests/test_c_oracle.py (reference goldens in f64,
+ * the Python oracle bit for bit in f32); used by bench.py
  * as the timed CPU baseline ("kind": "port") / the `--impl reference` arm.
  * The product path never links or loads this library.
  *

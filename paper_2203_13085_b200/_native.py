@@ -146,6 +146,7 @@ SIGNATURES = {
     "lasgd_comm_bytes_per_node": (ctypes.c_ulonglong, [_P, _I]),
     "lasgd_comm_resolve_algo": (_I, [_P, _I]),
     "lasgd_comm_resolve_fused_algo": (_I, [_P, _I]),
+    "lasgd_resolve_fused_algo_for": (_I, [_I, _SZ]),
     "lasgd_comm_peers_ahead": (_I, [_P, ctypes.c_ulonglong]),
     "lasgd_comm_set_gate": (_I, [_P, _I]),
     "lasgd_comm_set_nblocks": (_I, [_P, _I]),

@@ -444,6 +444,10 @@ extern "C" int lasgd_comm_resolve_algo(lasgd_comm* c, int algo) {
   return resolve_algo(algo, c->world, c->n * c->elem);
 }
 
+extern "C" int lasgd_resolve_fused_algo_for(int world, size_t bytes) {
+  return resolve_fused_algo(LASGD_ALGO_AUTO, world, bytes);
+}
+
 extern "C" int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   return resolve_fused_algo(algo, c->world, c->n * c->elem);

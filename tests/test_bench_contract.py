@@ -45,3 +45,28 @@ def test_our_arm_line():
     assert e["h2d_bytes_per_step"] == 4 * d["config"]["params"] and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 5  # one fused round per step at N = 1
     assert d["clocks"] is None or {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_reference_arm_records_our_config():
+    """Both arms name the same config (the driver compares them): the reference arm's
+    fused_round_algo is what our arm's communicator resolves at that world size."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert bench.fused_algo_name(1, 25_557_032) == "oneshot"
+    assert bench.fused_algo_name(2, 25_557_032) == "push"
+    assert bench.fused_algo_name(2, 3_504_872) == "oneshot"
+    assert bench.fused_algo_name(4, 25_557_032) == "push"
+    assert bench.fused_algo_name(4, 1_000_000) == "oneshot"
+    assert bench.fused_algo_name(8, 3_504_872) == "push"
+
+
+def test_fused_algo_name_matches_the_communicator():
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2203_13085_b200 import _native as N
+
+    for P in range(2, 9):
+        for n in (262_144, 2_097_152, 3_504_872, 11_181_642, 25_557_032):
+            got = N.lib().lasgd_resolve_fused_algo_for(P, 4 * n)
+            assert {1: "oneshot", 2: "twoshot", 3: "push"}[got] == bench.fused_algo_name(P, n), (P, n)
