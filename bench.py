@@ -67,8 +67,11 @@ def parse():
     ap.add_argument("--pipeline", choices=["overlap", "fused"], default="fused",
                     help="overlap: K5 | K4 | K2/K3 on a side stream; fused: one K7 pass per round boundary")
     ap.add_argument("--fused-nblocks", type=int, default=0, help="CTAs of the fused kernel (0 = 2 per SM)")
-    ap.add_argument("--train-steps", type=int, default=30)
+    ap.add_argument("--train-block", type=int, default=10, help="training steps per timed block")
+    ap.add_argument("--train-reps", type=int, default=5, help="interleaved repetitions of every training leg")
     ap.add_argument("--train-warmup", type=int, default=4)
+    ap.add_argument("--flat-align", type=int, default=256, help="byte alignment of every tensor in the flat buffer")
+    ap.add_argument("--bucket-mb", type=int, default=25, help="gradient bucket size of the bucketed SGD-AR / DDP legs")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="training leg: eager fwd/bwd instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -777,9 +780,30 @@ def main():
     return 0
 
 
+def _paired_stats(diffs):
+    """Median and 95% t-interval of the mean of paired per-block differences."""
+    import statistics as st
+
+    k = len(diffs)
+    mean = sum(diffs) / k
+    sd = st.stdev(diffs) if k > 1 else 0.0
+    tq = {2: 12.71, 3: 4.30, 4: 3.18, 5: 2.78, 6: 2.57, 7: 2.45, 8: 2.36, 9: 2.31, 10: 2.26}.get(k, 2.0)
+    hw = tq * sd / k ** 0.5
+    return {"median": st.median(diffs), "mean": mean, "ci95": [mean - hw, mean + hw], "ci95_halfwidth": hw,
+            "blocks": k}
+
+
 def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barrier, max_over_ranks):
     """Real training step (forward/backward in PyTorch, bf16 autocast, channels_last) with
-    the sync path under each schedule, and with sync disabled (the no-sync ceiling)."""
+    the sync path under each schedule, and with sync disabled (the no-sync ceiling).
+
+    The legs run interleaved in blocks (every leg once per repetition, in the same order)
+    and each leg's exposed sync time is the paired per-block difference against the
+    no-sync leg of the same repetition: median and 95% interval over the repetitions.
+    Graphed legs (forward/backward replayed as a CUDA graph; at N=1 the local step and
+    round boundary are captured into the same graph) compare with the graphed no-sync
+    leg; eager legs (the bucketed SGD-AR, whose buckets launch from autograd hooks, and
+    NCCL DDP) with the eager no-sync leg."""
     import torch
     import torchvision
 
@@ -789,13 +813,16 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     torch.backends.cudnn.benchmark = True
     model = getattr(torchvision.models, spec["ctor"])(num_classes=spec["classes"]).to(dev)
     model = model.to(memory_format=torch.channels_last)
-    flat = L.FlatParams(model, channels_last=True)
-    assert flat.numel == spec["params"], (flat.numel, spec["params"])
+    flat = L.FlatParams(model, channels_last=True, align_bytes=args.flat_align)
+    assert flat.n_params == spec["params"], (flat.n_params, spec["params"])
+    tcomm = comm
     if comm is not None:
-        # identical x0 on every rank (Algorithm 1 line 1)
         import torch.distributed as dist
 
+        # identical x0 on every rank (Algorithm 1 line 1)
         dist.broadcast(flat.x, 0)
+        if comm.n != flat.numel:  # 256-B aligned tensors: the flat vector carries padding
+            tcomm = L.P2PCommunicator(flat.numel, nblocks=args.nblocks, timeout_s=60.0)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     hw = spec["image"]
@@ -808,100 +835,197 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
             loss = lossf(model(images), labels)
         loss.backward()
 
-    if args.no_graphs:
-        def fwd_bwd():
-            flat.zero_grad()
-            fwd_bwd_eager()
-    else:
-        fwd_bwd = L.GraphedStep(flat, fwd_bwd_eager)  # one CUDA graph per gradient buffer
+    def fwd_bwd_zero():
+        flat.zero_grad()
+        fwd_bwd_eager()
 
-    def train(steps, warm, **wkw):
-        with torch.cuda.stream(compute):
-            w = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=args.sync_period, alpha=args.alpha, mode="pull",
-                              sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
-                              fused_nblocks=args.fused_nblocks, **wkw)
+    graphed = not args.no_graphs
+    fwd_bwd = L.GraphedStep(flat, fwd_bwd_eager) if graphed else fwd_bwd_zero
+    own_g = flat.g
+
+    # ---- legs: make() -> (one_step, finish, close); one_step runs one training step on `compute`
+    cached = {}  # N=1 graphed LASGD legs and DDP live across blocks (graphs captured once)
+
+    def lasgd_leg(**wkw):
+        key = repr(sorted(wkw.items()))
+
+        def make():
+            flat.bind_grads(own_g)
+            one_graph = None
+            if key in cached:
+                w, one_graph = cached[key]
+            else:
+                w = L.LASGDWorker(flat.x, flat.g, comm=tcomm, sync_period=args.sync_period, alpha=args.alpha,
+                                  mode="pull", sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
+                                  fused_nblocks=args.fused_nblocks, **wkw)
+                if graphed and world == 1 and not wkw.get("adaptive"):
+                    # one CUDA graph: zero_grad + forward + backward + local step (+ round boundary)
+                    fwd_bwd()  # the fwd/bwd graph exists: cuDNN autotuned, the shared pool warm
+                    k = args.sync_period if wkw.get("sync", True) else 1
+                    one_graph = w.capture_with(lambda t: (flat.zero_grad(), fwd_bwd_eager()), steps=k,
+                                               pool=fwd_bwd.pool)
+                    cached[key] = (w, one_graph)
+            state = {"t": 0}
 
             def one():
+                if one_graph is not None:
+                    if state["t"] % one_graph.steps == 0:
+                        one_graph.replay()
+                    state["t"] += 1
+                    return
                 fwd_bwd()
                 w.step()
 
-            for _ in range(warm):
-                one()
-            w.drain()
-        torch.cuda.synchronize()
-        barrier()
-        w.reset_records()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(compute):
-            a.record(compute)
-            for _ in range(steps):
-                one()
-            w.drain()
-            b.record(compute)
-        torch.cuda.synchronize()
-        ms = max_over_ranks(a.elapsed_time(b)) / steps
-        hist = dict(w.tau_hist)
-        w.close()
-        return ms, hist
+            def finish():
+                w.drain()
+                return w
 
-    def train_sgd_ar(steps, warm, nccl):
+            return one, finish, (lambda: None) if key in cached else w.close
+        return make
+
+    def sgd_ar_leg(kind):
         import torch.distributed as dist
 
         from paper_2203_13085_b200 import kernels as K
 
-        with torch.cuda.stream(compute):
-            if nccl:
+        def make():
+            if kind == "nccl":
                 flat.bind_grads(own_g)
                 m = torch.empty_like(flat.x)
                 clock = [0]
 
-                def update():
+                def one():
+                    fwd_bwd()
                     dist.all_reduce(flat.g, op=dist.ReduceOp.AVG)
                     K.sgd_step(flat.x, flat.g, lr, m=m, momentum=sgd.momentum, weight_decay=sgd.weight_decay,
                                nesterov=sgd.nesterov, first_step=clock[0] == 0, stream=compute)
                     clock[0] += 1
-            else:
-                update = L.SGDARWorker(flat.x, comm=comm, sgd=sgd, lr=lr, compute_stream=compute, flat=flat).step
+                return one, lambda: None, lambda: None
+            if kind == "p2p":
+                w = L.SGDARWorker(flat.x, comm=tcomm, sgd=sgd, lr=lr, compute_stream=compute, flat=flat)
+
+                def one():
+                    fwd_bwd()
+                    w.step()
+                return one, lambda: None, lambda: flat.bind_grads(own_g)
+            if kind == "bucketed":
+                w = L.BucketedSGDARWorker(flat, tcomm, sgd=sgd, lr=lr, bucket_bytes=args.bucket_mb << 20,
+                                          compute_stream=compute)
+
+                def one():
+                    fwd_bwd_zero()
+                    w.step()
+                return one, lambda: None, lambda: (w.close(), flat.bind_grads(own_g))
+            # torch DDP over NCCL (bucketed, overlapped with backward), our K5 after it
+            from torch.nn.parallel import DistributedDataParallel as DDP
+
+            flat.bind_grads(own_g)
+            if "ddp" not in cached:
+                cached["ddp"] = DDP(model, device_ids=[dev.index], bucket_cap_mb=args.bucket_mb,
+                                    broadcast_buffers=False, gradient_as_bucket_view=False)
+            ddp = cached["ddp"]
+            m = torch.empty_like(flat.x)
+            clock = [0]
 
             def one():
-                fwd_bwd()
-                update()
+                flat.zero_grad()
+                with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+                    loss = lossf(ddp(images), labels)
+                loss.backward()
+                K.sgd_step(flat.x, flat.g, lr, m=m, momentum=sgd.momentum, weight_decay=sgd.weight_decay,
+                           nesterov=sgd.nesterov, first_step=clock[0] == 0, stream=compute)
+                clock[0] += 1
+            return one, lambda: None, lambda: None
+        return make
 
-            for _ in range(warm):
+    def nosync_eager_leg():
+        from paper_2203_13085_b200 import kernels as K
+
+        def make():
+            flat.bind_grads(own_g)
+            m = torch.empty_like(flat.x)
+            clock = [0]
+
+            def one():
+                fwd_bwd_zero()
+                K.sgd_step(flat.x, flat.g, lr, m=m, momentum=sgd.momentum, weight_decay=sgd.weight_decay,
+                           nesterov=sgd.nesterov, first_step=clock[0] == 0, stream=compute)
+                clock[0] += 1
+            return one, lambda: None, lambda: None
+        return make
+
+    legs = {"nosync": (lasgd_leg(sync=False), "nosync"),
+            "fused": (lasgd_leg(pipeline="fused"), "nosync"),
+            "overlap": (lasgd_leg(pipeline="overlap"), "nosync"),
+            "overlap_adaptive": (lasgd_leg(pipeline="overlap", adaptive=True, tau_max=5), "nosync")}
+    if tcomm is not None:
+        legs.update({"sgd_ar": (sgd_ar_leg("p2p"), "nosync"), "sgd_ar_nccl": (sgd_ar_leg("nccl"), "nosync"),
+                     "nosync_eager": (nosync_eager_leg(), "nosync_eager"),
+                     "sgd_ar_bucketed": (sgd_ar_leg("bucketed"), "nosync_eager"),
+                     "ddp_nccl": (sgd_ar_leg("ddp"), "nosync_eager")})
+    times = {k: [] for k in legs}
+    hists = {}
+    B, R = args.train_block, args.train_reps
+    with torch.cuda.stream(compute):
+        for name, (make, _) in legs.items():  # one untimed pass per leg: graphs, cuDNN, NCCL buckets
+            one, finish, close = make()
+            for _ in range(args.train_warmup):
                 one()
-        torch.cuda.synchronize()
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(compute):
-            a.record(compute)
-            for _ in range(steps):
-                one()
-            b.record(compute)
-        torch.cuda.synchronize()
-        return max_over_ranks(a.elapsed_time(b)) / steps
+            finish()
+            close()
+    torch.cuda.synchronize()
+    for rep in range(R):
+        for name, (make, _) in legs.items():
+            with torch.cuda.stream(compute):
+                one, finish, close = make()
+                for _ in range(2):
+                    one()
+                w = finish()
+            torch.cuda.synchronize()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(compute):
+                if w is not None and hasattr(w, "reset_records"):
+                    w.reset_records()
+                a.record(compute)
+                for _ in range(B):
+                    one()
+                finish()
+                b.record(compute)
+            torch.cuda.synchronize()
+            times[name].append(max_over_ranks(a.elapsed_time(b)) / B)
+            if w is not None and hasattr(w, "tau_hist"):
+                for t, c in w.tau_hist.items():
+                    hists.setdefault(name, {}).setdefault(str(t), 0)
+                    hists[name][str(t)] += c
+            close()
+            barrier()
+    for key, v in list(cached.items()):
+        if key != "ddp":
+            v[0].close()
+    cached.clear()
+    if tcomm is not None and tcomm is not comm:
+        tcomm.close()
+    flat.bind_grads(own_g)
+
+    import statistics as st
 
     out = {"model": f"{spec['ctor']} (torchvision, random init, {hw}x{hw}, {spec['classes']} classes)",
-           "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params", "steps": args.train_steps,
-           "fwd_bwd": "eager" if args.no_graphs else "cuda_graph (zero_grad+fwd+bwd captured once per gradient buffer)"}
-    t_nosync, _ = train(args.train_steps, args.train_warmup, sync=False)
-    runs = {"fused": dict(pipeline="fused"), "overlap": dict(pipeline="overlap"),
-            "overlap_adaptive": dict(pipeline="overlap", adaptive=True, tau_max=5)}
-    for name, kw in runs.items():
-        t, hist = train(args.train_steps, args.train_warmup, **kw)
-        out[name] = {"images_per_s": world * args.batch / (t / 1e3), "ms_per_step": t,
-                     "exposed_sync_ms_per_step": t - t_nosync, "exposed_sync_frac": (t - t_nosync) / t}
-        if kw.get("adaptive"):
-            out[name]["tau_histogram"] = {str(k): v for k, v in sorted(hist.items())}
-    out["nosync"] = {"images_per_s": world * args.batch / (t_nosync / 1e3), "ms_per_step": t_nosync}
-    if comm is not None:
-        # SGD-AR (optimizer.py:214-242): gradient mean every step, on the same P2P
-        # all-reduce (grads written by backward into the registered slots) and on NCCL
-        own_g = flat.g
-        for name in ("sgd_ar", "sgd_ar_nccl"):
-            t = train_sgd_ar(args.train_steps, args.train_warmup, name == "sgd_ar_nccl")
-            out[name] = {"images_per_s": world * args.batch / (t / 1e3), "ms_per_step": t,
-                         "exposed_sync_ms_per_step": t - t_nosync, "exposed_sync_frac": (t - t_nosync) / t}
-        flat.bind_grads(own_g)
+           "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params",
+           "flat_align_bytes": args.flat_align, "blocks": f"{R} repetitions x {B} steps per leg, legs interleaved",
+           "fwd_bwd": ("cuda_graph (N=1: zero_grad+fwd+bwd+local step+round in one graph; N>1: fwd/bwd graph, "
+                       "sync launches after it)" if graphed else "eager")}
+    for name, (_, base) in legs.items():
+        med = st.median(times[name])
+        e = {"images_per_s": world * args.batch / (med / 1e3), "ms_per_step": med, "ms_per_step_blocks": times[name]}
+        if name != base:
+            d = _paired_stats([t - b for t, b in zip(times[name], times[base])])
+            e.update({"exposed_sync_ms_per_step": d["median"], "exposed_sync_ci95_ms": d["ci95"],
+                      "exposed_sync_ci95_halfwidth_ms": d["ci95_halfwidth"],
+                      "exposed_sync_frac": d["median"] / med, "baseline_leg": base})
+        if name in hists:
+            e["tau_histogram"] = hists[name]
+        out[name] = e
     main = out[args.pipeline]
     out["images_per_s_lasgd"] = main["images_per_s"]
     out["images_per_s_nosync"] = out["nosync"]["images_per_s"]

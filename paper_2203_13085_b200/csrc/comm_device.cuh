@@ -25,6 +25,11 @@ struct CommArgs {
   char* xbar[kMaxR];
   uint32_t* pad[kMaxR];
   size_t n;
+  // a launch over the sub-range [range_off, range_off + n) of an n_glob-element vector
+  // (bucketed SGD-AR) sums every element in the ring order of its chunk of the WHOLE
+  // vector, so bucketing leaves the mean bit-identical; n_glob == 0: the launch is the
+  // whole vector
+  size_t range_off, n_glob;
   int rank;
   int nblocks;
   uint32_t epoch;
@@ -76,6 +81,16 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __device__ __forceinline__ size_t chunk_bound(size_t n, int P, int c) {
   const size_t base = n / (size_t)P, rem = n % (size_t)P;
   return (size_t)c * base + ((size_t)c < rem ? (size_t)c : rem);
+}
+
+// Chunk bound c of the whole vector in this launch's local coordinates (clamped to
+// [0, n]): chunk_of over these bounds gives the ring-order start of a sub-range element.
+__device__ __forceinline__ size_t chunk_bound_local(const CommArgs& a, int P, int c) {
+  if (a.n_glob == 0) return chunk_bound(a.n, P, c);
+  const size_t g = chunk_bound(a.n_glob, P, c);
+  if (g <= a.range_off) return 0;
+  const size_t l = g - a.range_off;
+  return l < a.n ? l : a.n;
 }
 
 template <int P>

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
     const size_t n = a.n;
     size_t bnd[P + 1];
 #pragma unroll
-    for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound(n, P, c);
+    for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound_local(a, P, c);
     const T* src[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);

@@ -5,8 +5,12 @@
 
 namespace lasgd {
 
-template <int P>
-constexpr int unroll_for() { return P <= 2 ? 8 : (P <= 4 ? 4 : 2); }
+// packs in flight per thread of the two-shot reduce-scatter / all-gather, sized so the
+// loaded data fits the 128 registers of __launch_bounds__(256, 2) without spills
+template <typename T, int P>
+constexpr int unroll_for() { return (P <= 2 ? 8 : (P <= 4 ? 4 : 2)) / (sizeof(T) == 8 && P <= 4 ? 2 : 1); }
+template <typename T, int P>
+constexpr int ag_unroll() { return (sizeof(T) == 8 || P >= 5) ? 4 : 8; }
 template <int P>
 constexpr int oneshot_unroll() { return P <= 2 ? 4 : (P <= 4 ? 2 : 1); }  // <= 128 regs, no spills
 
@@ -17,7 +21,7 @@ int launch_allreduce(int algo, int P, const CommArgs& a, dim3 grid, int threads,
     if (algo == LASGD_ALGO_ONESHOT) return launch_kernel(false, k_oneshot<T, PP, VIRTUAL, oneshot_unroll<PP>()>, \
                                                          grid, threads, s, a);                            \
     {                                                                                                     \
-      auto kern = k_twoshot<T, PP, VIRTUAL, unroll_for<PP>(), 8>;                                         \
+      auto kern = k_twoshot<T, PP, VIRTUAL, unroll_for<T, PP>(), ag_unroll<T, PP>()>;                                         \
       CommArgs aa = a;                                                                                    \
       if (!VIRTUAL) {                                                                                     \
         const int cap = coop_capacity(kern, threads);                                                     \

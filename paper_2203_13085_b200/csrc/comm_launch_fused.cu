@@ -12,7 +12,7 @@ int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, in
 #define LASGD_FCASE(PP)                                                                             \
   case PP:                                                                                          \
     if (algo == LASGD_ALGO_TWOSHOT && PP > 1) {                                                     \
-      auto kern = k_fused_twoshot<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)>;                               \
+      auto kern = k_fused_twoshot<T, PP, VIRTUAL, (PP <= 4 && sizeof(T) == 4 ? 2 : 1)>;                               \
       CommArgs aa = a;                                                                              \
       if (!VIRTUAL) {                                                                               \
         const int cap = coop_capacity(kern, threads);                                               \
@@ -21,7 +21,7 @@ int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, in
       }                                                                                             \
       return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                \
     }                                                                                               \
-    return launch_kernel(false, k_fused_round<T, PP, VIRTUAL, (PP <= 2 ? 2 : 1)>, grid, threads, s, \
+    return launch_kernel(false, k_fused_round<T, PP, VIRTUAL, (PP <= 2 && (sizeof(T) == 4 || PP == 2) ? 2 : 1)>, grid, threads, s, \
                          a, f);
   switch (P) {
     LASGD_FCASE(1)

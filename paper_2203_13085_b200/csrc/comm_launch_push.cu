@@ -9,7 +9,7 @@ template <typename T, bool VIRTUAL>
 int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s) {
 #define LASGD_PCASE(PP)                                                                             \
   case PP: {                                                                                        \
-    auto kern = k_push_round<T, PP, VIRTUAL, (PP <= 4 ? 2 : 1)>;                                    \
+    auto kern = k_push_round<T, PP, VIRTUAL, (PP <= 4 && sizeof(T) == 4 ? 2 : 1)>;                                    \
     CommArgs aa = a;                                                                                \
     if (!VIRTUAL) {                                                                                 \
       const int cap = coop_capacity(kern, threads);                                                 \

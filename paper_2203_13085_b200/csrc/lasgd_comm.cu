@@ -722,6 +722,61 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
   return LASGD_OK;
 }
 
+// Bucketed SGD-AR (optimizer.py:214-242 with the gradient all-reduce split into
+// buckets, as a data-parallel trainer overlaps it with backward): one-shot K7 mode 2 over
+// the sub-range [off, off + len) of slot `snap_slot` — the ring-order mean of every
+// rank's gradient over NVLink and the local step of x[off, off + len) with it.  Every
+// element is summed in the rotation of its chunk of the whole vector, so any bucketing
+// gives the bits of the one-launch round.
+extern "C" int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off, size_t len, void* x, void* m,
+                                       const lasgd_sgd_params* sgd, int nblocks, unsigned long long* nonfinite,
+                                       void* stream, unsigned long long* seq) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->world < 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round needs P >= 2");
+  if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
+  if (len == 0 || off > c->n || len > c->n - off)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "range [%zu, %zu) outside the %zu-element vector", off, off + len, c->n);
+  const size_t W = 16 / c->elem;
+  if (off % W) return fail(LASGD_ERR_INVALID_ARGUMENT, "range offset %zu not a multiple of %zu elements", off, W);
+  char* xo = reinterpret_cast<char*>(x) + off * c->elem;
+  char* mo = m ? reinterpret_cast<char*>(m) + off * c->elem : nullptr;
+  void* xs[1] = {xo};
+  const void* gs[1] = {xo};  // unused by mode 2
+  void* ms[1] = {mo};
+  void* ns[1] = {xo};        // unused by mode 2
+  int rc = check_fused_args(1, xs, gs, m ? ms : nullptr, nullptr, ns, sgd, 1.0, 2);
+  if (rc) return rc;
+  if (nblocks <= 0) nblocks = 2 * num_sms() <= kMaxB ? 2 * num_sms() : kMaxB;
+  if (nblocks > kMaxB) return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d > %d", nblocks, kMaxB);
+  DeviceGuard dg(c->device);
+  CommArgs a;
+  unsigned long long s = 0;
+  rc = prepare_launch(c, snap_slot, a, s);
+  if (rc) return rc;
+  for (int r = 0; r < c->world; ++r) {
+    a.snap[r] += off * c->elem;
+    a.xbar[r] += off * c->elem;
+  }
+  a.n = len;
+  a.range_off = off;
+  a.n_glob = c->n;
+  a.nblocks = nblocks;
+  a.nonfinite = nonfinite;
+  c->push_slot = -1;
+  c->end_seq = 0;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (c->dtype == LASGD_F32)
+    rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, nullptr, ns, sgd, 1.0, 2),
+                                    dim3(nblocks, 1), c->threads, cs, LASGD_ALGO_ONESHOT);
+  else
+    rc = launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, nullptr, ns, sgd, 1.0, 2),
+                                     dim3(nblocks, 1), c->threads, cs, LASGD_ALGO_ONESHOT);
+  if (rc) return rc;
+  LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+  if (seq) *seq = s;
+  return LASGD_OK;
+}
+
 extern "C" int lasgd_comm_query(lasgd_comm* c, unsigned long long seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   const uint32_t err = __atomic_load_n(&c->status_host[ST_ERR], __ATOMIC_ACQUIRE);

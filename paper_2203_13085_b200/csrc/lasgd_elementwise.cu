@@ -206,7 +206,7 @@ struct FinalizeOp {
   T* snap_next;
   const T* z;
   const T* delta;
-  static constexpr int U = 2;
+  static constexpr int U = sizeof(T) == 8 ? 1 : 2;
   struct Loaded { Pack<T> z, d; };
   __device__ __forceinline__ void load(Loaded& L, size_t j) const {
     L.z = ld_stream(z + j);

@@ -437,3 +437,134 @@ class SGDARWorker:
 
     def check_finite(self) -> None:
         self._finite.check(self.x.numel())
+
+
+class BucketedSGDARWorker:
+    """SGD-AR (optimizer.py:214-242, ``sync_allreduce_sgd_round``) as a data-parallel
+    trainer runs it: the gradient all-reduce is split into buckets in reverse parameter
+    order and each bucket is reduced over NVLink — with the local step of its slice of x
+    fused in — on a side stream as soon as backward has accumulated every gradient in it,
+    so the exchange overlaps the rest of backward.  Only the last bucket's round is
+    exposed.  The per-element summation order is the whole-vector ring order whatever the
+    bucketing (lasgd_comm_sgd_ar_range), so x stays bit-identical to ``SGDARWorker`` and to
+    the reference's round.
+
+    Backward must write the gradients into the communicator's slots: the worker binds
+    ``flat``'s ``.grad`` views to slot ``grad_buffer`` and rebinds them every step.  Use:
+    ``flat.zero_grad(); loss.backward(); worker.step()`` on the compute stream, eagerly
+    (the buckets launch from autograd hooks).  A parameter must receive exactly one
+    gradient accumulation per backward (no weight sharing)."""
+
+    def __init__(self, flat, comm, *, sgd: Optional[SgdConfig] = None, schedule: Optional[LrSchedule] = None,
+                 lr: Optional[float] = None, bucket_bytes: int = 25 << 20,
+                 compute_stream: Optional[torch.cuda.Stream] = None, side_stream: Optional[torch.cuda.Stream] = None,
+                 nblocks: int = 0):
+        if (schedule is None) == (lr is None):
+            raise ValueError("give exactly one of schedule / lr")
+        if comm is None or comm.world < 2:
+            raise ValueError("the bucketed SGD-AR worker needs a communicator with P >= 2")
+        if comm.n != flat.numel or comm.dtype != flat.x.dtype:
+            raise ValueError("communicator buffers do not match the flat parameters")
+        if bucket_bytes <= 0:
+            raise ValueError("bucket_bytes must be positive")
+        self.sgd = sgd or SgdConfig()
+        self.sgd.validate()
+        self.flat, self.comm = flat, comm
+        self.x = flat.x
+        self.schedule, self.lr = schedule, lr
+        self.compute = compute_stream if compute_stream is not None else torch.cuda.current_stream(flat.x.device)
+        self.side = side_stream if side_stream is not None else comm.stream
+        self.nblocks = nblocks
+        self.m = torch.empty_like(flat.x) if self.sgd.momentum != 0 else None
+        self._finite = _FiniteMonitor(flat.x.device)
+        self.local_clock = 0
+        self.launches = collections.Counter()
+        self._slot = 0
+        # buckets: contiguous ranges from the end of the flat vector (backward produces the
+        # last layers' gradients first), boundaries on 16-byte multiples
+        esize = flat.x.element_size()
+        wpack = 16 // esize
+        cap = max(wpack, bucket_bytes // esize // wpack * wpack)
+        n = flat.numel
+        self.buckets = []
+        hi = n
+        while hi > 0:
+            lo = max(0, hi - cap)
+            lo = lo // wpack * wpack
+            self.buckets.append((lo, hi))
+            hi = lo
+        # bucket membership of every parameter (a tensor may straddle a boundary)
+        self._param_buckets = []
+        self._need = [0] * len(self.buckets)
+        for p, off in zip(flat.params, flat.offsets):
+            end = off + p.numel()
+            bs = [b for b, (lo, hi) in enumerate(self.buckets) if lo < end and off < hi]
+            self._param_buckets.append(bs)
+            for b in bs:
+                self._need[b] += 1
+        self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(i)) for i, p in enumerate(flat.params)]
+        self._reset_step()
+        flat.bind_grads(self.grad_buffer)
+
+    @property
+    def grad_buffer(self) -> torch.Tensor:
+        """Where the next backward must write its gradient."""
+        return self.comm.snapshots[self._slot]
+
+    def current_lr(self) -> float:
+        return self.lr if self.schedule is None else lr_at(self.schedule, self.local_clock)
+
+    def _reset_step(self) -> None:
+        self._pending = list(self._need)
+        self._ready = set(b for b, k in enumerate(self._pending) if k == 0)
+        self._next = 0
+        self._step_lr = None
+
+    def _make_hook(self, i):
+        def hook(_p):
+            for b in self._param_buckets[i]:
+                self._pending[b] -= 1
+                if self._pending[b] == 0:
+                    self._ready.add(b)
+            self._launch_ready()
+        return hook
+
+    def _launch(self, b: int) -> None:
+        if self._step_lr is None:
+            self._step_lr = self.current_lr()
+        lo, hi = self.buckets[b]
+        ev = torch.cuda.Event()
+        ev.record(self.compute)  # every gradient of the bucket has been accumulated on it
+        self.side.wait_event(ev)
+        s = self.sgd
+        self.comm.sgd_ar_range(self._slot, lo, hi - lo, self.x, self._step_lr, m=self.m, momentum=s.momentum,
+                               dampening=s.dampening, weight_decay=s.weight_decay, nesterov=s.nesterov,
+                               first_step=self.local_clock == 0, nblocks=self.nblocks,
+                               nonfinite=self._finite.counter, stream=self.side)
+        self.launches["sgd_ar_bucket"] += 1
+
+    def _launch_ready(self) -> None:
+        # strictly in bucket order: every rank issues the same launch sequence
+        while self._next < len(self.buckets) and self._next in self._ready:
+            self._launch(self._next)
+            self._next += 1
+
+    def step(self) -> None:
+        """Close the step (call on the compute stream after backward): launch whatever
+        bucket backward did not complete, order the compute stream after every bucket's
+        round (x is updated there) and move the gradients to the other slot."""
+        self._ready.update(range(len(self.buckets)))
+        self._launch_ready()
+        self.compute.wait_stream(self.side)
+        self.local_clock += 1
+        self._slot ^= 1
+        self._reset_step()
+        self.flat.bind_grads(self.grad_buffer)
+
+    def check_finite(self) -> None:
+        self._finite.check(self.x.numel())
+
+    def close(self) -> None:
+        for h in getattr(self, "_hooks", ()):
+            h.remove()
+        self._hooks = []

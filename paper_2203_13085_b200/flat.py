@@ -8,6 +8,11 @@ this is exactly the reference MlpOracle's flat vector (problems.py:202-205:
 W_l row-major then b_l).  4-D weights can be exposed as channels_last-strided
 views over the same contiguous storage.  BatchNorm running statistics are
 buffers, not parameters: they stay rank-local (not averaged).
+
+``align_bytes`` (e.g. 256) starts every tensor at an aligned offset so cuDNN sees
+aligned weights and gradients; the gaps are zero in ``x`` and ``g`` and stay zero
+under every sync kernel (zero gradient, zero weight decay term, zero mean).  The
+default 0 packs the tensors back to back (the reference's flat layout).
 """
 
 from __future__ import annotations
@@ -17,28 +22,34 @@ import torch
 
 class FlatParams:
     def __init__(self, module: torch.nn.Module, dtype: torch.dtype = torch.float32, device=None,
-                 channels_last: bool = False):
+                 channels_last: bool = False, align_bytes: int = 0):
         params = [p for p in module.parameters() if p.requires_grad]
         if not params:
             raise ValueError("module has no trainable parameters")
         device = device or params[0].device
-        self.numel = sum(p.numel() for p in params)
-        self.x = torch.empty(self.numel, dtype=dtype, device=device)
+        esize = torch.empty(0, dtype=dtype).element_size()
+        if align_bytes < 0 or (align_bytes and align_bytes % esize):
+            raise ValueError(f"align_bytes must be a non-negative multiple of {esize}")
+        step = max(1, align_bytes // esize)
+        self.offsets = []
+        off = 0
+        for p in params:
+            off = (off + step - 1) // step * step
+            self.offsets.append(off)
+            off += p.numel()
+        self.n_params = sum(p.numel() for p in params)
+        self.numel = off
+        self.x = torch.zeros(self.numel, dtype=dtype, device=device)
         self.g = torch.zeros(self.numel, dtype=dtype, device=device)
         self.params = params
         self.channels_last = channels_last
         self._grad_views = {}
-        self.offsets = []
-        off = 0
         with torch.no_grad():
-            for p in params:
-                n = p.numel()
-                v = self._view(self.x, off, p.shape, channels_last)
+            for p, o in zip(params, self.offsets):
+                v = self._view(self.x, o, p.shape, channels_last)
                 v.copy_(p.detach())
                 p.data = v
-                p.grad = self._view(self.g, off, p.shape, channels_last)
-                self.offsets.append(off)
-                off += n
+                p.grad = self._view(self.g, o, p.shape, channels_last)
 
     @staticmethod
     def _view(buf: torch.Tensor, off: int, shape, channels_last: bool) -> torch.Tensor:

@@ -203,6 +203,91 @@ def _w_sgd_ar(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_sgd_ar_bucketed(rank, world, port):
+    """Bucketed SGD-AR (rounds over sub-ranges launched from autograd hooks): bit-exact
+    against the oracle's SGD-AR loop (optimizer.py:214-242) for ragged buckets, and
+    bit-identical to the one-launch SGDARWorker when backward drives the buckets."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+
+    _init(rank, world, port)
+
+    class _Flat:  # a flat vector with no module: gradients are written by hand
+        def __init__(self, n):
+            self.numel, self.n_params = n, n
+            self.x = torch.empty(n, device="cuda")
+            self.params, self.offsets = [], []
+
+        def bind_grads(self, buf):
+            self.g = buf
+
+    n, steps = 65_541, 6
+    x0 = _vec(3, n)
+    grads = np.stack([np.stack([_vec(700 * t + r, n) for r in range(world)]) for t in range(steps)])
+    etas = np.array([0.1, 0.05, 0.2, 0.01, 0.07, 0.03])
+    for sgd in (None, L.SgdConfig(0.9, 0.0, 1e-4, True)):
+        for bucket_bytes in (16_000, 65_536 * 4, 1 << 30):
+            comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
+            flat = _Flat(n)
+            flat.x.copy_(torch.from_numpy(x0))
+            compute = torch.cuda.Stream()
+            with torch.cuda.stream(compute):
+                w = L.BucketedSGDARWorker(flat, comm, sgd=sgd, lr=1.0, bucket_bytes=bucket_bytes,
+                                          compute_stream=compute)
+                for t in range(steps):
+                    w.lr = float(etas[t])
+                    w.grad_buffer.copy_(torch.from_numpy(grads[t, rank]))
+                    w.step()
+            torch.cuda.synchronize()
+            cfg = None if sgd is None else O.SgdConfig(1.0, sgd.momentum, sgd.dampening, sgd.weight_decay,
+                                                       sgd.nesterov)
+            ref, _ = O.run_sgd_ar(x0, grads, etas, world, sgd=cfg)
+            assert _same_bits(flat.x.cpu().numpy(), ref), (sgd, bucket_bytes, rank)
+            assert w.launches["sgd_ar_bucket"] == steps * len(w.buckets)
+            w.close()
+            dist.barrier()
+            comm.close()
+
+    # backward drives the buckets: same bits as the one-launch SGD-AR round
+    def train(bucketed):
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.Tanh(), torch.nn.Linear(256, 256),
+                                    torch.nn.Tanh(), torch.nn.Linear(256, 1)).cuda()
+        flat = L.FlatParams(model, align_bytes=256)
+        comm = L.P2PCommunicator(flat.numel, nblocks=8, timeout_s=20.0)
+        compute = torch.cuda.Stream()
+        sgd = L.SgdConfig(0.9, 0.0, 1e-4, True)
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(10 + rank)
+        with torch.cuda.stream(compute):
+            if bucketed:
+                w = L.BucketedSGDARWorker(flat, comm, sgd=sgd, lr=0.05, bucket_bytes=64 * 1024,
+                                          compute_stream=compute)
+                assert len(w.buckets) >= 3
+            else:
+                w = L.SGDARWorker(flat.x, comm=comm, sgd=sgd, lr=0.05, compute_stream=compute, flat=flat)
+            for _ in range(5):
+                flat.zero_grad()
+                model(torch.randn(32, 64, device="cuda", generator=gen)).square().mean().backward()
+                w.step()
+        torch.cuda.synchronize()
+        out = flat.x.cpu()
+        if bucketed:
+            w.close()
+        dist.barrier()
+        comm.close()
+        return out
+
+    a, b = train(True), train(False)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32)), rank
+    xs = [None] * world
+    dist.all_gather_object(xs, a)
+    assert all(torch.equal(xs[0], v) for v in xs), "bucketed SGD-AR replicas diverged"
+    dist.destroy_process_group()
+
+
 def _w_full_size(rank, world, port):
     """The bench's configuration at BASELINE size: ResNet-50's n, Nesterov momentum +
     weight decay, sync period 1, fused pipeline with the AUTO algorithm (mirror push at
@@ -425,6 +510,11 @@ def test_worker_round_protocol_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_sgd_ar_worker_bit_exact():
     _spawn(_w_sgd_ar)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_sgd_ar_bucketed_bit_exact():
+    _spawn(_w_sgd_ar_bucketed)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")

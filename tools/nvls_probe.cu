@@ -41,9 +41,27 @@ __device__ __forceinline__ void mm_st(float* p, float4 v) {
                : "memory");
 }
 
-// chunk [c0, c1) in float4 units: sum over all GPUs in the switch, scale, multicast back
+// chunk [c0, c1) in float4 units: sum over all GPUs in the switch, scale, multicast back.
+// U independent multimem loads in flight per thread (the switch round trip is long:
+// one load per thread leaves the reduction latency-bound).
+template <int U>
 __global__ void __launch_bounds__(256) k_nvls_mean(float* mc_src, float* mc_dst, size_t c0, size_t c1, float inv) {
-  for (size_t i = c0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < c1; i += (size_t)gridDim.x * blockDim.x) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = c0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < c1; i += U * stride) {
+    float4 s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = mm_ld_reduce_add(mc_src + 4 * (i + u * stride));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      s[u].x *= inv;
+      s[u].y *= inv;
+      s[u].z *= inv;
+      s[u].w *= inv;
+      mm_st(mc_dst + 4 * (i + u * stride), s[u]);
+    }
+  }
+  for (; i < c1; i += stride) {
     float4 s = mm_ld_reduce_add(mc_src + 4 * i);
     s.x *= inv;
     s.y *= inv;
@@ -51,6 +69,27 @@ __global__ void __launch_bounds__(256) k_nvls_mean(float* mc_src, float* mc_dst,
     s.w *= inv;
     mm_st(mc_dst + 4 * i, s);
   }
+}
+
+// multicast fan-out only: this GPU's chunk (plain local loads) stored once through the
+// switch into every GPU's copy of the destination
+template <int U>
+__global__ void __launch_bounds__(256) k_nvls_bcast(const float* src, float* mc_dst, size_t c0, size_t c1) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = c0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < c1; i += U * stride) {
+    float4 s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = __ldcs(reinterpret_cast<const float4*>(src) + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) mm_st(mc_dst + 4 * (i + u * stride), s[u]);
+  }
+  for (; i < c1; i += stride) mm_st(mc_dst + 4 * i, __ldcs(reinterpret_cast<const float4*>(src) + i));
+}
+
+template <int U>
+void launch_mean(int ctas, cudaStream_t s, float* src, float* dst, size_t c0, size_t c1, float inv) {
+  k_nvls_mean<U><<<ctas, 256, 0, s>>>(src, dst, c0, c1, inv);
 }
 
 int main() {
@@ -119,6 +158,8 @@ int main() {
       CK(cudaMemcpy(uc[d] + off, h, sizeof(float) * (off + 1024 <= n ? 1024 : n - off), cudaMemcpyHostToDevice));
     delete[] h;
   }
+  for (int mode = 0; mode < 2; ++mode)
+  for (int U : {1, 4}) {
   for (int ctas : {148, 296, 592}) {
     float best = 1e9;
     for (int rep = 0; rep < 6; ++rep) {
@@ -130,7 +171,11 @@ int main() {
         CK(cudaSetDevice(d));
         const size_t c0 = n4 * d / P, c1 = n4 * (d + 1) / P;
         CK(cudaEventRecord(e0[d], st[d]));
-        k_nvls_mean<<<ctas, 256, 0, st[d]>>>(mcp[d], mcp[d] + S / 4, c0, c1, 1.0f / P);
+        if (mode == 1) {
+          if (U == 1) k_nvls_bcast<1><<<ctas, 256, 0, st[d]>>>(uc[d], mcp[d] + S / 4, c0, c1);
+          else k_nvls_bcast<4><<<ctas, 256, 0, st[d]>>>(uc[d], mcp[d] + S / 4, c0, c1);
+        } else if (U == 1) launch_mean<1>(ctas, st[d], mcp[d], mcp[d] + S / 4, c0, c1, 1.0f / P);
+        else launch_mean<4>(ctas, st[d], mcp[d], mcp[d] + S / 4, c0, c1, 1.0f / P);
         CK(cudaEventRecord(e1[d], st[d]));
       }
       float ms = 0;
@@ -146,9 +191,10 @@ int main() {
     float check = 0;
     CK(cudaSetDevice(P - 1));
     CK(cudaMemcpy(&check, uc[P - 1] + S / 4 + 12345, 4, cudaMemcpyDeviceToHost));
-    printf("{\"P\": %d, \"ctas\": %d, \"us\": %.1f, \"algbw_GBps\": %.1f, \"check\": %.3f, \"expect\": %.3f}\n", P, ctas,
-           best * 1e3, bytes / (best * 1e-3) / 1e9, check, (P + 1) / 2.0);
+    printf("{\"mode\": \"%s\", \"P\": %d, \"U\": %d, \"ctas\": %d, \"us\": %.1f, \"algbw_GBps\": %.1f, \"check\": %.3f, \"expect\": %.3f}\n", mode ? "bcast" : "mean", P, U, ctas,
+           best * 1e3, bytes / (best * 1e-3) / 1e9, check, mode ? (double)P : (P + 1) / 2.0);
     fflush(stdout);
+  }
   }
   return 0;
 }
