@@ -341,6 +341,9 @@ int lasgd_graph_destroy(lasgd_graph* gr);
 /* One thread that holds `stream` until lasgd_hold_release (or `timeout_s` passes): the
  * host enqueues a whole timed region behind it, then releases it, so host-side jitter
  * cannot open gaps in the region.  Destroy only after the stream has drained. */
+/* Write the device's %globaltimer (ns) to *out (device memory) in stream order: the
+ * clock of the communicator's per-CTA trace (lasgd_comm_read_trace). */
+int lasgd_stamp(unsigned long long* out, void* stream);
 typedef struct lasgd_hold lasgd_hold;
 int lasgd_hold_create(lasgd_hold** out);
 int lasgd_hold_enqueue(lasgd_hold* h, void* stream, double timeout_s);

@@ -177,6 +177,7 @@ SIGNATURES = {
     "lasgd_worker_capture_end": (_I, [_P]),
     "lasgd_graph_launch": (_I, [_P]),
     "lasgd_graph_destroy": (_I, [_P]),
+    "lasgd_stamp": (_I, [_P, _P]),
     "lasgd_hold_create": (_I, [ctypes.POINTER(_P)]),
     "lasgd_hold_enqueue": (_I, [_P, _P, _D]),
     "lasgd_hold_release": (_I, [_P]),

@@ -174,3 +174,22 @@ extern "C" int lasgd_hold_destroy(lasgd_hold* h) {
   delete h;
   return LASGD_OK;
 }
+
+// ---------------------------------------------------------------- device timestamps
+// %globaltimer (ns, the clock the communicator's per-CTA trace uses) written in stream
+// order: puts compute-stream events (forward start, backward end) on the same timeline
+// as the side-stream all-reduce CTAs.
+namespace lasgd {
+__global__ void k_stamp(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+}  // namespace lasgd
+
+extern "C" int lasgd_stamp(unsigned long long* out, void* stream) {
+  if (!out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null output");
+  k_stamp<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out);
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
