@@ -150,7 +150,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------- helpers
 class Hold:
     """lasgd_hold: a one-thread kernel that holds a stream until released, so a whole
-    timed region is enqueued before the device starts it (bounded: 30 s)."""
+    timed region is enqueued before the device starts it (bounded: 5 s; under ncu, which serialises launches, it always waits the 5 s)."""
 
     def __init__(self, N):
         import ctypes
@@ -160,7 +160,7 @@ class Hold:
         N.check(N.lib().lasgd_hold_create(ctypes.byref(self._h)), "lasgd_hold_create")
 
     def enqueue(self, stream):
-        self._N.check(self._N.lib().lasgd_hold_enqueue(self._h, self._c.c_void_p(stream.cuda_stream), 30.0))
+        self._N.check(self._N.lib().lasgd_hold_enqueue(self._h, self._c.c_void_p(stream.cuda_stream), 5.0))
 
     def release(self):
         self._N.check(self._N.lib().lasgd_hold_release(self._h))
@@ -780,17 +780,20 @@ def main():
     return 0
 
 
-def _paired_stats(diffs):
-    """Median and 95% t-interval of the mean of paired per-block differences."""
+def _exposed_stats(leg, base, resamples=4000):
+    """Exposed sync = median block time of the leg - median block time of its no-sync
+    baseline (medians: a rare slow or fast block, e.g. a clock step, does not move them),
+    with a 95% bootstrap percentile interval (blocks resampled with replacement,
+    fixed seed)."""
+    import random
     import statistics as st
 
-    k = len(diffs)
-    mean = sum(diffs) / k
-    sd = st.stdev(diffs) if k > 1 else 0.0
-    tq = {2: 12.71, 3: 4.30, 4: 3.18, 5: 2.78, 6: 2.57, 7: 2.45, 8: 2.36, 9: 2.31, 10: 2.26}.get(k, 2.0)
-    hw = tq * sd / k ** 0.5
-    return {"median": st.median(diffs), "mean": mean, "ci95": [mean - hw, mean + hw], "ci95_halfwidth": hw,
-            "blocks": k}
+    rng = random.Random(12345)
+    d0 = st.median(leg) - st.median(base)
+    boots = sorted(st.median(rng.choices(leg, k=len(leg))) - st.median(rng.choices(base, k=len(base)))
+                   for _ in range(resamples))
+    lo, hi = boots[int(0.025 * resamples)], boots[int(0.975 * resamples) - 1]
+    return {"median": d0, "ci95": [lo, hi], "ci95_halfwidth": (hi - lo) / 2, "blocks": len(leg)}
 
 
 def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barrier, max_over_ranks):
@@ -798,8 +801,8 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     the sync path under each schedule, and with sync disabled (the no-sync ceiling).
 
     The legs run interleaved in blocks (every leg once per repetition, in the same order)
-    and each leg's exposed sync time is the paired per-block difference against the
-    no-sync leg of the same repetition: median and 95% interval over the repetitions.
+    and each leg's exposed sync time is its median block time minus the median block time
+    of its no-sync baseline, with a bootstrap 95% interval over the blocks.
     Graphed legs (forward/backward replayed as a CUDA graph; at N=1 the local step and
     round boundary are captured into the same graph) compare with the graphed no-sync
     leg; eager legs (the bucketed SGD-AR, whose buckets launch from autograd hooks, and
@@ -1019,7 +1022,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         med = st.median(times[name])
         e = {"images_per_s": world * args.batch / (med / 1e3), "ms_per_step": med, "ms_per_step_blocks": times[name]}
         if name != base:
-            d = _paired_stats([t - b for t, b in zip(times[name], times[base])])
+            d = _exposed_stats(times[name], times[base])
             e.update({"exposed_sync_ms_per_step": d["median"], "exposed_sync_ci95_ms": d["ci95"],
                       "exposed_sync_ci95_halfwidth_ms": d["ci95_halfwidth"],
                       "exposed_sync_frac": d["median"] / med, "baseline_leg": base})

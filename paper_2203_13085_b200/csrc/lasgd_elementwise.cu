@@ -137,14 +137,18 @@ struct SgdOp {
   T* delta;
   T* snap;  // optional: also write the updated x here (K7 at P = 1: local step + next snapshot)
   SgdCoef<T> c;
+  // load m / delta whenever they exist (their values are ignored on a first step / after
+  // a reset): the loads then do not wait for first / reset, which the graph-replayable
+  // kernel reads from the device round descriptor at entry
+  bool load_all = false;
   static constexpr int U = 2;
   struct Loaded { Pack<T> x, g, m, d; };
 
   __device__ __forceinline__ void load(Loaded& L, size_t j) const {
     L.x = ld_stream(x + j);
     L.g = ld_stream(g + j);
-    if (c.use_mom && !c.first) L.m = ld_stream(m + j);
-    if (c.use_delta && !c.reset) L.d = ld_stream(delta + j);
+    if (c.use_mom && (load_all || !c.first)) L.m = ld_stream(m + j);
+    if (c.use_delta && (load_all || !c.reset)) L.d = ld_stream(delta + j);
   }
   __device__ __forceinline__ unsigned compute_store(Loaded& L, size_t j) const {
     unsigned bad = 0;
@@ -304,6 +308,7 @@ int sgd_dyn_t(void* x, const void* g, void* m, void* delta, void* const* snaps, 
   op.delta = (T*)delta;
   op.snap = nullptr;
   op.c = make_sgd_coef<T>(p, delta != nullptr);
+  op.load_all = true;
   const size_t npack = n / Pack<T>::W;
   const size_t work = npack > (size_t)kThreads ? npack : (size_t)kThreads;
   const bool al = aligned16(x) && aligned16(g) && (!op.c.use_mom || aligned16(m)) &&
