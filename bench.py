@@ -67,8 +67,8 @@ def parse():
     ap.add_argument("--pipeline", choices=["overlap", "fused"], default="fused",
                     help="overlap: K5 | K4 | K2/K3 on a side stream; fused: one K7 pass per round boundary")
     ap.add_argument("--fused-nblocks", type=int, default=0, help="CTAs of the fused kernel (0 = 2 per SM)")
-    ap.add_argument("--train-block", type=int, default=10, help="training steps per timed block")
-    ap.add_argument("--train-reps", type=int, default=5, help="interleaved repetitions of every training leg")
+    ap.add_argument("--train-block", type=int, default=2, help="training steps per timed block")
+    ap.add_argument("--train-reps", type=int, default=24, help="interleaved repetitions of every training leg")
     ap.add_argument("--train-warmup", type=int, default=4)
     ap.add_argument("--flat-align", type=int, default=256, help="byte alignment of every tensor in the flat buffer")
     ap.add_argument("--bucket-mb", type=int, default=25, help="gradient bucket size of the bucketed SGD-AR / DDP legs")
@@ -781,19 +781,20 @@ def main():
 
 
 def _exposed_stats(leg, base, resamples=4000):
-    """Exposed sync = median block time of the leg - median block time of its no-sync
-    baseline (medians: a rare slow or fast block, e.g. a clock step, does not move them),
-    with a 95% bootstrap percentile interval (blocks resampled with replacement,
-    fixed seed)."""
+    """Exposed sync = median over repetitions of the paired difference (leg block - no-sync
+    block of the same repetition), with a 95% bootstrap percentile interval of that
+    median (repetitions resampled with replacement, fixed seed).  Pairing cancels the
+    slow drifts of the step time (the GPU's step time switches between two levels ~0.4 ms
+    apart for stretches of several blocks), the median ignores the rare repetition in
+    which a switch falls between the two blocks."""
     import random
     import statistics as st
 
+    diffs = [a - b for a, b in zip(leg, base)]
     rng = random.Random(12345)
-    d0 = st.median(leg) - st.median(base)
-    boots = sorted(st.median(rng.choices(leg, k=len(leg))) - st.median(rng.choices(base, k=len(base)))
-                   for _ in range(resamples))
+    boots = sorted(st.median(rng.choices(diffs, k=len(diffs))) for _ in range(resamples))
     lo, hi = boots[int(0.025 * resamples)], boots[int(0.975 * resamples) - 1]
-    return {"median": d0, "ci95": [lo, hi], "ci95_halfwidth": (hi - lo) / 2, "blocks": len(leg)}
+    return {"median": st.median(diffs), "ci95": [lo, hi], "ci95_halfwidth": (hi - lo) / 2, "blocks": len(diffs)}
 
 
 def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barrier, max_over_ranks):
@@ -801,8 +802,9 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     the sync path under each schedule, and with sync disabled (the no-sync ceiling).
 
     The legs run interleaved in blocks (every leg once per repetition, in the same order)
-    and each leg's exposed sync time is its median block time minus the median block time
-    of its no-sync baseline, with a bootstrap 95% interval over the blocks.
+    and each leg's exposed sync time is the median over repetitions of its block time
+    minus the no-sync baseline's block time in the same repetition, with a bootstrap 95%
+    interval.
     Graphed legs (forward/backward replayed as a CUDA graph; at N=1 the local step and
     round boundary are captured into the same graph) compare with the graphed no-sync
     leg; eager legs (the bucketed SGD-AR, whose buckets launch from autograd hooks, and
