@@ -78,7 +78,7 @@ def parse():
     ap.add_argument("--kernels-only", action="store_true", help="short run for ncu: sync path only")
     ap.add_argument("--no-virtual", action="store_true", help="skip the virtual-rank (P=2/4/8 on one GPU) kernels")
     ap.add_argument("--no-sync-graph", action="store_true",
-                    help="N=1: issue the timed steps one by one instead of replaying them as one CUDA graph")
+                    help="issue the timed steps one by one instead of replaying them as one CUDA graph")
     return ap.parse_args()
 
 
@@ -537,18 +537,20 @@ def main():
 
     hold = Hold(N)
 
-    # ---------------- value: HBM-resident gradients, device-timed.  One rank: the K steps
-    # replay as ONE CUDA graph (LASGDWorker.capture: the deterministic loop reads its
-    # per-round scalars from the device round descriptor).  Every N: the timed region is
-    # enqueued behind a hold kernel and released at once, so host jitter cannot open gaps.
+    # ---------------- value: HBM-resident gradients, device-timed.  The K steps replay as
+    # ONE CUDA graph (LASGDWorker.capture: the deterministic loop reads its per-round
+    # scalars — rate, first step, snapshot slot, launch sequence — from the device round
+    # descriptor; fused pipeline at N>1).  The timed region is enqueued behind a hold
+    # kernel and released at once, so host jitter cannot open gaps in it.
     with torch.cuda.stream(compute):
         w = make_worker(False)
         run_sync_path(w, args.warmup, lambda t: grads[t % 2])
         w.drain()
         graph = None
-        if world == 1 and not args.no_sync_graph:
+        if not args.no_sync_graph and (args.pipeline == "fused" or world == 1) and args.steps % args.sync_period == 0:
             graph = w.capture([grads[t % 2] for t in range(args.steps)])
             graph.replay()  # graph upload; one more untimed pass
+            w.drain()
     torch.cuda.synchronize()
     clocks = ClockSampler(local) if rank == 0 else None
     barrier()

@@ -51,7 +51,64 @@ struct CommArgs {
   int cur;                       // snapshot slot / staging parity read this round
   uint32_t prev_push;            // launch whose end signals certify the staged contributions
   uint32_t prev_end;             // K7: the previous launch, if its end signals certify this one's inputs (else 0)
+  // graph-replayable launch (adv.rd != nullptr): the sequence number (epoch of every
+  // flag), the snapshot slot and the work-queue / counter slots come from the worker's
+  // device round descriptor instead of the fields above; snap[] then point at slot 0
+  // (slot 1 is slot_stride bytes further) and the counters at their slot-0 entries.
+  // dyn_chain: the previous launch raised end signals (every round of a captured
+  // steady-state loop does), so K7 enters on them.  The last CTA advances the descriptor.
+  RoundAdv adv;
+  size_t slot_stride;
+  int dyn_chain;
 };
+
+// Per-CTA copy of the dynamic launch arguments (read once by thread 0 at entry).
+struct DynComm {
+  unsigned long long seq;
+  int cur;
+};
+static __shared__ DynComm s_dyn;
+
+__device__ __forceinline__ void dyn_comm_begin(const CommArgs& a) {
+  if (a.adv.rd == nullptr) return;
+  if (threadIdx.x == 0) {
+    s_dyn.seq = __ldcg(&a.adv.rd->seq) + 1ull;
+    s_dyn.cur = __ldcg(&a.adv.rd->snap_idx);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ unsigned long long cseq(const CommArgs& a) { return a.adv.rd ? s_dyn.seq : a.seq; }
+__device__ __forceinline__ uint32_t cepoch(const CommArgs& a) { return a.adv.rd ? (uint32_t)s_dyn.seq : a.epoch; }
+__device__ __forceinline__ int ccur(const CommArgs& a) { return a.adv.rd ? s_dyn.cur : a.cur; }
+__device__ __forceinline__ uint32_t cprev_push(const CommArgs& a) {
+  return a.adv.rd ? (uint32_t)(s_dyn.seq - 1ull) : a.prev_push;
+}
+__device__ __forceinline__ uint32_t cprev_end(const CommArgs& a) {
+  return a.adv.rd ? (a.dyn_chain ? (uint32_t)(s_dyn.seq - 1ull) : 0u) : a.prev_end;
+}
+__device__ __forceinline__ unsigned long long* ctile(const CommArgs& a) {
+  return (a.adv.rd && a.tile_ctr) ? a.tile_ctr + 2 * (s_dyn.seq % kDoneSlots) : a.tile_ctr;
+}
+__device__ __forceinline__ unsigned* cmid(const CommArgs& a) {
+  return (a.adv.rd && a.mid_ctr) ? a.mid_ctr + (s_dyn.seq % kDoneSlots) : a.mid_ctr;
+}
+__device__ __forceinline__ unsigned* cend(const CommArgs& a) {
+  return (a.adv.rd && a.end_ctr) ? a.end_ctr + (s_dyn.seq % kDoneSlots) : a.end_ctr;
+}
+// rank q's snapshot slot `slot` (dynamic launches), or the launch's slot (static)
+__device__ __forceinline__ const char* csnap(const CommArgs& a, int q) {
+  return a.snap[q] + ((a.adv.rd && s_dyn.cur) ? a.slot_stride : 0);
+}
+__device__ __forceinline__ const char* cslot(const CommArgs& a, int q, int slot) {
+  return a.snap[q] + (slot ? a.slot_stride : 0);
+}
+// the learning rate / first step / delta reset of a dynamic launch
+template <typename T>
+__device__ __forceinline__ SgdCoef<T> ccoef(const CommArgs& a, const SgdCoef<T>& c) {
+  SgdCoef<T> r = c;
+  if (a.adv.rd) dyn_coef(r, dyn_read(a.adv.rd));
+  return r;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer();
 
@@ -133,8 +190,8 @@ __device__ inline void report_failure(const CommArgs& a, int code, int peer, int
     a.status[ST_PEER] = peer;
     a.status[ST_PHASE] = phase;
     a.status[ST_BLOCK] = block;
-    a.status[ST_SEQ_LO] = (uint32_t)(a.seq & 0xffffffffu);
-    a.status[ST_SEQ_HI] = (uint32_t)(a.seq >> 32);
+    a.status[ST_SEQ_LO] = (uint32_t)(cseq(a) & 0xffffffffu);
+    a.status[ST_SEQ_HI] = (uint32_t)(cseq(a) >> 32);
     a.status[ST_RANK] = rank;
     __threadfence_system();
   }
@@ -151,11 +208,11 @@ __device__ bool cta_barrier(const CommArgs& a, int phase, int b, int rank) {
     const size_t slot = ((size_t)phase * kMaxB + b) * kMaxR;
     if (a.skip_signal_phase != phase) {
       __threadfence_system();
-      st_release_sys(a.pad[q] + slot + rank, a.epoch);
+      st_release_sys(a.pad[q] + slot + rank, cepoch(a));
     }
     const uint32_t* f = a.pad[rank] + slot + q;
     const unsigned long long t0 = globaltimer();
-    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+    while ((int32_t)(ld_acquire_sys(f) - cepoch(a)) < 0) {
       if ((long long)(globaltimer() - t0) > a.timeout_ns) {
         report_failure(a, ERR_TIMEOUT, q, phase, b, rank);
         ok = 0;
@@ -167,18 +224,34 @@ __device__ bool cta_barrier(const CommArgs& a, int phase, int b, int rank) {
   return __syncthreads_and(ok) != 0;
 }
 
-// Last CTA of a launch publishes the sequence number to host-mapped memory.
+// Last CTA of a launch publishes the sequence number to host-mapped memory (and, for a
+// graph-replayable launch, advances the worker's device round descriptor: every CTA
+// read it at entry, before counting itself in here).
 __device__ inline void publish_done(const CommArgs& a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    const unsigned slot = (unsigned)(a.seq % kDoneSlots);
+    const unsigned long long seq = cseq(a);
+    const unsigned slot = (unsigned)(seq % kDoneSlots);
     const unsigned prev = atomicAdd(&a.done_ctr[slot], 1u);
     if (prev == (unsigned)a.nblocks - 1u) {
       a.done_ctr[slot] = 0u;
-      if (a.tile_ctr) a.tile_ctr[0] = a.tile_ctr[1] = 0ull;  // every CTA has left its tile loops
+      unsigned long long* tq = ctile(a);
+      if (tq) tq[0] = tq[1] = 0ull;  // every CTA has left its tile loops
+      if (a.adv.rd) {
+        DevRound* r = a.adv.rd;
+        r->clock += (unsigned long long)a.adv.steps;
+        r->seq += (unsigned long long)a.adv.seq_inc;
+        if (a.adv.steps && a.adv.has_mom) r->mom_started = 1;
+        if (a.adv.close) {
+          r->snap_idx ^= 1;
+          r->delta_fresh = a.adv.has_delta;
+        } else if (a.adv.steps) {
+          r->delta_fresh = 0;
+        }
+      }
       __threadfence_system();
-      st_release_sys64(a.done_seq, a.seq);
+      st_release_sys64(a.done_seq, seq);
     }
   }
 }
@@ -246,7 +319,7 @@ __device__ __forceinline__ void tile_loop(unsigned long long* ctr, int b, int nb
 
 template <int U, typename F>
 __device__ __forceinline__ void for_tiles(const CommArgs& a, int b, size_t npack, F&& range) {
-  tile_loop(a.tile_ctr, b, a.nblocks, 0, npack, (size_t)kTileIters * U * blockDim.x, range);
+  tile_loop(ctile(a), b, a.nblocks, 0, npack, (size_t)kTileIters * U * blockDim.x, range);
 }
 
 // Rank-level signal of kind k (0 = mid: reduce-scatter / mean pushes done, 1 = end:
@@ -269,7 +342,7 @@ __device__ void rank_signal(const CommArgs& a, int kind, unsigned* ctr, int rank
   if (s_last && threadIdx.x < P && !(kind == 0 && a.skip_signal_phase == 1) &&
       !(kind == 1 && a.skip_signal_phase == 2)) {
     __threadfence_system();
-    st_release_sys(a.pad[threadIdx.x] + slot + rank, a.epoch);
+    st_release_sys(a.pad[threadIdx.x] + slot + rank, cepoch(a));
   }
 }
 
@@ -298,8 +371,8 @@ __device__ bool rank_wait(const CommArgs& a, int kind, uint32_t epoch, int b, in
 // CTAs co-resident: the P2P two-shot kernels are launched cooperatively.
 template <int P>
 __device__ bool rank_barrier(const CommArgs& a, int b, int rank) {
-  rank_signal<P>(a, 0, a.mid_ctr, rank);
-  return rank_wait<P>(a, 0, a.epoch, b, rank);
+  rank_signal<P>(a, 0, cmid(a), rank);
+  return rank_wait<P>(a, 0, cepoch(a), b, rank);
 }
 
 // Launch gate (one warp, launched in stream order just before a side-stream

@@ -39,12 +39,14 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
   const int vr = VIRTUAL ? (int)blockIdx.y : 0;
   const int b = blockIdx.x;
   bool ok = true;
+  dyn_comm_begin(a);
+  const SgdCoef<T> cf = ccoef(a, f.c);
   trace_mark(a, b, 0);
   // Entry: every peer's snapshot slot must be final and every peer must be done reading
   // this rank's other slot.  When the previous launch was a round that raised end
   // signals (K7 one-shot or K8), those certify both and were raised before the peers
   // even launched this kernel; otherwise the per-CTA entry barrier.
-  if (!VIRTUAL && P > 1) ok = a.prev_end ? rank_wait<P>(a, 1, a.prev_end, b, rank) : cta_barrier<P>(a, 0, b, rank);
+  if (!VIRTUAL && P > 1) ok = cprev_end(a) ? rank_wait<P>(a, 1, cprev_end(a), b, rank) : cta_barrier<P>(a, 0, b, rank);
   trace_mark(a, b, 1);
   unsigned bad = 0;
   if (ok) {
@@ -54,22 +56,22 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
     for (int c = 0; c <= P; ++c) bnd[c] = chunk_bound_local(a, P, c);
     const T* src[P];
 #pragma unroll
-    for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(a.snap[q]);
+    for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const T*>(csnap(a, q));
     T* const x = f.x[vr];
     const T* const g = f.g[vr];
     T* const m = f.m[vr];
     T* const dl = f.delta[vr];
-    T* const sn = f.snap_next[vr];
-    const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-    const bool store_d = f.c.use_delta && (P == 1 || f.mode == 0);  // finalize resets delta
+    T* const sn = a.adv.rd ? reinterpret_cast<T*>(const_cast<char*>(cslot(a, rank, 1 - ccur(a)))) : f.snap_next[vr];
+    const bool load_m = cf.use_mom && !cf.first, load_d = cf.use_delta && !cf.reset;
+    const bool store_d = cf.use_delta && (P == 1 || f.mode == 0);  // finalize resets delta
     auto element = [&](T& xv, T gv, T& mv, T& dv, const T (&lane)[P], int cidx) -> T {
       if constexpr (P > 1) {
         if (f.mode == 2) {  // SGD-AR: the local step with the ring-order mean of the gradients
-          bad += sgd_elem(f.c, xv, mean_div<T, P>(rot_sum<T, P>(lane, cidx)), mv, dv);
+          bad += sgd_elem(cf, xv, mean_div<T, P>(rot_sum<T, P>(lane, cidx)), mv, dv);
           return xv;
         }
       }
-      unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+      unsigned bb = sgd_elem(cf, xv, gv, mv, dv);
       if constexpr (P > 1) {
         const T zb = mean_div<T, P>(rot_sum<T, P>(lane, cidx));
         if (f.mode == 0) {
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
             element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], lane, cidx);
           }
           st_stream(x + j0, vx[u]);
-          if (f.c.use_mom) st_stream(m + j0, vm[u]);
+          if (cf.use_mom) st_stream(m + j0, vm[u]);
           if (store_d) st_stream(dl + j0, vd[u]);
           if (f.mode != 2) st_stream(sn + j0, vx[u]);
         }
@@ -134,13 +136,13 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
         T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
         element(xv, f.mode == 2 ? T(0) : g[j], mv, dv, lane, chunk_of<P>(j, bnd));
         x[j] = xv;
-        if (f.c.use_mom) m[j] = mv;
+        if (cf.use_mom) m[j] = mv;
         if (store_d) dl[j] = dv;
         if (f.mode != 2) sn[j] = xv;
       }
     }
   }
-  if (!VIRTUAL && P > 1 && ok) rank_signal<P>(a, 1, a.end_ctr, rank);  // certifies the next round's entry
+  if (!VIRTUAL && P > 1 && ok) rank_signal<P>(a, 1, cend(a), rank);  // certifies the next round's entry
   report_nonfinite(a.nonfinite, bad);
   trace_mark(a, b, 3);
   if (!VIRTUAL) publish_done(a);

@@ -21,7 +21,7 @@ int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, in
       }                                                                                             \
       return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                \
     }                                                                                               \
-    return launch_kernel(false, k_fused_round<T, PP, VIRTUAL, (PP <= 2 && (sizeof(T) == 4 || PP == 2) ? 2 : 1)>, grid, threads, s, \
+    return launch_kernel(false, k_fused_round<T, PP, VIRTUAL, (PP <= 2 && sizeof(T) == 4 ? 2 : 1)>, grid, threads, s, \
                          a, f);
   switch (P) {
     LASGD_FCASE(1)

@@ -19,7 +19,7 @@ int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int
     return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                  \
   }
   if (P == 2) {  // mirror form
-    auto kern = k_push_mirror<T, VIRTUAL, 2>;
+    auto kern = k_push_mirror<T, VIRTUAL, sizeof(T) == 4 ? 2 : 1>;
     CommArgs aa = a;
     if (!VIRTUAL) {
       const int cap = coop_capacity(kern, threads);

@@ -36,12 +36,14 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
   const int vr = VIRTUAL ? (int)blockIdx.y : 0;
   const int b = blockIdx.x;
   const size_t n = a.n;
-  const int cur = a.cur, nxt = 1 - a.cur;
+  dyn_comm_begin(a);
+  const SgdCoef<T> cf = ccoef(a, f.c);
+  const int cur = ccur(a), nxt = 1 - cur;
   bool ok = true;
   unsigned bad = 0;
-  unsigned long long* q0 = a.tile_ctr ? a.tile_ctr : nullptr;
-  unsigned long long* q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
-  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  unsigned long long* q0 = ctile(a);
+  unsigned long long* q1 = ctile(a) ? ctile(a) + 1 : nullptr;
+  const T* const snap_own = reinterpret_cast<const T*>(csnap(a, rank));
   trace_mark(a, b, 0);
   // offset of element j of chunk c inside a staging slot (keeps 16-byte alignment)
   auto soff = [&](int c, size_t j) { return j - chunk_bound(n, P, c) / W * W; };
@@ -65,17 +67,17 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
         }
       },
       [&](int c, size_t j) { stage_ptr<T>(a, c, cur, rank, P)[soff(c, j)] = snap_own[j]; });
-    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+    if (!VIRTUAL) rank_signal<P>(a, 1, cend(a), rank);
   }
   T* const x = f.x[vr];
   const T* const g = f.g[vr];
   T* const m = f.m[vr];
   T* const dl = f.delta[vr];
-  T* const sn = f.snap_next[vr];
-  const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-  const bool store_d = f.c.use_delta && f.mode == 0;
+  T* const sn = a.adv.rd ? reinterpret_cast<T*>(const_cast<char*>(cslot(a, rank, nxt))) : f.snap_next[vr];
+  const bool load_m = cf.use_mom && !cf.first, load_d = cf.use_delta && !cf.reset;
+  const bool store_d = cf.use_delta && f.mode == 0;
   auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
-    unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+    unsigned bb = sgd_elem(cf, xv, gv, mv, dv);
     if (f.mode == 0) {
       bb += pull_elem(f.neg_alpha, xv, sv, zb);
     } else {
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
     bad += bb;
   };
   if (a.phases & 1) {
-    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
+    if (!VIRTUAL) ok = rank_wait<P>(a, 1, cprev_push(a), b, rank);
     trace_mark(a, b, 1);
     if (ok) {
       size_t cs, ce, cp0, cp1;
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
               for (int q = 0; q < P; ++q)
                 if (q != rank) st_plain(reinterpret_cast<T*>(a.xbar[q]) + j, z);  // the mean to every peer
               st_stream(x + j, vx[u]);
-              if (f.c.use_mom) st_stream(m + j, vm[u]);
+              if (cf.use_mom) st_stream(m + j, vm[u]);
               if (store_d) st_stream(dl + j, vd[u]);
               st_stream(sn + j, vx[u]);
             }
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
           element(xv, g[j], mv, dv, snap_own[j], zb);
           x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
+          if (cf.use_mom) m[j] = mv;
           if (store_d) dl[j] = dv;
           sn[j] = xv;
         };
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
                   element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], vs[u].v[k], vz[u].v[k]);
                 st_plain(dst + soff(c, j), vx[u]);  // next-round contribution to owner c
                 st_stream(x + j, vx[u]);
-                if (f.c.use_mom) st_stream(m + j, vm[u]);
+                if (cf.use_mom) st_stream(m + j, vm[u]);
                 if (store_d) st_stream(dl + j, vd[u]);
                 st_stream(sn + j, vx[u]);
               }
@@ -209,12 +211,12 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
           element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), zl[j]);
           x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
+          if (cf.use_mom) m[j] = mv;
           if (store_d) dl[j] = dv;
           sn[j] = xv;
           stage_ptr<T>(a, c, nxt, rank, P)[soff(c, j)] = xv;
         });
-      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+      if (!VIRTUAL) rank_signal<P>(a, 1, cend(a), rank);
     }
   }
   report_nonfinite(a.nonfinite, bad);
@@ -244,10 +246,12 @@ __global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T
   const int peer = 1 - rank;
   const int b = blockIdx.x;
   const size_t n = a.n;
-  const int cur = a.cur, nxt = 1 - a.cur;
+  dyn_comm_begin(a);
+  const SgdCoef<T> cf = ccoef(a, f.c);
+  const int cur = ccur(a), nxt = 1 - cur;
   bool ok = true;
   unsigned bad = 0;
-  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  const T* const snap_own = reinterpret_cast<const T*>(csnap(a, rank));
   trace_mark(a, b, 0);
   if (a.phases & 4) {  // initial mirror: the current snapshot -> the peer's mirror, parity cur
     T* dst = mirror_ptr<T>(a, peer, cur);
@@ -256,10 +260,10 @@ __global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T
     });
     if (b == a.nblocks - 1)
       for (size_t j = (n / W) * W + threadIdx.x; j < n; j += blockDim.x) dst[j] = snap_own[j];
-    if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+    if (!VIRTUAL) rank_signal<P>(a, 1, cend(a), rank);
   }
   if (a.phases & 1) {
-    if (!VIRTUAL) ok = rank_wait<P>(a, 1, a.prev_push, b, rank);
+    if (!VIRTUAL) ok = rank_wait<P>(a, 1, cprev_push(a), b, rank);
     trace_mark(a, b, 1);
     if (ok) {
       size_t bnd[P + 1];
@@ -271,11 +275,11 @@ __global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T
       const T* const g = f.g[vr];
       T* const m = f.m[vr];
       T* const dl = f.delta[vr];
-      T* const sn = f.snap_next[vr];
-      const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
-      const bool store_d = f.c.use_delta && f.mode == 0;
+      T* const sn = a.adv.rd ? reinterpret_cast<T*>(const_cast<char*>(cslot(a, rank, nxt))) : f.snap_next[vr];
+      const bool load_m = cf.use_mom && !cf.first, load_d = cf.use_delta && !cf.reset;
+      const bool store_d = cf.use_delta && f.mode == 0;
       auto element = [&](T& xv, T gv, T& mv, T& dv, T own, T oth, int cidx) {
-        unsigned bb = sgd_elem(f.c, xv, gv, mv, dv);
+        unsigned bb = sgd_elem(cf, xv, gv, mv, dv);
         T lane[P];  // lanes by rank, selected without dynamic register indexing
         lane[0] = rank == 0 ? own : oth;
         lane[1] = rank == 0 ? oth : own;
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T
                         c0 == c1 ? c0 : chunk_of<P>(j0 + k, bnd));
               st_plain(out + j0, vx[u]);  // posted NVLink write into the peer's mirror
               st_stream(x + j0, vx[u]);
-              if (f.c.use_mom) st_stream(m + j0, vm[u]);
+              if (cf.use_mom) st_stream(m + j0, vm[u]);
               if (store_d) st_stream(dl + j0, vd[u]);
               st_stream(sn + j0, vx[u]);
             }
@@ -328,13 +332,13 @@ __global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
           element(xv, g[j], mv, dv, snap_own[j], mir[j], chunk_of<P>(j, bnd));
           x[j] = xv;
-          if (f.c.use_mom) m[j] = mv;
+          if (cf.use_mom) m[j] = mv;
           if (store_d) dl[j] = dv;
           sn[j] = xv;
           out[j] = xv;
         }
       }
-      if (!VIRTUAL) rank_signal<P>(a, 1, a.end_ctr, rank);
+      if (!VIRTUAL) rank_signal<P>(a, 1, cend(a), rank);
     }
   }
   report_nonfinite(a.nonfinite, bad);

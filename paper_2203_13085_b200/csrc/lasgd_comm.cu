@@ -722,6 +722,95 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
   return LASGD_OK;
 }
 
+namespace lasgd {
+
+int comm_mirror_get(lasgd_comm* c, CommMirror* m) {
+  if (!c || !m) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  m->seq = c->seq;
+  m->last_push = c->last_push;
+  m->end_seq = c->end_seq;
+  m->push_slot = c->push_slot;
+  return LASGD_OK;
+}
+
+int comm_mirror_set(lasgd_comm* c, const CommMirror& m) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  c->seq = m.seq;
+  c->last_push = m.last_push;
+  c->end_seq = m.end_seq;
+  c->push_slot = m.push_slot;
+  return LASGD_OK;
+}
+
+int comm_record_last(lasgd_comm* c, void* stream) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->seq == 0) return LASGD_OK;
+  DeviceGuard g(c->device);
+  LASGD_CUDA_TRY(cudaEventRecord(c->ev[c->seq % kEvents], reinterpret_cast<cudaStream_t>(stream)));
+  return LASGD_OK;
+}
+
+int comm_fused_round_dyn(lasgd_comm* c, int snap_slot, int algo, void* x, const void* g, void* m, void* delta,
+                         const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+                         unsigned long long* nonfinite, void* stream, const RoundAdv& adv, unsigned long long* seq) {
+  if (!c || !adv.rd) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm or round descriptor");
+  if (mode == 2) return fail(LASGD_ERR_UNSUPPORTED, "graph replay of SGD-AR rounds is not built");
+  if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
+  algo = resolve_fused_algo(algo, c->world, c->n * c->elem);
+  const bool push = algo == LASGD_ALGO_PUSH;
+  if (!push && algo != LASGD_ALGO_ONESHOT)
+    return fail(LASGD_ERR_UNSUPPORTED, "graph replay covers the one-shot and push rounds (algo %d)", algo);
+  void* xs[1] = {x};
+  const void* gs[1] = {g};
+  void* ms[1] = {m};
+  void* ds[1] = {delta};
+  void* ns[1] = {c->base + c->off_snap[1 - snap_slot]};  // checked here; the kernel picks the slot itself
+  int rc = check_fused_args(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode);
+  if (rc) return rc;
+  // steady state: this round enters on the previous launch's end signals
+  if (push ? (c->seq == 0 || c->push_slot != snap_slot || c->last_push != c->seq)
+           : (c->seq == 0 || c->end_seq != c->seq))
+    return fail(LASGD_ERR_STATE, "capture a round only after an eager round of the same kind (launch %llu)", c->seq);
+  if (nblocks <= 0) nblocks = 2 * num_sms() <= kMaxB ? 2 * num_sms() : kMaxB;
+  if (nblocks > kMaxB) return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d > %d", nblocks, kMaxB);
+  DeviceGuard dg(c->device);
+  CommArgs a;
+  unsigned long long s = 0;
+  rc = prepare_launch(c, 0, a, s);  // slot-0 pointers; the kernel offsets by the slot in rd
+  if (rc) return rc;
+  a.adv = adv;
+  a.slot_stride = c->off_snap[1] - c->off_snap[0];
+  a.dyn_chain = 1;
+  a.tile_ctr = c->tile_ctr;  // slot-0 entries: the kernel indexes them by its dynamic sequence number
+  a.mid_ctr = c->mid_ctr;
+  a.end_ctr = c->end_ctr;
+  a.skip_signal_phase = -1;
+  a.nblocks = nblocks;
+  a.nonfinite = nonfinite;
+  a.phases = 3;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (push) {
+    rc = c->dtype == LASGD_F32
+             ? launch_push<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs)
+             : launch_push<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs);
+    if (rc) return rc;
+    c->last_push = s;
+    c->end_seq = s;
+    c->push_slot = 1 - snap_slot;
+  } else {
+    rc = c->dtype == LASGD_F32
+             ? launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, LASGD_ALGO_ONESHOT)
+             : launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, delta ? ds : nullptr, ns, sgd, alpha, mode), dim3(nblocks, 1), c->threads, cs, LASGD_ALGO_ONESHOT);
+    if (rc) return rc;
+    c->end_seq = s;
+    c->push_slot = -1;
+  }
+  if (seq) *seq = s;
+  return LASGD_OK;
+}
+
+}  // namespace lasgd
+
 // Bucketed SGD-AR (optimizer.py:214-242 with the gradient all-reduce split into
 // buckets, as a data-parallel trainer overlaps it with backward): one-shot K7 mode 2 over
 // the sub-range [off, off + len) of slot `snap_slot` — the ring-order mean of every

@@ -214,6 +214,25 @@ __device__ __forceinline__ void dyn_advance(const RoundAdv& ad, unsigned total) 
   }
 }
 
+// Host-side communicator bookkeeping a graph replay must advance like the captured
+// launches did (lasgd_comm.cu): launches issued, the last push round, the last launch
+// that raised end-of-round signals, the staging parity that holds valid contributions.
+struct CommMirror {
+  unsigned long long seq, last_push, end_seq;
+  int push_slot;
+};
+int comm_mirror_get(lasgd_comm* c, CommMirror* m);
+int comm_mirror_set(lasgd_comm* c, const CommMirror& m);
+// Record the completion event of launch c->seq on `stream` (after a graph replay).
+int comm_record_last(lasgd_comm* c, void* stream);
+// The fused round (K7 one-shot or K8 push) in graph-replayable form: sequence number,
+// snapshot slot, learning rate, first step and delta reset from adv.rd; requires the
+// steady state of a deterministic loop (the previous launch was a round of the same
+// kind).  Issues no event (the captured graph is the unit of completion).
+int comm_fused_round_dyn(lasgd_comm* c, int snap_slot, int algo, void* x, const void* g, void* m, void* delta,
+                         const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
+                         unsigned long long* nonfinite, void* stream, const RoundAdv& adv, unsigned long long* seq);
+
 // CTAs per SM of the streaming kernels (tunable, lasgd_set_stream_ctas_per_sm).  The
 // default leaves half of every SM's registers/threads free so the all-reduce CTAs on
 // the side stream can co-reside with a local step instead of queueing behind it.

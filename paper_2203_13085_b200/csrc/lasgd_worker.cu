@@ -66,6 +66,7 @@ struct lasgd_worker {
   bool dyn = false;       // issuing into a capture: launches take their scalars from rd
   cudaStream_t cap_stream = nullptr;  // lasgd_worker_graph_capture records here
   bool rd_dirty = true;   // eager launches ran since rd was last written
+  unsigned long long rd_seq = 0;  // communicator launches rd accounts for
   // instrumentation
   bool timed = false;
   std::vector<TimingRec> recs;
@@ -193,8 +194,17 @@ static int fused_step(lasgd_worker* w, const void* g, double lr) {
   lasgd_sgd_params p = sgd_params(w, lr);
   const int mode = finalize_mode(w) ? 1 : 0;
   int rc;
-  if (w->dyn) {
+  if (w->dyn && w->world == 1) {
     rc = dyn_step(w, g, 1);
+  } else if (w->dyn) {
+    unsigned long long s = 0;
+    RoundAdv adv = make_adv(w, 1);
+    adv.seq_inc = 1;
+    rc = issue(w, K_FUSED, w->compute, [&] {
+      return comm_fused_round_dyn(w->comm, cur, w->cfg.algo, w->x, g, w->m, w->delta, &p, w->cfg.alpha, mode,
+                                  w->cfg.fused_nblocks, w->nonfinite, (void*)w->compute, adv, &s);
+    });
+    if (!rc) w->seq = s;
   } else if (w->world == 1) {
     void* xs[1] = {w->x};
     const void* gs[1] = {g};
@@ -425,6 +435,8 @@ struct lasgd_graph_saved {
   int tau, snap_idx;
   long long clock, gclock;
   bool mom, dfresh;
+  unsigned long long seq;
+  CommMirror comm;  // communicator bookkeeping (world > 1)
   long long launches[K_KINDS], hist[LASGD_TAU_HIST];
 };
 
@@ -433,6 +445,7 @@ struct lasgd_graph {
   cudaGraphExec_t exec = nullptr;
   int steps = 0, tau0 = 0;
   lasgd_graph_saved saved;
+  CommMirror comm_after;  // the communicator bookkeeping after the captured launches
   // what one replay does to the host mirror of the protocol state
   long long d_clock = 0, d_rounds = 0;
   bool mom_after = false, delta_fresh_after = false;
@@ -473,7 +486,8 @@ extern "C" int lasgd_worker_set_lr_table(lasgd_worker* w, const double* lr, size
 
 static int capture_check(lasgd_worker* w) {
   if (w->cfg.adaptive) return fail(LASGD_ERR_UNSUPPORTED, "graph replay needs the deterministic schedule");
-  if (w->world > 1) return fail(LASGD_ERR_UNSUPPORTED, "graph replay of multi-rank rounds is not built");
+  if (w->world > 1 && w->cfg.sync && w->cfg.pipeline != 1)
+    return fail(LASGD_ERR_UNSUPPORTED, "multi-rank graph replay needs the fused pipeline");
   if (w->timed) return fail(LASGD_ERR_STATE, "per-launch timing cannot be captured");
   if (w->dyn) return fail(LASGD_ERR_STATE, "a capture is already open on this worker");
   if (!w->lr_dev || !w->rd)
@@ -491,6 +505,8 @@ static void capture_open(lasgd_worker* w, lasgd_graph* gr) {
   v.gclock = w->global_clock;
   v.mom = w->mom_started;
   v.dfresh = w->delta_fresh;
+  v.seq = w->seq;
+  if (w->comm) comm_mirror_get(w->comm, &v.comm);
   memcpy(v.launches, w->launches, sizeof(v.launches));
   memcpy(v.hist, w->tau_hist, sizeof(v.hist));
   w->dyn = true;
@@ -514,6 +530,11 @@ static int capture_close(lasgd_worker* w, lasgd_graph* gr) {
   w->global_clock = v.gclock;
   w->mom_started = v.mom;
   w->delta_fresh = v.dfresh;
+  w->seq = v.seq;
+  if (w->comm) {
+    comm_mirror_get(w->comm, &gr->comm_after);
+    comm_mirror_set(w->comm, v.comm);
+  }
   memcpy(w->launches, v.launches, sizeof(v.launches));
   memcpy(w->tau_hist, v.hist, sizeof(v.hist));
   if (w->cfg.sync && tau_end != gr->tau0)
@@ -594,8 +615,20 @@ extern "C" int lasgd_graph_launch(lasgd_graph* gr) {
   if (w->lr_len > 1 && (unsigned long long)(w->local_clock + gr->d_clock) > w->lr_len)
     return fail(LASGD_ERR_STATE, "learning-rate table holds %zu clocks, the replay needs %lld", w->lr_len,
                 w->local_clock + gr->d_clock);
+  CommMirror cm = {0, 0, 0, -1};
+  if (w->comm) {
+    // the replayed rounds enter on the end signals of the launch before them: the
+    // communicator must be where it was at capture (relative to its latest launch)
+    comm_mirror_get(w->comm, &cm);
+    const CommMirror& pre = gr->saved.comm;
+    auto lag = [](unsigned long long seq, unsigned long long v) { return v ? (long long)(seq - v) : -1LL; };
+    if (cm.push_slot != pre.push_slot || lag(cm.seq, cm.last_push) != lag(pre.seq, pre.last_push) ||
+        lag(cm.seq, cm.end_seq) != lag(pre.seq, pre.end_seq))
+      return fail(LASGD_ERR_STATE, "the communicator's last launch differs from the capture's; run one eager round");
+    if (cm.seq != w->rd_seq) w->rd_dirty = true;  // launches the descriptor has not seen
+  }
   if (w->rd_dirty) {
-    k_round_set<<<1, 1, 0, w->compute>>>(w->rd, (unsigned long long)w->local_clock, w->seq, w->lr_dev,
+    k_round_set<<<1, 1, 0, w->compute>>>(w->rd, (unsigned long long)w->local_clock, cm.seq, w->lr_dev,
                                          (unsigned long long)w->lr_len, w->snap_idx, w->mom_started ? 1 : 0,
                                          w->delta_fresh ? 1 : 0);
     LASGD_CUDA_TRY(cudaGetLastError());
@@ -611,6 +644,23 @@ extern "C" int lasgd_graph_launch(lasgd_graph* gr) {
   }
   for (int k = 0; k < K_KINDS; ++k) w->launches[k] += gr->d_launches[k];
   for (int t = 0; t < LASGD_TAU_HIST; ++t) w->tau_hist[t] += gr->d_tau_hist[t];
+  if (w->comm) {
+    const CommMirror& pre = gr->saved.comm;
+    const CommMirror& post = gr->comm_after;
+    const unsigned long long d = post.seq - pre.seq;
+    CommMirror now;
+    now.seq = cm.seq + d;
+    now.last_push = post.last_push ? now.seq - (post.seq - post.last_push) : 0;
+    now.end_seq = post.end_seq ? now.seq - (post.seq - post.end_seq) : 0;
+    now.push_slot = post.push_slot;
+    comm_mirror_set(w->comm, now);
+    if (d) {
+      w->seq = now.seq;
+      int rc = comm_record_last(w->comm, (void*)w->compute);
+      if (rc) return rc;
+    }
+    w->rd_seq = now.seq;
+  }
   return LASGD_OK;
 }
 

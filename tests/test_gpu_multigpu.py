@@ -288,6 +288,68 @@ def _w_sgd_ar_bucketed(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_graph_replay(rank, world, port):
+    """Multi-rank graph replay (device round descriptor carries the launch sequence and
+    the snapshot slot): fused rounds replayed from a CUDA graph — K8 push (mirror at P=2,
+    staged at P>=3) and K7 one-shot — are bit-identical to the same steps issued one by
+    one and to the oracle's deterministic loop, on every rank."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+    from paper_2203_13085_b200 import _native as N
+
+    _init(rank, world, port)
+    n = 65_541
+    x0 = _vec(5, n)
+    gsrc = [[_vec(900 + 10 * i + r, n) for r in range(world)] for i in range(2)]
+    sgd = L.SgdConfig(0.9, 0.0, 1e-4, True)
+    for algo in (N.ALGO_PUSH, N.ALGO_ONESHOT):
+        for k, alpha in ((1, 1.0), (2, 0.5)):
+            pre, S, R, post = k, 4 * k, 3, k
+            total = pre + S * R + post
+            grads = [torch.from_numpy(gsrc[i][rank]).cuda() for i in range(2)]
+
+            def run(graphed):
+                comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
+                x = torch.from_numpy(x0.copy()).cuda()
+                compute = torch.cuda.Stream()
+                with torch.cuda.stream(compute):
+                    w = L.LASGDWorker(x, grads[0], comm=comm, sync_period=k, alpha=alpha, mode="pull", sgd=sgd,
+                                      lr=0.05, algo=algo, pipeline="fused", compute_stream=compute)
+                    t = 0
+                    for _ in range(pre if graphed else total):
+                        w.g = grads[t % 2]
+                        w.step()
+                        t += 1
+                    if graphed:
+                        graph = w.capture([grads[(pre + i) % 2] for i in range(S)])
+                        for _ in range(R):
+                            graph.replay()
+                        t += S * R
+                        for _ in range(post):
+                            w.g = grads[t % 2]
+                            w.step()
+                            t += 1
+                    w.drain()
+                torch.cuda.synchronize()
+                out = (x.cpu().numpy(), w.state.x_snapshot.cpu().numpy(), w.state.local_clock, w.state.global_clock,
+                       comm.launches())
+                w.close()
+                dist.barrier()
+                comm.close()
+                return out
+
+            a, b = run(True), run(False)
+            assert a[2:4] == b[2:4] == (total, total // k), (a[2:], b[2:])
+            assert _same_bits(a[0], b[0]) and _same_bits(a[1], b[1]), (algo, k, rank)
+            gl = np.stack([np.stack(gsrc[t % 2]) for t in range(total)])
+            ref, _, _, _ = O.run_lasgd_pull(x0, gl, [0.05] * total, world, k, alpha,
+                                            sgd=O.SgdConfig(0.05, 0.9, 0.0, 1e-4, True))
+            assert _same_bits(a[0], ref[rank]), (algo, k, rank)
+    dist.destroy_process_group()
+
+
 def _w_full_size(rank, world, port):
     """The bench's configuration at BASELINE size: ResNet-50's n, Nesterov momentum +
     weight decay, sync period 1, fused pipeline with the AUTO algorithm (mirror push at
@@ -515,6 +577,11 @@ def test_sgd_ar_worker_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_sgd_ar_bucketed_bit_exact():
     _spawn(_w_sgd_ar_bucketed)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_graph_replay_multi_rank_bit_exact():
+    _spawn(_w_graph_replay)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
