@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--train-warmup", type=int, default=4)
     ap.add_argument("--flat-align", type=int, default=256, help="byte alignment of every tensor in the flat buffer")
     ap.add_argument("--bucket-mb", type=int, default=25, help="gradient bucket size of the bucketed SGD-AR / DDP legs")
+    ap.add_argument("--bucket-ctas", type=int, default=0, help="CTAs of each bucketed SGD-AR launch (0: 2 per SM)")
+    ap.add_argument("--legs", default="", help="comma list: run only these training legs (and their baselines)")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="training leg: eager fwd/bwd instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -917,7 +919,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
                 return one, lambda: None, lambda: flat.bind_grads(own_g)
             if kind == "bucketed":
                 w = L.BucketedSGDARWorker(flat, tcomm, sgd=sgd, lr=lr, bucket_bytes=args.bucket_mb << 20,
-                                          compute_stream=compute)
+                                          compute_stream=compute, nblocks=args.bucket_ctas)
 
                 def one():
                     fwd_bwd_zero()
@@ -970,6 +972,10 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
                      "nosync_eager": (nosync_eager_leg(), "nosync_eager"),
                      "sgd_ar_bucketed": (sgd_ar_leg("bucketed"), "nosync_eager"),
                      "ddp_nccl": (sgd_ar_leg("ddp"), "nosync_eager")})
+    if args.legs:
+        keep = set(args.legs.split(","))
+        keep |= {legs[k][1] for k in keep if k in legs}
+        legs = {k: v for k, v in legs.items() if k in keep}
     times = {k: [] for k in legs}
     hists = {}
     B, R = args.train_block, args.train_reps
@@ -1033,11 +1039,12 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         if name in hists:
             e["tau_histogram"] = hists[name]
         out[name] = e
-    main = out[args.pipeline]
-    out["images_per_s_lasgd"] = main["images_per_s"]
-    out["images_per_s_nosync"] = out["nosync"]["images_per_s"]
-    out["exposed_sync_ms_per_step"] = main["exposed_sync_ms_per_step"]
-    out["exposed_sync_frac"] = main["exposed_sync_frac"]
+    if args.pipeline in out and "nosync" in out:
+        main = out[args.pipeline]
+        out["images_per_s_lasgd"] = main["images_per_s"]
+        out["images_per_s_nosync"] = out["nosync"]["images_per_s"]
+        out["exposed_sync_ms_per_step"] = main["exposed_sync_ms_per_step"]
+        out["exposed_sync_frac"] = main["exposed_sync_frac"]
     return out
 
 
