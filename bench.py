@@ -80,7 +80,10 @@ def parse():
     ap.add_argument("--kernels-only", action="store_true", help="short run for ncu: sync path only")
     ap.add_argument("--no-virtual", action="store_true", help="skip the virtual-rank (P=2/4/8 on one GPU) kernels")
     ap.add_argument("--no-sync-graph", action="store_true",
-                    help="issue the timed steps one by one instead of replaying them as one CUDA graph")
+                    help="N=1: issue the timed steps one by one instead of replaying them as one CUDA graph")
+    ap.add_argument("--sync-graph", action="store_true",
+                    help="N>1: replay the timed steps as one CUDA graph (fused pipeline; ~2.5%% slower per round "
+                         "than eager launches behind the hold kernel, DESIGN.md §12)")
     return ap.parse_args()
 
 
@@ -539,17 +542,18 @@ def main():
 
     hold = Hold(N)
 
-    # ---------------- value: HBM-resident gradients, device-timed.  The K steps replay as
-    # ONE CUDA graph (LASGDWorker.capture: the deterministic loop reads its per-round
-    # scalars — rate, first step, snapshot slot, launch sequence — from the device round
-    # descriptor; fused pipeline at N>1).  The timed region is enqueued behind a hold
-    # kernel and released at once, so host jitter cannot open gaps in it.
+    # ---------------- value: HBM-resident gradients, device-timed.  At N=1 the K steps
+    # replay as ONE CUDA graph (LASGDWorker.capture: the deterministic loop reads its
+    # per-round scalars — rate, first step, snapshot slot, launch sequence — from the
+    # device round descriptor; --sync-graph does the same at N>1).  The timed region is
+    # enqueued behind a hold kernel and released at once, so host jitter cannot open gaps.
     with torch.cuda.stream(compute):
         w = make_worker(False)
         run_sync_path(w, args.warmup, lambda t: grads[t % 2])
         w.drain()
         graph = None
-        if not args.no_sync_graph and (args.pipeline == "fused" or world == 1) and args.steps % args.sync_period == 0:
+        use_graph = (world == 1 and not args.no_sync_graph) or (args.sync_graph and args.pipeline == "fused")
+        if use_graph and args.steps % args.sync_period == 0:
             graph = w.capture([grads[t % 2] for t in range(args.steps)])
             graph.replay()  # graph upload; one more untimed pass
             w.drain()

@@ -65,21 +65,22 @@ struct CommArgs {
 // Per-CTA copy of the dynamic launch arguments (read once by thread 0 at entry).
 struct DynComm {
   unsigned long long seq;
-  int cur;
+  DynView v;
 };
 static __shared__ DynComm s_dyn;
 
+// One round trip: thread 0 loads every field this launch needs, the CTA shares them.
 __device__ __forceinline__ void dyn_comm_begin(const CommArgs& a) {
   if (a.adv.rd == nullptr) return;
   if (threadIdx.x == 0) {
     s_dyn.seq = __ldcg(&a.adv.rd->seq) + 1ull;
-    s_dyn.cur = __ldcg(&a.adv.rd->snap_idx);
+    s_dyn.v = dyn_read(a.adv.rd);
   }
   __syncthreads();
 }
 __device__ __forceinline__ unsigned long long cseq(const CommArgs& a) { return a.adv.rd ? s_dyn.seq : a.seq; }
 __device__ __forceinline__ uint32_t cepoch(const CommArgs& a) { return a.adv.rd ? (uint32_t)s_dyn.seq : a.epoch; }
-__device__ __forceinline__ int ccur(const CommArgs& a) { return a.adv.rd ? s_dyn.cur : a.cur; }
+__device__ __forceinline__ int ccur(const CommArgs& a) { return a.adv.rd ? s_dyn.v.cur : a.cur; }
 __device__ __forceinline__ uint32_t cprev_push(const CommArgs& a) {
   return a.adv.rd ? (uint32_t)(s_dyn.seq - 1ull) : a.prev_push;
 }
@@ -97,7 +98,7 @@ __device__ __forceinline__ unsigned* cend(const CommArgs& a) {
 }
 // rank q's snapshot slot `slot` (dynamic launches), or the launch's slot (static)
 __device__ __forceinline__ const char* csnap(const CommArgs& a, int q) {
-  return a.snap[q] + ((a.adv.rd && s_dyn.cur) ? a.slot_stride : 0);
+  return a.snap[q] + ((a.adv.rd && s_dyn.v.cur) ? a.slot_stride : 0);
 }
 __device__ __forceinline__ const char* cslot(const CommArgs& a, int q, int slot) {
   return a.snap[q] + (slot ? a.slot_stride : 0);
@@ -106,7 +107,7 @@ __device__ __forceinline__ const char* cslot(const CommArgs& a, int q, int slot)
 template <typename T>
 __device__ __forceinline__ SgdCoef<T> ccoef(const CommArgs& a, const SgdCoef<T>& c) {
   SgdCoef<T> r = c;
-  if (a.adv.rd) dyn_coef(r, dyn_read(a.adv.rd));
+  if (a.adv.rd) dyn_coef(r, s_dyn.v);  // after dyn_comm_begin
   return r;
 }
 
@@ -238,18 +239,7 @@ __device__ inline void publish_done(const CommArgs& a) {
       a.done_ctr[slot] = 0u;
       unsigned long long* tq = ctile(a);
       if (tq) tq[0] = tq[1] = 0ull;  // every CTA has left its tile loops
-      if (a.adv.rd) {
-        DevRound* r = a.adv.rd;
-        r->clock += (unsigned long long)a.adv.steps;
-        r->seq += (unsigned long long)a.adv.seq_inc;
-        if (a.adv.steps && a.adv.has_mom) r->mom_started = 1;
-        if (a.adv.close) {
-          r->snap_idx ^= 1;
-          r->delta_fresh = a.adv.has_delta;
-        } else if (a.adv.steps) {
-          r->delta_fresh = 0;
-        }
-      }
+      if (a.adv.rd) dyn_apply(a.adv.rd, a.adv);
       __threadfence_system();
       st_release_sys64(a.done_seq, seq);
     }

@@ -18,7 +18,7 @@ int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int
     }                                                                                               \
     return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);                                  \
   }
-  if (P == 2) {  // mirror form
+  if (P == 2) {  // mirror form: one phase, no barrier inside the launch, so no cooperative launch
     auto kern = k_push_mirror<T, VIRTUAL, sizeof(T) == 4 ? 2 : 1>;
     CommArgs aa = a;
     if (!VIRTUAL) {
@@ -26,7 +26,7 @@ int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int
       if ((int)grid.x > cap) grid.x = cap;
       aa.nblocks = grid.x;
     }
-    return launch_kernel(!VIRTUAL, kern, grid, threads, s, aa, f);
+    return launch_kernel(false, kern, grid, threads, s, aa, f);
   }
   switch (P) {
     LASGD_PCASE(3)

@@ -148,6 +148,7 @@ __device__ __forceinline__ unsigned pull_elem(T neg_alpha, T& xv, T sv, T zv) {
 struct DevRound {
   unsigned long long clock;         // local steps taken (NodeState.local_clock)
   unsigned long long seq;           // communicator launches issued (epoch of the next one - 1)
+  double lr_now;                    // lr[min(clock, lr_len - 1)]: one load at kernel entry
   const double* lr;                 // learning rate per local clock
   unsigned long long lr_len;        // clock >= lr_len reads the last entry
   int snap_idx;                     // current snapshot slot
@@ -170,17 +171,33 @@ struct DynView {
   int first, reset, cur;
 };
 
-// Every thread reads the descriptor (one L2 line, written by the previous kernel).
+// Every thread reads the descriptor (independent loads of one L2 line written by the
+// previous kernel: a single round trip).
 __device__ __forceinline__ DynView dyn_read(const DevRound* r) {
   DynView v;
-  const unsigned long long k = __ldcg(&r->clock);
-  const unsigned long long len = __ldcg(&r->lr_len);
-  const double* lr = (const double*)__ldcg((const unsigned long long*)&r->lr);
-  v.lr = __ldcg(lr + (k < len ? k : len - 1));
+  v.lr = __ldcg(&r->lr_now);
   v.first = !__ldcg(&r->mom_started);
   v.reset = __ldcg(&r->delta_fresh);
   v.cur = __ldcg(&r->snap_idx);
   return v;
+}
+
+// Advance by `ad` (the last CTA of a launch): clock, launch count, flags, and the rate of
+// the new clock.
+__device__ __forceinline__ void dyn_apply(DevRound* r, const RoundAdv& ad) {
+  r->clock += (unsigned long long)ad.steps;
+  r->seq += (unsigned long long)ad.seq_inc;
+  if (ad.steps) {
+    const unsigned long long k = r->clock, len = r->lr_len;
+    r->lr_now = r->lr[k < len ? k : len - 1];
+  }
+  if (ad.steps && ad.has_mom) r->mom_started = 1;
+  if (ad.close) {
+    r->snap_idx ^= 1;
+    r->delta_fresh = ad.has_delta;
+  } else if (ad.steps) {
+    r->delta_fresh = 0;
+  }
 }
 
 template <typename T>
@@ -200,15 +217,7 @@ __device__ __forceinline__ void dyn_advance(const RoundAdv& ad, unsigned total) 
     DevRound* r = ad.rd;
     if (atomicAdd(&r->arrive, 1u) == total - 1u) {
       r->arrive = 0u;
-      r->clock += (unsigned long long)ad.steps;
-      r->seq += (unsigned long long)ad.seq_inc;
-      if (ad.steps && ad.has_mom) r->mom_started = 1;
-      if (ad.close) {
-        r->snap_idx ^= 1;
-        r->delta_fresh = ad.has_delta;
-      } else if (ad.steps) {
-        r->delta_fresh = 0;
-      }
+      dyn_apply(r, ad);
       __threadfence();
     }
   }

@@ -284,6 +284,12 @@ int sgd_step_snapshot(int dtype, void* x, const void* g, void* m, void* delta, v
 template <typename T, int U>
 __global__ void __launch_bounds__(kThreads, 4) k_sgd_dyn(SgdOp<T> op, T* snap0, T* snap1, size_t n,
                                                         unsigned long long* nonfinite, RoundAdv adv, bool aligned) {
+  // Programmatic dependent launch: let the next step's kernel get its CTAs onto the SMs
+  // now (they wait in griddepcontrol.wait below until this grid has completed and its
+  // writes are visible), then wait for the previous step's grid the same way.  Saves the
+  // launch ramp between back-to-back steps of a replayed graph.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const DynView v = dyn_read(adv.rd);
   dyn_coef(op.c, v);
   op.snap = snap0 == nullptr ? nullptr : (v.cur ? snap0 : snap1);  // next slot = 1 - cur
@@ -313,9 +319,17 @@ int sgd_dyn_t(void* x, const void* g, void* m, void* delta, void* const* snaps, 
   const size_t work = npack > (size_t)kThreads ? npack : (size_t)kThreads;
   const bool al = aligned16(x) && aligned16(g) && (!op.c.use_mom || aligned16(m)) &&
                   (!op.c.use_delta || aligned16(delta)) && (!snaps || (aligned16(snaps[0]) && aligned16(snaps[1])));
-  k_sgd_dyn<T, SgdOp<T>::U><<<stream_grid(work, kThreads), kThreads, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      op, snaps ? (T*)snaps[0] : nullptr, snaps ? (T*)snaps[1] : nullptr, n, nf, adv, al);
-  LASGD_CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(stream_grid(work, kThreads));
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = reinterpret_cast<cudaStream_t>(s);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LASGD_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sgd_dyn<T, SgdOp<T>::U>, op, snaps ? (T*)snaps[0] : nullptr,
+                                    snaps ? (T*)snaps[1] : nullptr, n, nf, adv, al));
   return LASGD_OK;
 }
 

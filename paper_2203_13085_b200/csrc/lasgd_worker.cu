@@ -460,6 +460,7 @@ __global__ void k_round_set(DevRound* r, unsigned long long clock, unsigned long
   r->seq = seq;
   r->lr = lr;
   r->lr_len = lr_len;
+  r->lr_now = lr[clock < lr_len ? clock : lr_len - 1];
   r->snap_idx = snap_idx;
   r->mom_started = mom_started;
   r->delta_fresh = delta_fresh;
