@@ -439,6 +439,31 @@ class SGDARWorker:
         self._finite.check(self.x.numel())
 
 
+def plan_buckets(n: int, tensors, bucket_bytes: int, esize: int):
+    """Gradient buckets of ``BucketedSGDARWorker``: contiguous ranges covering [0, n) from
+    the END of the flat vector (backward produces the last layers' gradients first), at
+    most ``bucket_bytes`` each, every boundary a 16-byte multiple (the kernels' pack
+    alignment).  ``tensors`` = (offset, numel) of every parameter.  Returns (buckets as
+    (lo, hi) in launch order, the buckets each tensor overlaps, the number of tensors each
+    bucket waits for)."""
+    wpack = max(1, 16 // esize)
+    cap = max(wpack, bucket_bytes // esize // wpack * wpack)
+    buckets = []
+    hi = n
+    while hi > 0:
+        lo = max(0, hi - cap) // wpack * wpack
+        buckets.append((lo, hi))
+        hi = lo
+    member, need = [], [0] * len(buckets)
+    for off, cnt in tensors:
+        end = off + cnt
+        bs = [b for b, (lo, hi) in enumerate(buckets) if lo < end and off < hi]
+        member.append(bs)
+        for b in bs:
+            need[b] += 1
+    return buckets, member, need
+
+
 class BucketedSGDARWorker:
     """SGD-AR (optimizer.py:214-242, ``sync_allreduce_sgd_round``) as a data-parallel
     trainer runs it: the gradient all-reduce is split into buckets in reverse parameter
@@ -480,28 +505,9 @@ class BucketedSGDARWorker:
         self.local_clock = 0
         self.launches = collections.Counter()
         self._slot = 0
-        # buckets: contiguous ranges from the end of the flat vector (backward produces the
-        # last layers' gradients first), boundaries on 16-byte multiples
-        esize = flat.x.element_size()
-        wpack = 16 // esize
-        cap = max(wpack, bucket_bytes // esize // wpack * wpack)
-        n = flat.numel
-        self.buckets = []
-        hi = n
-        while hi > 0:
-            lo = max(0, hi - cap)
-            lo = lo // wpack * wpack
-            self.buckets.append((lo, hi))
-            hi = lo
-        # bucket membership of every parameter (a tensor may straddle a boundary)
-        self._param_buckets = []
-        self._need = [0] * len(self.buckets)
-        for p, off in zip(flat.params, flat.offsets):
-            end = off + p.numel()
-            bs = [b for b, (lo, hi) in enumerate(self.buckets) if lo < end and off < hi]
-            self._param_buckets.append(bs)
-            for b in bs:
-                self._need[b] += 1
+        self.buckets, self._param_buckets, self._need = plan_buckets(
+            flat.numel, [(off, p.numel()) for p, off in zip(flat.params, flat.offsets)], bucket_bytes,
+            flat.x.element_size())
         self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(i)) for i, p in enumerate(flat.params)]
         self._reset_step()
         flat.bind_grads(self.grad_buffer)

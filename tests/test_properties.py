@@ -118,3 +118,35 @@ def test_degenerate_inputs_raise_like_the_reference():
     with pytest.raises(ValueError, match="num_chunks must be positive"):
         partition_chunks(5, 0)
     assert [tuple(b) for b in partition_chunks(2, 5).bounds] == [(0, 1), (1, 2), (2, 2), (2, 2), (2, 2)]
+
+
+def test_sgd_ar_bucket_plan_covers_the_vector_in_reverse():
+    """BucketedSGDARWorker's buckets: contiguous, disjoint, cover [0, n) from the end,
+    16-byte aligned boundaries, at most bucket_bytes each; every tensor is counted in
+    every bucket it overlaps (CPU, no device)."""
+    import random
+
+    from paper_2203_13085_b200.engine import plan_buckets
+
+    rng = random.Random(3)
+    for _ in range(200):
+        sizes = [rng.randint(1, 5000) for _ in range(rng.randint(1, 30))]
+        align = rng.choice([1, 64])
+        offs, off = [], 0
+        for c in sizes:
+            off = (off + align - 1) // align * align
+            offs.append(off)
+            off += c
+        n = off
+        bb = rng.choice([16, 100, 4096, 40_000, 1 << 30])
+        buckets, member, need = plan_buckets(n, list(zip(offs, sizes)), bb, 4)
+        assert buckets[0][1] == n and buckets[-1][0] == 0
+        for (lo, hi), (lo2, hi2) in zip(buckets, buckets[1:]):
+            assert hi2 == lo and lo2 < hi2
+        for lo, hi in buckets:
+            assert lo % 4 == 0 and 0 < hi - lo <= max(4, bb // 4 // 4 * 4) + 3
+        for b in range(len(buckets)):
+            lo, hi = buckets[b]
+            assert need[b] == sum(1 for o, c in zip(offs, sizes) if o < hi and lo < o + c)
+        for (o, c), bs in zip(zip(offs, sizes), member):
+            assert bs and all(buckets[b][0] < o + c and o < buckets[b][1] for b in bs)
