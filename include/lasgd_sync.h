@@ -207,13 +207,14 @@ int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len);
 unsigned long long lasgd_comm_bytes_per_node(lasgd_comm* c, int algo);
 int lasgd_comm_resolve_algo(lasgd_comm* c, int algo);
 /* Bucketed SGD-AR (optimizer.py:214-242; the all-reduce split into buckets that a
- * trainer launches as backward completes them): one-shot mean over NVLink of every
- * rank's gradient in slot `snap_slot` over elements [off, off + len) and the local step
- * of x[off, off + len) (and m) with it.  Each element is summed in the ring order of its
+ * trainer launches as backward completes them): the mean over NVLink of every rank's
+ * gradient in slot `snap_slot` over elements [off, off + len) and the local step of
+ * x[off, off + len) (and m) with it — one-shot, or two-shot (`algo`; AUTO picks by the
+ * bucket's size like the all-reduce).  Each element is summed in the ring order of its
  * chunk of the WHOLE vector (collective.py:183-200), so the result is bit-identical to
  * one lasgd_comm_fused_round(mode 2) for any bucketing.  off must be 16-byte aligned in
  * elements.  A launch like lasgd_comm_allreduce (sequence numbers, query / wait). */
-int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off, size_t len, void* x, void* m,
+int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off, size_t len, int algo, void* x, void* m,
                             const lasgd_sgd_params* sgd, int nblocks, unsigned long long* nonfinite, void* stream,
                             unsigned long long* seq);
 /* The algorithm lasgd_comm_fused_round runs for `algo`: AUTO resolves to PUSH (the

@@ -139,7 +139,7 @@ SIGNATURES = {
                                     _ULLP]),
     "lasgd_fused_round_virtual": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _SZ, _I, ctypes.POINTER(SgdParams), _D,
                                        _I, _I, _P, _P]),
-    "lasgd_comm_sgd_ar_range": (_I, [_P, _I, _SZ, _SZ, _P, _P, ctypes.POINTER(SgdParams), _I, _P, _P, _ULLP]),
+    "lasgd_comm_sgd_ar_range": (_I, [_P, _I, _SZ, _SZ, _I, _P, _P, ctypes.POINTER(SgdParams), _I, _P, _P, _ULLP]),
     "lasgd_comm_query": (_I, [_P, ctypes.c_ulonglong]),
     "lasgd_comm_stream_wait": (_I, [_P, ctypes.c_ulonglong, _P]),
     "lasgd_comm_wait": (_I, [_P, ctypes.c_ulonglong, _D]),

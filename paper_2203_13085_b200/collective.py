@@ -443,8 +443,8 @@ class P2PCommunicator:
         return seq.value
 
     def sgd_ar_range(self, slot: int, off: int, length: int, x: torch.Tensor, lr: float, *, m=None, momentum=0.0,
-                     dampening=0.0, weight_decay=0.0, nesterov=False, first_step=False, nblocks: int = 0,
-                     nonfinite=None, stream=None) -> int:
+                     dampening=0.0, weight_decay=0.0, nesterov=False, first_step=False, algo: int = N.ALGO_AUTO,
+                     nblocks: int = 0, nonfinite=None, stream=None) -> int:
         """One bucket of a bucketed SGD-AR step (optimizer.py:214-242): the ring-order
         mean over all ranks of gradient slot ``slot`` on elements [off, off + length), and
         the local step of ``x`` (and ``m``) there — bit-identical to the whole-vector round
@@ -453,7 +453,7 @@ class P2PCommunicator:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         p = K.sgd_params(lr, momentum, dampening, weight_decay, nesterov, first_step)
         seq = ctypes.c_ulonglong()
-        N.check(N.lib().lasgd_comm_sgd_ar_range(self._h, slot, int(off), int(length), K._ptr(x), K._ptr(m),
+        N.check(N.lib().lasgd_comm_sgd_ar_range(self._h, slot, int(off), int(length), int(algo), K._ptr(x), K._ptr(m),
                                                 ctypes.byref(p), int(nblocks), K._ptr(nonfinite),
                                                 ctypes.c_void_p(s.cuda_stream), ctypes.byref(seq)),
                 "lasgd_comm_sgd_ar_range")

@@ -159,6 +159,16 @@ __device__ __forceinline__ int chunk_of(size_t j, const size_t (&bnd)[P + 1]) {
   return c;
 }
 
+// Ring-order start of element j of this launch: its chunk of the whole vector
+// (== the owner chunk for a whole-vector launch).
+template <int P>
+__device__ __forceinline__ int rot_of(const CommArgs& a, size_t j) {
+  int c = 0;
+#pragma unroll
+  for (int k = 1; k < P; ++k) c += (j >= chunk_bound_local(a, P, k));
+  return c;
+}
+
 // Sum v[c], v[c+1], ..., v[c-1] (mod P) left to right: the reference ring order.
 template <typename T, int P>
 __device__ __forceinline__ T rot_sum(const T (&v)[P], int c) {

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
   const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
   const bool load_m = f.c.use_mom && !f.c.first, load_d = f.c.use_delta && !f.c.reset;
   const bool store_d = f.c.use_delta && f.mode == 0;
+  const bool ranged = a.n_glob != 0;  // bucket of a bucketed SGD-AR step
   auto element = [&](T& xv, T gv, T& mv, T& dv, T sv, T zb) {
     if (f.mode == 2) {  // SGD-AR: the local step with the mean gradient
       bad += sgd_elem(f.c, xv, zb, mv, dv);
@@ -223,6 +224,9 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
             if (pu < p1) {
               const size_t j = pu * W;
               Pack<T> z;
+              // ring-order start: the owner chunk, or for a bucket (sub-range launch) the
+              // element's chunk of the whole vector
+              const int r0 = ranged ? rot_of<P>(a, j) : rank, r1 = ranged ? rot_of<P>(a, j + W - 1) : rank;
 #pragma unroll
               for (int k = 0; k < W; ++k) {
                 T lane[P];
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
                 T sv = lane[0];
 #pragma unroll
                 for (int q = 1; q < P; ++q) sv = (q == rank) ? lane[q] : sv;
-                z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+                z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, r0 == r1 ? r0 : rot_of<P>(a, j + k)));
                 element(vx[u].v[k], vg[u].v[k], vm[u].v[k], vd[u].v[k], sv, z.v[k]);
               }
               st_plain(own + j, z);
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound
         const size_t he = cp0 * W < ce ? cp0 * W : ce;
         const size_t ts = cp1 * W > he ? cp1 * W : he;
         auto scalar = [&](size_t j) {
-          const T zb = mean_div<T, P>(ordered_sum<T, P>(src, rank, j));
+          const T zb = mean_div<T, P>(ordered_sum<T, P>(src, ranged ? rot_of<P>(a, j) : rank, j));
           own[j] = zb;
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
           element(xv, f.mode == 2 ? T(0) : g[j], mv, dv, snap_own[j], zb);

@@ -817,9 +817,9 @@ int comm_fused_round_dyn(lasgd_comm* c, int snap_slot, int algo, void* x, const 
 // rank's gradient over NVLink and the local step of x[off, off + len) with it.  Every
 // element is summed in the rotation of its chunk of the whole vector, so any bucketing
 // gives the bits of the one-launch round.
-extern "C" int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off, size_t len, void* x, void* m,
-                                       const lasgd_sgd_params* sgd, int nblocks, unsigned long long* nonfinite,
-                                       void* stream, unsigned long long* seq) {
+extern "C" int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off, size_t len, int algo, void* x,
+                                       void* m, const lasgd_sgd_params* sgd, int nblocks,
+                                       unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   if (c->world < 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round needs P >= 2");
   if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
@@ -853,13 +853,18 @@ extern "C" int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off,
   a.nonfinite = nonfinite;
   c->push_slot = -1;
   c->end_seq = 0;
+  // one-shot, or two-shot for large buckets at P >= 3 (the bucket's own partition decides
+  // who reduces what; the summation order stays the whole vector's)
+  algo = resolve_algo(algo == LASGD_ALGO_PUSH ? LASGD_ALGO_AUTO : algo, c->world, len * c->elem);
+  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
+  a.phases = 3;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (c->dtype == LASGD_F32)
     rc = launch_fused<float, false>(c->world, a, make_fused<float>(1, xs, gs, m ? ms : nullptr, nullptr, ns, sgd, 1.0, 2),
-                                    dim3(nblocks, 1), c->threads, cs, LASGD_ALGO_ONESHOT);
+                                    dim3(nblocks, 1), c->threads, cs, algo);
   else
     rc = launch_fused<double, false>(c->world, a, make_fused<double>(1, xs, gs, m ? ms : nullptr, nullptr, ns, sgd, 1.0, 2),
-                                     dim3(nblocks, 1), c->threads, cs, LASGD_ALGO_ONESHOT);
+                                     dim3(nblocks, 1), c->threads, cs, algo);
   if (rc) return rc;
   LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
   if (seq) *seq = s;

@@ -483,7 +483,7 @@ class BucketedSGDARWorker:
     def __init__(self, flat, comm, *, sgd: Optional[SgdConfig] = None, schedule: Optional[LrSchedule] = None,
                  lr: Optional[float] = None, bucket_bytes: int = 25 << 20,
                  compute_stream: Optional[torch.cuda.Stream] = None, side_stream: Optional[torch.cuda.Stream] = None,
-                 nblocks: int = 0):
+                 nblocks: int = 0, algo: int = N.ALGO_AUTO):
         if (schedule is None) == (lr is None):
             raise ValueError("give exactly one of schedule / lr")
         if comm is None or comm.world < 2:
@@ -500,6 +500,7 @@ class BucketedSGDARWorker:
         self.compute = compute_stream if compute_stream is not None else torch.cuda.current_stream(flat.x.device)
         self.side = side_stream if side_stream is not None else comm.stream
         self.nblocks = nblocks
+        self.algo = algo
         self.m = torch.empty_like(flat.x) if self.sgd.momentum != 0 else None
         self._finite = _FiniteMonitor(flat.x.device)
         self.local_clock = 0
@@ -545,7 +546,7 @@ class BucketedSGDARWorker:
         s = self.sgd
         self.comm.sgd_ar_range(self._slot, lo, hi - lo, self.x, self._step_lr, m=self.m, momentum=s.momentum,
                                dampening=s.dampening, weight_decay=s.weight_decay, nesterov=s.nesterov,
-                               first_step=self.local_clock == 0, nblocks=self.nblocks,
+                               first_step=self.local_clock == 0, algo=self.algo, nblocks=self.nblocks,
                                nonfinite=self._finite.counter, stream=self.side)
         self.launches["sgd_ar_bucket"] += 1
 

@@ -227,7 +227,10 @@ def _w_sgd_ar_bucketed(rank, world, port):
     x0 = _vec(3, n)
     grads = np.stack([np.stack([_vec(700 * t + r, n) for r in range(world)]) for t in range(steps)])
     etas = np.array([0.1, 0.05, 0.2, 0.01, 0.07, 0.03])
-    for sgd in (None, L.SgdConfig(0.9, 0.0, 1e-4, True)):
+    from paper_2203_13085_b200 import _native as N
+
+    for sgd, algo in ((None, N.ALGO_ONESHOT), (L.SgdConfig(0.9, 0.0, 1e-4, True), N.ALGO_ONESHOT),
+                      (L.SgdConfig(0.9, 0.0, 1e-4, True), N.ALGO_TWOSHOT)):
         for bucket_bytes in (16_000, 65_536 * 4, 1 << 30):
             comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
             flat = _Flat(n)
@@ -235,7 +238,7 @@ def _w_sgd_ar_bucketed(rank, world, port):
             compute = torch.cuda.Stream()
             with torch.cuda.stream(compute):
                 w = L.BucketedSGDARWorker(flat, comm, sgd=sgd, lr=1.0, bucket_bytes=bucket_bytes,
-                                          compute_stream=compute)
+                                          compute_stream=compute, algo=algo)
                 for t in range(steps):
                     w.lr = float(etas[t])
                     w.grad_buffer.copy_(torch.from_numpy(grads[t, rank]))
@@ -244,7 +247,7 @@ def _w_sgd_ar_bucketed(rank, world, port):
             cfg = None if sgd is None else O.SgdConfig(1.0, sgd.momentum, sgd.dampening, sgd.weight_decay,
                                                        sgd.nesterov)
             ref, _ = O.run_sgd_ar(x0, grads, etas, world, sgd=cfg)
-            assert _same_bits(flat.x.cpu().numpy(), ref), (sgd, bucket_bytes, rank)
+            assert _same_bits(flat.x.cpu().numpy(), ref), (sgd, algo, bucket_bytes, rank)
             assert w.launches["sgd_ar_bucket"] == steps * len(w.buckets)
             w.close()
             dist.barrier()
