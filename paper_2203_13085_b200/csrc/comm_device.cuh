@@ -241,7 +241,12 @@ __device__ bool cta_barrier(const CommArgs& a, int phase, int b, int rank) {
 __device__ inline void publish_done(const CommArgs& a) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    // device scope is enough here: the counter is device-local, and the host only learns
+    // "launch done" from done_seq (every data read by the host or another stream is
+    // ordered by the launch's event); the last CTA's system-scope fence + release below
+    // publishes it.  (Peers' data visibility is the rank-level signals' job, which keep
+    // their per-CTA system-scope fences.)
+    __threadfence();
     const unsigned long long seq = cseq(a);
     const unsigned slot = (unsigned)(seq % kDoneSlots);
     const unsigned prev = atomicAdd(&a.done_ctr[slot], 1u);
