@@ -70,3 +70,19 @@ def test_fused_algo_name_matches_the_communicator():
         for n in (262_144, 2_097_152, 3_504_872, 11_181_642, 25_557_032):
             got = N.lib().lasgd_resolve_fused_algo_for(P, 4 * n)
             assert {1: "oneshot", 2: "twoshot", 3: "push"}[got] == bench.fused_algo_name(P, n), (P, n)
+
+
+def test_exposed_stats_pairs_blocks_and_ignores_level_switches():
+    """The training legs' exposed-sync estimator: median of paired per-repetition
+    differences; a level switch of the whole step (both legs shift together) cancels,
+    one switch between the two blocks of a repetition is an outlier the median ignores."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    base = [51.30] * 12 + [51.70] * 12
+    leg = [b + 0.08 for b in base]
+    leg[5] += 0.40  # the switch fell between the two blocks of repetition 5
+    d = bench._exposed_stats(leg, base)
+    assert abs(d["median"] - 0.08) < 1e-9
+    assert d["ci95"][0] - 1e-9 <= 0.08 <= d["ci95"][1] + 1e-9 and d["ci95_halfwidth"] < 0.01
+    assert d["blocks"] == 24
