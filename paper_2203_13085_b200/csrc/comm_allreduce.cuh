@@ -11,6 +11,7 @@ namespace lasgd {
 // ------------------------------------------------------------------ one-shot (K2)
 template <typename T, int P, bool VIRTUAL, int U>
 __global__ void __launch_bounds__(256, 2) k_oneshot(CommArgs a) {
+  pdl_entry();
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int b = blockIdx.x;
@@ -211,6 +212,7 @@ __device__ __forceinline__ unsigned reduce_own_chunk(const CommArgs& a, int b, i
 
 template <typename T, int P, bool VIRTUAL, int U, int UAG>
 __global__ void __launch_bounds__(256, 2) k_twoshot(CommArgs a) {
+  pdl_entry();
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int b = blockIdx.x;

@@ -34,6 +34,7 @@ struct FusedRound {
 
 template <typename T, int P, bool VIRTUAL, int U>
 __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs a, FusedRound<T> f) {
+  pdl_entry();
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int vr = VIRTUAL ? (int)blockIdx.y : 0;
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : 2)) k_fused_round(CommArgs 
 // work queues.  Virtual ranks run phase 1 and phase 2 as two launches.
 template <typename T, int P, bool VIRTUAL, int U>
 __global__ void __launch_bounds__(256, 2) k_fused_twoshot(CommArgs a, FusedRound<T> f) {
+  pdl_entry();
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int vr = VIRTUAL ? (int)blockIdx.y : 0;

@@ -15,9 +15,17 @@ namespace lasgd {
 
 template <typename... Args>
 int launch_kernel(bool coop, void (*kernel)(Args...), dim3 grid, int threads, cudaStream_t s, Args... args) {
-  if (!coop) {
-    kernel<<<grid, threads, 0, s>>>(args...);
-    LASGD_CUDA_TRY(cudaGetLastError());
+  if (!coop) {  // programmatic dependent launch: the kernels start with pdl_entry()
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LASGD_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
     return LASGD_OK;
   }
   void* kargs[] = {(void*)&args...};

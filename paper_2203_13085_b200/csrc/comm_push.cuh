@@ -31,6 +31,7 @@ __device__ __forceinline__ T* stage_ptr(const CommArgs& a, int owner, int parity
 
 template <typename T, int P, bool VIRTUAL, int U>
 __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T> f) {
+  pdl_entry();
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;
   const int vr = VIRTUAL ? (int)blockIdx.y : 0;
@@ -239,6 +240,7 @@ __device__ __forceinline__ T* mirror_ptr(const CommArgs& a, int owner, int parit
 
 template <typename T, bool VIRTUAL, int U>
 __global__ void __launch_bounds__(256, 2) k_push_mirror(CommArgs a, FusedRound<T> f) {
+  pdl_entry();
   constexpr int P = 2;
   constexpr int W = Pack<T>::W;
   const int rank = VIRTUAL ? (int)blockIdx.y : a.rank;

@@ -137,6 +137,16 @@ __device__ __forceinline__ unsigned pull_elem(T neg_alpha, T& xv, T sv, T zv) {
   return !finite(diff) + !finite(xv);
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// First statement of every sync kernel: let a dependent grid (launched with programmatic
+// stream serialization) get onto the SMs as soon as this grid's CTAs exit, then wait
+// until the previous grid in the stream has completed and its writes are visible.  With
+// a plain launch both are no-ops; nothing is read before the wait.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- device round descriptor
 // The per-launch scalars of the deterministic schedule (optimizer.py:181-207 with
 // collective_complete = (tau_i == k)) live in device memory so that a captured loop of

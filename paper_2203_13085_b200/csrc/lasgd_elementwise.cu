@@ -50,6 +50,7 @@ __device__ __forceinline__ void stream_body(Op& op, size_t n, unsigned long long
 
 template <typename T, typename Op, int U>
 __global__ void __launch_bounds__(kThreads, 4) k_stream(Op op, size_t n, unsigned long long* nonfinite) {
+  pdl_entry();
   stream_body<T, Op, U>(op, n, nonfinite);
 }
 
@@ -69,7 +70,16 @@ int launch(const Op& op, size_t n, bool aligned, unsigned long long* nonfinite, 
   if (aligned) {
     const size_t npack = n / Pack<T>::W;
     const size_t work = npack > (size_t)kThreads ? npack : (size_t)kThreads;
-    k_stream<T, Op, Op::U><<<stream_grid(work, kThreads), kThreads, 0, s>>>(op, n, nonfinite);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(stream_grid(work, kThreads));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LASGD_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_stream<T, Op, Op::U>, op, n, nonfinite));
   } else {
     k_scalar<T, Op><<<stream_grid(n, kThreads), kThreads, 0, s>>>(op, n, nonfinite);
   }
@@ -288,8 +298,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_sgd_dyn(SgdOp<T> op, T* snap0, 
   // now (they wait in griddepcontrol.wait below until this grid has completed and its
   // writes are visible), then wait for the previous step's grid the same way.  Saves the
   // launch ramp between back-to-back steps of a replayed graph.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_entry();
   const DynView v = dyn_read(adv.rd);
   dyn_coef(op.c, v);
   op.snap = snap0 == nullptr ? nullptr : (v.cur ? snap0 : snap1);  // next slot = 1 - cur
