@@ -615,6 +615,7 @@ static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned lo
   a.stage_elems = c->stage_elems;
   a.cur = snap_slot;
   a.done_seq = c->done_dev;
+
   a.seq = s;
   a.nonfinite = nullptr;
   a.trace = c->trace_on ? c->trace_buf : nullptr;
