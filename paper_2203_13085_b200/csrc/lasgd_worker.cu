@@ -22,6 +22,8 @@
 
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges show up in Nsight timelines, free otherwise
+
 #include "lasgd_common.cuh"
 
 namespace lasgd {
@@ -74,6 +76,13 @@ struct lasgd_worker {
   long long launches[K_KINDS] = {0};
   long long tau_hist[LASGD_TAU_HIST] = {0};
 };
+
+namespace {
+struct NvtxRange {  // one named range per worker call
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 static cudaEvent_t pool_get(lasgd_worker* w) {
   if (!w->pool.empty()) {
@@ -142,6 +151,7 @@ static void close_round_bookkeeping(lasgd_worker* w, int closed_tau) {
 
 // Round boundary of the overlap pipeline (optimizer.py:152-178 + the next submit).
 static int close_round(lasgd_worker* w) {
+  NvtxRange range("lasgd.close_round");
   const int cur = w->snap_idx, nxt = 1 - cur;
   int rc;
   if (w->world == 1) {
@@ -311,6 +321,7 @@ extern "C" int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* del
 
 extern "C" int lasgd_worker_step(lasgd_worker* w, const void* g, double lr) {
   if (!w || !g) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
+  NvtxRange range(w->dyn ? "lasgd.step (captured)" : "lasgd.step");
   if (!w->dyn) w->rd_dirty = true;
   const bool closes = w->cfg.sync && !w->cfg.adaptive && w->tau + 1 == w->cfg.sync_period;
   if ((w->cfg.pipeline == 1 || (w->dyn && w->world == 1)) && closes) return fused_step(w, g, lr);
@@ -610,6 +621,7 @@ extern "C" int lasgd_worker_capture_end(lasgd_graph* gr) {
 
 extern "C" int lasgd_graph_launch(lasgd_graph* gr) {
   if (!gr) return fail(LASGD_ERR_INVALID_ARGUMENT, "null graph");
+  NvtxRange range("lasgd.graph_launch");
   lasgd_worker* w = gr->w;
   if (w->tau != gr->tau0)
     return fail(LASGD_ERR_STATE, "graph captured at local step %d of a round, worker is at step %d", gr->tau0, w->tau);
