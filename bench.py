@@ -208,6 +208,8 @@ def kernel_bytes(name, n, world, comm, algo_code, sgd_momentum=True):
         return 5 * B if sgd_momentum else 3 * B, "hbm"
     if name == "pull":
         return 5 * B, "hbm"
+    if name == "sgd_pull":  # x, g, m, snap, xbar in; x, m, next snapshot out
+        return (8 if sgd_momentum else 7) * B, "hbm"
     if name == "finalize":
         return 4 * B, "hbm"
     if name == "snapshot":

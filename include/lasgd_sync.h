@@ -101,6 +101,15 @@ int lasgd_sgd_step(void* x, const void* g, void* m, void* delta, size_t n, int d
 int lasgd_elastic_pull(void* x, void* snap_next, const void* snap, const void* xbar, size_t n, int dtype,
                        double alpha, unsigned long long* nonfinite, void* stream);
 
+/* K5 + K4 in one pass — the round boundary of the deterministic overlap pipeline, once
+ * the (previous round's) mean has landed: the local step of lasgd_sgd_step, then mode 0
+ * the pull x -= alpha*(snap - xbar) or mode 1 the finalize x = xbar + delta'; snap_next =
+ * x.  Bit-identical to lasgd_sgd_step followed by lasgd_elastic_pull / lasgd_finalize.
+ * Replaces optimizer.py:145-146 + 170-174 (Algorithm 1 lines 8-9a). */
+int lasgd_sgd_pull(void* x, const void* g, void* m, void* delta, void* snap_next, const void* snap, const void* xbar,
+                   size_t n, int dtype, const lasgd_sgd_params* p, double alpha, int mode,
+                   unsigned long long* nonfinite, void* stream);
+
 /* K4b: reference finalize new = 1*z + 1*delta; x = new; snap_next = new (nullable).
  * delta may be NULL: the accumulator is zero (no local step since the previous
  * finalize reset it, optimizer.py:174), so new = z + 0.
@@ -264,7 +273,7 @@ int lasgd_comm_shape(lasgd_comm* c, size_t* n, int* dtype);
 typedef struct lasgd_worker lasgd_worker;
 
 #define LASGD_TAU_HIST 64
-#define LASGD_KERNEL_KINDS 6 /* sgd_step, snapshot, pull, finalize, allreduce, fused_round */
+#define LASGD_KERNEL_KINDS 7 /* sgd_step, snapshot, pull, finalize, allreduce, fused_round, sgd_pull */
 
 typedef struct {
   int sync_period;     /* deterministic schedule: local steps per round (tau)                    */

@@ -75,7 +75,7 @@ class CommConfig(ctypes.Structure):
 
 
 TAU_HIST = 64
-KERNEL_KINDS = ("sgd_step", "snapshot", "pull", "finalize", "allreduce", "fused_round")
+KERNEL_KINDS = ("sgd_step", "snapshot", "pull", "finalize", "allreduce", "fused_round", "sgd_pull")
 
 
 class WorkerConfig(ctypes.Structure):
@@ -129,6 +129,7 @@ SIGNATURES = {
     "lasgd_sgd_step": (_I, [_P, _P, _P, _P, _SZ, _I, ctypes.POINTER(SgdParams), _P, _P]),
     "lasgd_elastic_pull": (_I, [_P, _P, _P, _P, _SZ, _I, _D, _P, _P]),
     "lasgd_finalize": (_I, [_P, _P, _P, _P, _SZ, _I, _P, _P]),
+    "lasgd_sgd_pull": (_I, [_P, _P, _P, _P, _P, _P, _P, _SZ, _I, ctypes.POINTER(SgdParams), _D, _I, _P, _P]),
     "lasgd_mean_virtual": (_I, [_P, _I, _P, _I, _SZ, _I, _I, _I, _P, _P]),
     "lasgd_comm_create": (_I, [_I, _I, _I, _SZ, _I, ctypes.POINTER(CommConfig), ctypes.POINTER(_P)]),
     "lasgd_comm_ipc_handle": (_I, [_P, _P]),

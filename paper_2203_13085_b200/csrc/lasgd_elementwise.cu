@@ -251,6 +251,85 @@ struct FinalizeOp {
   }
 };
 
+// ------------------------------------------------------------- K5 + K4 in one pass
+// The round boundary of the deterministic overlap pipeline: the local step, then the
+// pull towards the (stale) mean that the side stream has already delivered (mode 0), or
+// the reference finalize new = xbar + delta' (mode 1); the next snapshot written in the
+// same pass.  The element function is K7's, so the bits equal K5 followed by K4.  8B
+// (x, g, m, snap, xbar in; x, m, snap_next out) instead of 5B + 5B.
+template <typename T>
+struct SgdPullOp {
+  T* x;
+  const T* g;
+  T* m;
+  T* delta;
+  T* snap_next;
+  const T* snap;
+  const T* xbar;
+  SgdCoef<T> c;
+  T neg_alpha;
+  int mode;
+  static constexpr int U = 1;
+  struct Loaded { Pack<T> x, g, m, d, s, z; };
+  __device__ __forceinline__ unsigned elem(T& xv, T gv, T& mv, T& dv, T sv, T zv) const {
+    unsigned bad = sgd_elem(c, xv, gv, mv, dv);
+    if (mode == 0) {
+      bad += pull_elem(neg_alpha, xv, sv, zv);
+    } else {
+      xv = add_rn(zv, dv);  // blend(1, z, 1, delta), optimizer.py:171
+      bad += !finite(xv);
+    }
+    return bad;
+  }
+  __device__ __forceinline__ void load(Loaded& L, size_t j) const {
+    L.x = ld_stream(x + j);
+    L.g = ld_stream(g + j);
+    if (c.use_mom && !c.first) L.m = ld_stream(m + j);
+    if (c.use_delta && !c.reset) L.d = ld_stream(delta + j);
+    if (mode == 0) L.s = ld_stream(snap + j);
+    L.z = ld_stream(xbar + j);
+  }
+  __device__ __forceinline__ unsigned compute_store(Loaded& L, size_t j) const {
+    unsigned bad = 0;
+#pragma unroll
+    for (int k = 0; k < Pack<T>::W; ++k) bad += elem(L.x.v[k], L.g.v[k], L.m.v[k], L.d.v[k], L.s.v[k], L.z.v[k]);
+    st_stream(x + j, L.x);
+    if (c.use_mom) st_stream(m + j, L.m);
+    if (c.use_delta && mode == 0) st_stream(delta + j, L.d);  // finalize resets delta (lazily)
+    st_stream(snap_next + j, L.x);
+    return bad;
+  }
+  __device__ __forceinline__ unsigned scalar(size_t j) const {
+    T xv = x[j], mv = (c.use_mom && !c.first) ? m[j] : T(0), dv = (c.use_delta && !c.reset) ? delta[j] : T(0);
+    unsigned bad = elem(xv, g[j], mv, dv, mode == 0 ? snap[j] : T(0), xbar[j]);
+    x[j] = xv;
+    if (c.use_mom) m[j] = mv;
+    if (c.use_delta && mode == 0) delta[j] = dv;
+    snap_next[j] = xv;
+    return bad;
+  }
+};
+
+template <typename T>
+int sgd_pull_t(void* x, const void* g, void* m, void* delta, void* snap_next, const void* snap, const void* xbar,
+               size_t n, const lasgd_sgd_params* p, double alpha, int mode, unsigned long long* nf, void* s) {
+  SgdPullOp<T> op;
+  op.x = (T*)x;
+  op.g = (const T*)g;
+  op.m = (T*)m;
+  op.delta = (T*)delta;
+  op.snap_next = (T*)snap_next;
+  op.snap = (const T*)snap;
+  op.xbar = (const T*)xbar;
+  op.c = make_sgd_coef<T>(p, delta != nullptr);
+  op.neg_alpha = (T)(-alpha);
+  op.mode = mode;
+  const bool al = aligned16(x) && aligned16(g) && (!op.c.use_mom || aligned16(m)) &&
+                  (!op.c.use_delta || aligned16(delta)) && aligned16(snap_next) && (mode != 0 || aligned16(snap)) &&
+                  aligned16(xbar);
+  return launch<T>(op, n, al, nf, s);
+}
+
 // ------------------------------------------------------------- typed entry points
 template <typename T>
 int blend_t(void* out, double a, const void* u, double b, const void* v, size_t n, unsigned long long* nf,
@@ -410,6 +489,22 @@ extern "C" int lasgd_elastic_pull(void* x, void* snap_next, const void* snap, co
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(LASGD_ERR_INVALID_ARGUMENT, "alpha must be in [0, 1], got %g", alpha);
   DISPATCH_DTYPE(dtype, pull_t<float>(x, snap_next, snap, xbar, n, alpha, nonfinite, stream),
                  pull_t<double>(x, snap_next, snap, xbar, n, alpha, nonfinite, stream));
+}
+
+extern "C" int lasgd_sgd_pull(void* x, const void* g, void* m, void* delta, void* snap_next, const void* snap,
+                              const void* xbar, size_t n, int dtype, const lasgd_sgd_params* p, double alpha, int mode,
+                              unsigned long long* nonfinite, void* stream) {
+  if (!p) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_sgd_pull: null params");
+  if (n && (!x || !g || !snap_next || !xbar || (mode == 0 && !snap)))
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_sgd_pull: null buffer");
+  if (mode != 0 && mode != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "mode %d (0 pull, 1 finalize)", mode);
+  if (mode == 1 && !delta) return fail(LASGD_ERR_INVALID_ARGUMENT, "finalize mode needs the delta buffer");
+  if (mode == 0 && !(alpha > 0.0 && alpha <= 1.0)) return fail(LASGD_ERR_INVALID_ARGUMENT, "alpha must be in (0, 1]");
+  if (p->momentum != 0.0 && !m) return fail(LASGD_ERR_INVALID_ARGUMENT, "lasgd_sgd_pull: momentum needs m");
+  if (p->nesterov && (p->momentum <= 0.0 || p->dampening != 0.0))
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "Nesterov momentum requires a momentum and zero dampening");
+  DISPATCH_DTYPE(dtype, sgd_pull_t<float>(x, g, m, delta, snap_next, snap, xbar, n, p, alpha, mode, nonfinite, stream),
+                 sgd_pull_t<double>(x, g, m, delta, snap_next, snap, xbar, n, p, alpha, mode, nonfinite, stream));
 }
 
 extern "C" int lasgd_finalize(void* x, void* snap_next, const void* z, const void* delta, size_t n, int dtype,

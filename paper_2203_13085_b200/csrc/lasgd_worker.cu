@@ -28,7 +28,7 @@
 
 namespace lasgd {
 
-enum Kind { K_SGD = 0, K_SNAPSHOT, K_PULL, K_FINALIZE, K_ALLREDUCE, K_FUSED, K_KINDS };
+enum Kind { K_SGD = 0, K_SNAPSHOT, K_PULL, K_FINALIZE, K_ALLREDUCE, K_FUSED, K_SGD_PULL, K_KINDS };
 
 struct TimingRec {
   int kind;
@@ -242,6 +242,29 @@ static int fused_step(lasgd_worker* w, const void* g, double lr) {
   return 1;
 }
 
+// Round boundary of the deterministic overlap pipeline (P > 1): the previous round's
+// mean has been on its way for a whole round, so the compute stream waits for it and
+// applies the local step AND the pull / finalize in one pass (lasgd_sgd_pull, 8B instead
+// of K5 5B + K4 5B), then hands the new snapshot to the side stream.
+static int overlap_boundary(lasgd_worker* w, const void* g, double lr) {
+  NvtxRange range("lasgd.close_round");
+  const int cur = w->snap_idx, nxt = 1 - cur;
+  lasgd_sgd_params p = sgd_params(w, lr);
+  int rc = lasgd_comm_stream_wait(w->comm, w->seq, (void*)w->compute);
+  if (rc) return rc;
+  const int mode = finalize_mode(w) ? 1 : 0;
+  rc = issue(w, K_SGD_PULL, w->compute, [&] {
+    return lasgd_sgd_pull(w->x, g, w->m, w->delta, w->snap[nxt], w->snap[cur], w->xbar, w->n, w->dtype, &p,
+                          w->cfg.alpha, mode, w->nonfinite, (void*)w->compute);
+  });
+  if (rc) return rc;
+  w->mom_started = w->m != nullptr;
+  w->local_clock++;
+  close_round_bookkeeping(w, w->tau + 1);
+  rc = submit_allreduce(w, w->snap_idx);
+  return rc ? rc : 1;
+}
+
 extern "C" int lasgd_worker_create(lasgd_comm* comm, void* x, void* m, void* delta, void* snap0, void* snap1,
                                    size_t n, int dtype, const lasgd_worker_config* cfg, void* compute_stream,
                                    void* side_stream, unsigned long long* nonfinite, lasgd_worker** out) {
@@ -324,7 +347,11 @@ extern "C" int lasgd_worker_step(lasgd_worker* w, const void* g, double lr) {
   NvtxRange range(w->dyn ? "lasgd.step (captured)" : "lasgd.step");
   if (!w->dyn) w->rd_dirty = true;
   const bool closes = w->cfg.sync && !w->cfg.adaptive && w->tau + 1 == w->cfg.sync_period;
-  if ((w->cfg.pipeline == 1 || (w->dyn && w->world == 1)) && closes) return fused_step(w, g, lr);
+  // deterministic round boundary: one pass — the fused round (fused pipeline, and P = 1
+  // where the boundary is the local step with the snapshot fused in), or the local step
+  // fused with the pull of the mean the side stream delivered (overlap pipeline)
+  if ((w->cfg.pipeline == 1 || w->world == 1) && closes) return fused_step(w, g, lr);
+  if (closes && !w->dyn) return overlap_boundary(w, g, lr);
   lasgd_sgd_params p = sgd_params(w, lr);
   int rc = w->dyn ? dyn_step(w, g, 0) : issue(w, K_SGD, w->compute, [&] {
     return lasgd_sgd_step(w->x, g, w->m, w->delta, w->n, w->dtype, &p, w->nonfinite, (void*)w->compute);

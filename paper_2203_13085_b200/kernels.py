@@ -96,6 +96,19 @@ def finalize(x, z, delta, snap_next=None, nonfinite=None, stream=None) -> torch.
     return x
 
 
+def sgd_pull(x, g, snap_next, snap, xbar, lr: float, *, m=None, delta=None, momentum=0.0, dampening=0.0,
+             weight_decay=0.0, nesterov=False, first_step=False, delta_reset=False, alpha: float = 1.0, mode: int = 0,
+             nonfinite=None, stream=None) -> torch.Tensor:
+    """K5 + K4 in one pass: the local step, then the pull towards ``xbar`` (mode 0) or the
+    reference finalize ``x = xbar + delta'`` (mode 1); ``snap_next = x``."""
+    code, n = _check(x, g, snap_next, xbar, snap, m, delta)
+    p = sgd_params(lr, momentum, dampening, weight_decay, nesterov, first_step, delta_reset)
+    N.check(N.lib().lasgd_sgd_pull(_ptr(x), _ptr(g), _ptr(m), _ptr(delta), _ptr(snap_next), _ptr(snap), _ptr(xbar), n,
+                                   code, ctypes.byref(p), float(alpha), int(mode), _ptr(nonfinite), _stream(stream)),
+            "sgd_pull")
+    return x
+
+
 def sgd_params(lr: float, momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False, first_step=False,
                delta_reset=False) -> N.SgdParams:
     return N.SgdParams(float(lr), float(momentum), float(dampening), float(weight_decay), int(bool(nesterov)),

@@ -185,3 +185,26 @@ def test_dimension_and_dtype_errors():
         K.snapshot(a, torch.zeros(10, device="cuda", dtype=torch.float16))
     with pytest.raises(ValueError):
         K.elastic_pull(a, a, a, 1.5)
+
+
+@pytest.mark.parametrize("n", [1, 7, 4099, 1_000_003])
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+@pytest.mark.parametrize("first", [True, False])
+def test_sgd_pull_one_pass_equals_step_then_pull(n, alpha, first):
+    """lasgd_sgd_pull (the deterministic overlap pipeline's round boundary) == K5 then K4,
+    bit for bit, against the oracle; and the finalize form against step-then-finalize."""
+    cfg = O.SgdConfig(0.1, 0.9, 0.0, 1e-4, True)
+    x, g, m, s, z, d = (rnd(n, 40 + i) for i in range(6))
+    xt, gt, mt, st, zt = dev(x), dev(g), dev(m), dev(s), dev(z)
+    nt = torch.full_like(xt, float("nan"))
+    K.sgd_pull(xt, gt, nt, st, zt, cfg.lr, m=mt, momentum=0.9, weight_decay=1e-4, nesterov=True, first_step=first,
+               alpha=alpha)
+    x1, m1, _ = O.sgd_step_momentum(x, g, m, cfg, first_step=first)
+    ref = O.elastic_pull(x1, s, z, alpha)
+    assert same_bits(host(xt), ref) and same_bits(host(nt), ref) and same_bits(host(mt), m1)
+    # finalize form (reference bookkeeping, plain SGD): x = z + (delta + (-lr) g)
+    xt, dt, nt = dev(x), dev(d), torch.empty_like(dev(x))
+    K.sgd_pull(xt, dev(g), nt, dev(s), dev(z), 0.05, delta=dt, mode=1)
+    _, d1 = O.sgd_step_delta(x, d, g, 0.05)
+    ref = O.finalize_delta(z, d1, x, 2)
+    assert same_bits(host(xt), ref) and same_bits(host(nt), ref)
