@@ -345,6 +345,7 @@ int lasgd_worker_capture_end(lasgd_graph* gr);
 /* Replay on the worker's compute stream and advance the worker's state by the captured
  * steps; LASGD_ERR_STATE if the worker is not at the round position of the capture. */
 int lasgd_graph_launch(lasgd_graph* gr);
+/* Destroy every graph of a worker before the worker itself. */
 int lasgd_graph_destroy(lasgd_graph* gr);
 
 /* ---- measurement aid ------------------------------------------------------ */
