@@ -132,7 +132,7 @@ class ClockSampler:
         self.p.wait()
         self.f.flush()
         self.f.seek(0)
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.f.read().splitlines():
             parts = [x.strip() for x in line.split(",")]
@@ -143,13 +143,21 @@ class ClockSampler:
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+            except ValueError:
+                pass
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         os.unlink(self.f.name)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+        if pw:
+            out["power_w_median"] = statistics.median(pw)
+            out["sm_mhz_min"] = min(sm)
+        return out
 
 
 # ---------------------------------------------------------------------------- helpers
@@ -702,7 +710,12 @@ def main():
     # ---------------- real training: ResNet-50 fwd/bwd + LASGD vs no-sync ceiling
     training = None
     if not args.no_train and not args.kernels_only:
+        tclk = ClockSampler(local) if rank == 0 else None
         training = run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barrier, max_over_ranks)
+        if tclk is not None:
+            # clocks and power over the training legs: ResNet-50 bf16 at batch 256 runs at the
+            # 1 kW cap, so SM clocks move with each leg's power draw
+            training["clocks"] = tclk.stop()
 
     # ---------------- report
     imgs = world * args.batch * args.steps
