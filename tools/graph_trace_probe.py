@@ -22,10 +22,17 @@ from paper_2203_13085_b200 import _native as N  # noqa: E402
 
 def summary(tr):
     t0 = min(t[0] for t in tr)
-    return {"span_us": (max(t[3] for t in tr) - t0) / 1e3,
-            "start_skew_us": (max(t[0] for t in tr) - t0) / 1e3,
-            "entry_wait_us_median": statistics.median((t[1] - t[0]) / 1e3 for t in tr),
-            "entry_passed_last_us": (max(t[1] for t in tr) - t0) / 1e3}
+    out = {"span_us": (max(t[3] for t in tr) - t0) / 1e3,
+           "start_skew_us": (max(t[0] for t in tr) - t0) / 1e3,
+           "entry_wait_us_median": statistics.median((t[1] - t[0]) / 1e3 for t in tr),
+           "entry_passed_last_us": (max(t[1] for t in tr) - t0) / 1e3}
+    mids = [t for t in tr if t[2] > t[1]]
+    if mids:  # phase A (own chunk, until the mid barrier passed) and phase B
+        out["mid_passed_first_us"] = (min(t[2] for t in mids) - t0) / 1e3
+        out["mid_passed_last_us"] = (max(t[2] for t in mids) - t0) / 1e3
+        out["phase_b_us_median"] = statistics.median((t[3] - t[2]) / 1e3 for t in mids)
+        out["first_end_us"] = (min(t[3] for t in tr) - t0) / 1e3
+    return out
 
 
 def main():
