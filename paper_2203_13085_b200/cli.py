@@ -19,6 +19,7 @@ Config (YAML or JSON, schema 1; unknown keys are errors):
     problem: {kind: mlp, n: 4096, d: 784, hidden: [128], noise: 0.1, data_seed: 0, batch: 32}
     algo: lasgd                     # lasgd | sgd_ar
     lasgd: {tau_max: 4, adaptive: false, alpha: 1.0, mode: pull, pipeline: overlap}
+    sgd_ar: {bucketed: false, bucket_mb: 25}   # bucketed: the all-reduce overlapped with backward
     sgd: {momentum: 0.0, dampening: 0.0, weight_decay: 0.0, nesterov: false}
     lr: {base_lr: 0.01, scale_nodes: 1, warmup_epochs: 0.0, decay_epochs: [], decay_factor: 10.0}
     steps: 100
@@ -48,6 +49,7 @@ DEFAULTS = {
     "problem": {"kind": "mlp", "n": 4096, "d": 784, "hidden": [128], "noise": 0.1, "data_seed": 0, "batch": 32},
     "algo": "lasgd",
     "lasgd": {"tau_max": 4, "adaptive": False, "alpha": 1.0, "mode": "pull", "pipeline": "overlap"},
+    "sgd_ar": {"bucketed": False, "bucket_mb": 25},
     "sgd": {"momentum": 0.0, "dampening": 0.0, "weight_decay": 0.0, "nesterov": False},
     "lr": {"base_lr": 0.01, "scale_nodes": 1, "warmup_epochs": 0.0, "decay_epochs": [], "decay_factor": 10.0},
     "steps": 100,
@@ -94,7 +96,7 @@ def resolve(cfg: dict) -> dict:
     if not isinstance(cfg, dict):
         raise ConfigError(["config must be a mapping"])
     merge(out, cfg, "")
-    p, la, sg, lr = out["problem"], out["lasgd"], out["sgd"], out["lr"]
+    p, la, sg, lr, sa = out["problem"], out["lasgd"], out["sgd"], out["lr"], out["sgd_ar"]
 
     def need(cond, msg):
         if not cond:
@@ -126,6 +128,8 @@ def resolve(cfg: dict) -> dict:
                       "(optimizer.py:71-72); use mode=pull for alpha < 1")
     if la["pipeline"] == "fused" and la["adaptive"]:
         errors.append("lasgd.pipeline=fused implements the deterministic schedule only (adaptive needs overlap)")
+    need(isinstance(sa["bucketed"], bool), "sgd_ar.bucketed must be a boolean")
+    need(num(sa["bucket_mb"]) and sa["bucket_mb"] > 0, "sgd_ar.bucket_mb must be > 0")
     for k in ("momentum", "dampening", "weight_decay"):
         need(num(sg[k]) and sg[k] >= 0, f"sgd.{k} must be >= 0")
     need(num(sg["dampening"]) and sg["dampening"] <= 1, "sgd.dampening must be <= 1")
@@ -242,7 +246,11 @@ def cmd_run(cfg: dict, out_dir: str) -> int:
     if world > 1:
         dist.barrier()
     with torch.cuda.stream(compute):
-        if cfg["algo"] == "sgd_ar":
+        if cfg["algo"] == "sgd_ar" and cfg["sgd_ar"]["bucketed"] and comm is not None:
+            # buckets launched from autograd hooks as backward completes them (same bits)
+            worker = L.BucketedSGDARWorker(flat, comm, sgd=sgd, schedule=sched, compute_stream=compute,
+                                           bucket_bytes=max(16, int(cfg["sgd_ar"]["bucket_mb"] * (1 << 20))))
+        elif cfg["algo"] == "sgd_ar":
             worker = L.SGDARWorker(flat.x, comm=comm, sgd=sgd, schedule=sched, compute_stream=compute, flat=flat)
         else:
             worker = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=la["tau_max"], alpha=la["alpha"],

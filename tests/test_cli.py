@@ -110,3 +110,12 @@ def test_compare_and_plotdata(tmp_path, capsys):
     kinds = {ln.split(",")[2] for ln in lines[1:]}
     assert kinds == {"time", "epoch"}
     assert os.path.exists(tmp_path / "cmp.csv")
+
+
+def test_sgd_ar_bucketed_option_validated():
+    cfg = cli.resolve({"algo": "sgd_ar", "sgd_ar": {"bucketed": True, "bucket_mb": 0.5}})
+    assert cfg["sgd_ar"] == {"bucketed": True, "bucket_mb": 0.5}
+    with pytest.raises(cli.ConfigError) as e:
+        cli.resolve({"sgd_ar": {"bucketed": "yes", "bucket_mb": 0, "colour": 1}})
+    msg = str(e.value)
+    assert "sgd_ar.bucketed" in msg and "sgd_ar.bucket_mb" in msg and "unknown key 'sgd_ar.colour'" in msg
