@@ -484,6 +484,7 @@ struct lasgd_graph {
   int steps = 0, tau0 = 0;
   lasgd_graph_saved saved;
   CommMirror comm_after;  // the communicator bookkeeping after the captured launches
+  int snap_after = 0;     // the worker's snapshot slot after the captured steps
   // what one replay does to the host mirror of the protocol state
   long long d_clock = 0, d_rounds = 0;
   bool mom_after = false, delta_fresh_after = false;
@@ -561,6 +562,7 @@ static int capture_close(lasgd_worker* w, lasgd_graph* gr) {
   gr->mom_after = w->mom_started;
   gr->delta_fresh_after = w->delta_fresh;
   const int tau_end = w->tau;
+  gr->snap_after = w->snap_idx;
   for (int k = 0; k < K_KINDS; ++k) gr->d_launches[k] = w->launches[k] - v.launches[k];
   for (int t = 0; t < LASGD_TAU_HIST; ++t) gr->d_tau_hist[t] = w->tau_hist[t] - v.hist[t];
   w->tau = v.tau;
@@ -662,8 +664,10 @@ extern "C" int lasgd_graph_launch(lasgd_graph* gr) {
     comm_mirror_get(w->comm, &cm);
     const CommMirror& pre = gr->saved.comm;
     auto lag = [](unsigned long long seq, unsigned long long v) { return v ? (long long)(seq - v) : -1LL; };
-    if (cm.push_slot != pre.push_slot || lag(cm.seq, cm.last_push) != lag(pre.seq, pre.last_push) ||
-        lag(cm.seq, cm.end_seq) != lag(pre.seq, pre.end_seq))
+    // staging parity relative to the snapshot slot (the graph itself is parity-agnostic)
+    auto staged = [](int push_slot, int snap) { return push_slot < 0 ? -1 : (push_slot == snap ? 1 : 0); };
+    if (staged(cm.push_slot, w->snap_idx) != staged(pre.push_slot, gr->saved.snap_idx) ||
+        lag(cm.seq, cm.last_push) != lag(pre.seq, pre.last_push) || lag(cm.seq, cm.end_seq) != lag(pre.seq, pre.end_seq))
       return fail(LASGD_ERR_STATE, "the communicator's last launch differs from the capture's; run one eager round");
     if (cm.seq != w->rd_seq) w->rd_dirty = true;  // launches the descriptor has not seen
   }
@@ -692,7 +696,9 @@ extern "C" int lasgd_graph_launch(lasgd_graph* gr) {
     now.seq = cm.seq + d;
     now.last_push = post.last_push ? now.seq - (post.seq - post.last_push) : 0;
     now.end_seq = post.end_seq ? now.seq - (post.seq - post.end_seq) : 0;
-    now.push_slot = post.push_slot;
+    // w->snap_idx has advanced by the replay already; map the capture's final staging
+    // parity (relative to its final slot) onto it
+    now.push_slot = post.push_slot < 0 ? -1 : (post.push_slot == gr->snap_after ? w->snap_idx : 1 - w->snap_idx);
     comm_mirror_set(w->comm, now);
     if (d) {
       w->seq = now.seq;

@@ -345,6 +345,30 @@ def _w_graph_replay(rank, world, port):
 
             a, b = run(True), run(False)
             assert a[2:4] == b[2:4] == (total, total // k), (a[2:], b[2:])
+            if algo == N.ALGO_PUSH and k == 1:
+                # a replay is refused once another launch moved the communicator, and
+                # accepted again after one eager round
+                comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
+                x = torch.from_numpy(x0.copy()).cuda()
+                compute = torch.cuda.Stream()
+                with torch.cuda.stream(compute):
+                    w = L.LASGDWorker(x, grads[0], comm=comm, sync_period=1, sgd=sgd, lr=0.05, algo=algo,
+                                      pipeline="fused", compute_stream=compute)
+                    w.step()
+                    graph = w.capture(grads)
+                    graph.replay()
+                    comm.stream.wait_stream(compute)
+                    comm.wait(comm.allreduce(w.state.snap_idx), 20.0)
+                    compute.wait_stream(comm.stream)
+                    with pytest.raises(RuntimeError, match="eager round"):
+                        graph.replay()
+                    w.g = grads[0]
+                    w.step()
+                    graph.replay()
+                torch.cuda.synchronize()
+                w.close()
+                dist.barrier()
+                comm.close()
             assert _same_bits(a[0], b[0]) and _same_bits(a[1], b[1]), (algo, k, rank)
             gl = np.stack([np.stack(gsrc[t % 2]) for t in range(total)])
             ref, _, _, _ = O.run_lasgd_pull(x0, gl, [0.05] * total, world, k, alpha,
