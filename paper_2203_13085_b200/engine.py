@@ -188,7 +188,8 @@ class LASGDWorker:
         """Capture ``steps`` local steps (default ``len(grads)``; a whole number of rounds),
         step t reading gradient ``grads[t % len(grads)]``, as one CUDA graph.  Nothing runs
         until ``replay()``; each replay advances the worker exactly as ``steps`` calls of
-        ``step()`` would, with bit-identical results (deterministic schedule, one rank)."""
+        ``step()`` would, with bit-identical results (deterministic schedule; one rank, or
+        the fused pipeline over a communicator after one eager round)."""
         grads = list(grads)
         steps = len(grads) if steps is None else int(steps)
         for t in grads:
@@ -211,6 +212,7 @@ class LASGDWorker:
         graph = torch.cuda.CUDAGraph()
         h = ctypes.c_void_p()
         self._capturing = True
+        clock0 = self._local_clock
         try:
             with torch.cuda.graph(graph, stream=self.compute, pool=pool):
                 N.check(N.lib().lasgd_worker_capture_begin(self._h, ctypes.byref(h)), "lasgd_worker_capture_begin")
@@ -227,7 +229,7 @@ class LASGDWorker:
             raise
         finally:
             self._capturing = False
-            self._local_clock -= steps  # step() advanced the Python clock during capture
+            self._local_clock = clock0  # step() advanced the Python clock during capture
         gr = SyncGraph(self, h, steps, [self.g], external=graph)
         self._graphs.append(gr)
         return gr
