@@ -479,8 +479,8 @@ class BucketedSGDARWorker:
     Backward must write the gradients into the communicator's slots: the worker binds
     ``flat``'s ``.grad`` views to slot ``grad_buffer`` and rebinds them every step.  Use:
     ``flat.zero_grad(); loss.backward(); worker.step()`` on the compute stream, eagerly
-    (the buckets launch from autograd hooks).  A parameter must receive exactly one
-    gradient accumulation per backward (no weight sharing)."""
+    (the buckets launch from autograd hooks), one backward per ``step()``.  A parameter
+    must receive exactly one gradient accumulation per backward (no weight sharing)."""
 
     def __init__(self, flat, comm, *, sgd: Optional[SgdConfig] = None, schedule: Optional[LrSchedule] = None,
                  lr: Optional[float] = None, bucket_bytes: int = 25 << 20,
