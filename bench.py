@@ -74,6 +74,7 @@ def parse():
     ap.add_argument("--bucket-mb", type=int, default=25, help="gradient bucket size of the bucketed SGD-AR / DDP legs")
     ap.add_argument("--bucket-ctas", type=int, default=0, help="CTAs of each bucketed SGD-AR launch (0: 2 per SM)")
     ap.add_argument("--legs", default="", help="comma list: run only these training legs (and their baselines)")
+    ap.add_argument("--no-nvls-leg", action="store_true", help="skip the NVLS (in-switch mean) training leg at N>=4")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="training leg: eager fwd/bwd instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -874,8 +875,8 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     # ---- legs: make() -> (one_step, finish, close); one_step runs one training step on `compute`
     cached = {}  # N=1 graphed LASGD legs and DDP live across blocks (graphs captured once)
 
-    def lasgd_leg(**wkw):
-        key = repr(sorted(wkw.items()))
+    def lasgd_leg(leg_comm=None, **wkw):
+        key = repr(sorted(wkw.items())) + ("nvls" if leg_comm is not None else "")
 
         def make():
             flat.bind_grads(own_g)
@@ -883,7 +884,8 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
             if key in cached:
                 w, one_graph = cached[key]
             else:
-                w = L.LASGDWorker(flat.x, flat.g, comm=tcomm, sync_period=args.sync_period, alpha=args.alpha,
+                w = L.LASGDWorker(flat.x, flat.g, comm=leg_comm if leg_comm is not None else tcomm,
+                                  sync_period=args.sync_period, alpha=args.alpha,
                                   mode="pull", sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
                                   fused_nblocks=args.fused_nblocks, **wkw)
                 if graphed and world == 1 and not wkw.get("adaptive"):
@@ -986,6 +988,15 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
             "fused": (lasgd_leg(pipeline="fused"), "nosync"),
             "overlap": (lasgd_leg(pipeline="overlap"), "nosync"),
             "overlap_adaptive": (lasgd_leg(pipeline="overlap", adaptive=True, tau_max=5), "nosync")}
+    ncomm = None
+    if tcomm is not None and world >= 4 and not args.no_nvls_leg:
+        # the overlap pipeline on the in-switch (NVLS, tolerance-mode) side-stream mean
+        try:
+            ncomm = L.P2PCommunicator(flat.numel, nblocks=args.nblocks, timeout_s=60.0, nvls=True)
+        except ValueError:
+            ncomm = None
+        if ncomm is not None:
+            legs["overlap_nvls"] = (lasgd_leg(leg_comm=ncomm, pipeline="overlap"), "nosync")
     if tcomm is not None:
         legs.update({"sgd_ar": (sgd_ar_leg("p2p"), "nosync"), "sgd_ar_nccl": (sgd_ar_leg("nccl"), "nosync"),
                      "nosync_eager": (nosync_eager_leg(), "nosync_eager"),
@@ -1038,6 +1049,8 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     cached.clear()
     if tcomm is not None and tcomm is not comm:
         tcomm.close()
+    if ncomm is not None:
+        ncomm.close()
     flat.bind_grads(own_g)
 
     import statistics as st

@@ -51,6 +51,8 @@ extern "C" {
 #define LASGD_ALGO_AUTO 0
 #define LASGD_ALGO_ONESHOT 1
 #define LASGD_ALGO_TWOSHOT 2
+#define LASGD_ALGO_NVLS 4 /* all-reduce only, NVLS communicators: reduced inside the NVSwitch
+                            (tolerance mode, see lasgd_comm_nvls_bind) */
 #define LASGD_ALGO_PUSH 3 /* fused round only, data moved by remote stores: P = 2 mirrors the peer's
                              snapshot; P >= 3 owners reduce locally staged chunks, means pushed */
 
@@ -265,6 +267,24 @@ int lasgd_comm_invalidate_staging(lasgd_comm* c);
 int lasgd_comm_launches(lasgd_comm* c, unsigned long long* out);
 /* rank, world size and the mean buffer of a communicator (any pointer may be NULL). */
 int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar);
+/* ---- NVLink SHARP (tolerance mode) -----------------------------------------
+ * The mean reduced inside the NVSwitch: multimem.ld_reduce of the rank's chunk over the
+ * multicast view of the snapshot slot, multimem.st of the mean into every rank's mean
+ * buffer — (P+1)/P*B per link direction instead of 2(P-1)/P*B.  The switch's summation
+ * order is not the reference ring's (collective.py:183-200): the mean matches it to
+ * rounding (the north star's 1e-6 relative); every rank receives the same bits.
+ * Setup, collectively: rank 0 lasgd_comm_nvls_create (exports the multicast object as a
+ * POSIX fd, which the caller passes to the other ranks, e.g. SCM_RIGHTS), the others
+ * lasgd_comm_nvls_import; every rank lasgd_comm_nvls_add_device; after ALL have added,
+ * lasgd_comm_nvls_bind.  From then on the snapshot slots and the mean buffer
+ * (lasgd_comm_buffer / lasgd_comm_info) live in the multicast-bound allocation and
+ * lasgd_comm_allreduce runs the in-switch mean (AUTO or NVLS); fused rounds are refused.
+ * fp32 only. */
+int lasgd_comm_nvls_supported(lasgd_comm* c);
+int lasgd_comm_nvls_create(lasgd_comm* c, int* fd_out);
+int lasgd_comm_nvls_import(lasgd_comm* c, int fd);
+int lasgd_comm_nvls_add_device(lasgd_comm* c);
+int lasgd_comm_nvls_bind(lasgd_comm* c);
 /* Element count and element type of the communicator's buffers (either pointer may be NULL). */
 int lasgd_comm_shape(lasgd_comm* c, size_t* n, int* dtype);
 

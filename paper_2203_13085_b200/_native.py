@@ -31,6 +31,7 @@ ALGO_AUTO = 0
 ALGO_ONESHOT = 1
 ALGO_TWOSHOT = 2
 ALGO_PUSH = 3
+ALGO_NVLS = 4
 MAX_RANKS = 8
 MAX_BLOCKS = 512
 IPC_HANDLE_BYTES = 64
@@ -157,6 +158,11 @@ SIGNATURES = {
     "lasgd_comm_destroy": (_I, [_P]),
     "lasgd_comm_info": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_P)]),
     "lasgd_comm_shape": (_I, [_P, ctypes.POINTER(_SZ), ctypes.POINTER(_I)]),
+    "lasgd_comm_nvls_supported": (_I, [_P]),
+    "lasgd_comm_nvls_create": (_I, [_P, ctypes.POINTER(_I)]),
+    "lasgd_comm_nvls_import": (_I, [_P, _I]),
+    "lasgd_comm_nvls_add_device": (_I, [_P]),
+    "lasgd_comm_nvls_bind": (_I, [_P]),
     "lasgd_comm_peer_max_seq": (_I, [_P, _ULLP]),
     "lasgd_comm_launches": (_I, [_P, _ULLP]),
     "lasgd_comm_invalidate_staging": (_I, [_P]),

@@ -360,6 +360,50 @@ def exchange_handles(mine: bytes, world: int, group=None) -> bytes:
     return b"".join(gathered)
 
 
+def share_fd(fd: Optional[int], rank: int, world: int, group=None) -> int:
+    """Pass a file descriptor from rank 0 to every other rank of this node (SCM_RIGHTS
+    over an abstract-namespace UNIX socket whose name rank 0 broadcasts).  Returns the
+    descriptor valid in this process."""
+    import secrets
+    import socket
+    import time
+
+    import torch.distributed as dist
+
+    name = [f"\0lasgd-nvls-{secrets.token_hex(8)}" if rank == 0 else None]
+    dist.broadcast_object_list(name, src=0, group=group)
+    if rank == 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name[0])
+        srv.listen(world)
+        dist.barrier(group=group)
+        try:
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"f"], [fd])
+        finally:
+            srv.close()
+        return fd
+    dist.barrier(group=group)
+    deadline = time.monotonic() + 60.0
+    while True:
+        cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        try:
+            cli.connect(name[0])
+            break
+        except OSError:
+            cli.close()
+            if time.monotonic() > deadline:
+                raise
+            time.sleep(0.01)
+    with cli:
+        _, fds, _, _ = socket.recv_fds(cli, 16, 1)
+    if not fds:
+        raise RuntimeError("no file descriptor received from rank 0")
+    return fds[0]
+
+
 class P2PCommunicator:
     """One rank's endpoint of the NVLink P2P mean all-reduce (K2/K3/K6).
 
@@ -367,11 +411,17 @@ class P2PCommunicator:
     buffer) and maps every peer's region.  Handles are exchanged once at
     construction through ``torch.distributed`` (any backend; gloo works).
     All ranks must issue the same sequence of ``allreduce`` calls.
+
+    ``nvls=True`` (fp32, P >= 2): the snapshot slots and the mean buffer move into a
+    multicast-bound allocation and ``allreduce`` reduces inside the NVSwitch
+    (``ALGO_NVLS``, tolerance mode: within rounding of the ring-order mean, identical
+    bits on every rank); fused rounds are then unavailable (use the overlap pipeline).
     """
 
     def __init__(self, n: int, *, dtype: torch.dtype = torch.float32, rank: Optional[int] = None,
                  world: Optional[int] = None, device=None, group=None, nblocks: int = 96, threads: int = 256,
-                 timeout_s: float = 30.0, fault_seq: int = -1, fault_phase: int = 0, stream_priority: int = 0):
+                 timeout_s: float = 30.0, fault_seq: int = -1, fault_phase: int = 0, stream_priority: int = 0,
+                 nvls: bool = False):
         import torch.distributed as dist
 
         if rank is None:
@@ -395,6 +445,9 @@ class P2PCommunicator:
         if world > 1:
             allh = exchange_handles(mine, world, group)
             N.check(N.lib().lasgd_comm_open(self._h, allh), "lasgd_comm_open")
+        self.nvls = bool(nvls)
+        if self.nvls:
+            self._setup_nvls(group)
         typestr = "<f4" if dtype == torch.float32 else "<f8"
         self.snapshots = []
         for which in (0, 1):
@@ -407,6 +460,32 @@ class P2PCommunicator:
         self.stream = torch.cuda.Stream(device=self.device, priority=stream_priority)
         if world > 1 and dist.is_initialized():
             dist.barrier(group=group)
+
+    def _setup_nvls(self, group) -> None:
+        import torch.distributed as dist
+
+        if self.world < 2 or not dist.is_initialized():
+            raise ValueError("NVLS needs P >= 2 ranks under torch.distributed")
+        ok = [bool(N.lib().lasgd_comm_nvls_supported(self._h))]
+        oks = [None] * self.world
+        dist.all_gather_object(oks, ok[0], group=group)
+        if not all(oks):
+            raise ValueError("NVLink SHARP multicast is not supported on every rank's device")
+        with torch.cuda.device(self.device):
+            fd = ctypes.c_int(-1)
+            if self.rank == 0:
+                N.check(N.lib().lasgd_comm_nvls_create(self._h, ctypes.byref(fd)), "lasgd_comm_nvls_create")
+            got = share_fd(fd.value if self.rank == 0 else None, self.rank, self.world, group)
+            if self.rank != 0:
+                N.check(N.lib().lasgd_comm_nvls_import(self._h, got), "lasgd_comm_nvls_import")
+            N.check(N.lib().lasgd_comm_nvls_add_device(self._h), "lasgd_comm_nvls_add_device")
+            dist.barrier(group=group)  # every device added before anyone binds
+            N.check(N.lib().lasgd_comm_nvls_bind(self._h), "lasgd_comm_nvls_bind")
+            if self.rank == 0:
+                import os
+
+                os.close(fd.value)
+        dist.barrier(group=group)
 
     def slot_of(self, t: torch.Tensor) -> Optional[int]:
         for i, s in enumerate(self.snapshots):

@@ -42,6 +42,7 @@
 #include <utility>
 
 #include "comm_launch.cuh"
+#include "comm_nvls.h"
 #include "lasgd_common.cuh"
 
 namespace lasgd {
@@ -317,6 +318,12 @@ struct lasgd_comm {
   bool trace_on = false;
   bool gate = false;           // launch k_gate ahead of every all-reduce (side-stream use)
   unsigned long long seq = 0;  // launches issued
+  // NVLink SHARP (tolerance mode): once bound, the snapshot slots and the mean buffer live
+  // in a multicast-bound allocation: nvls_uc (this rank's view) / nvls_mc (the switch's)
+  NvlsState* nvls = nullptr;
+  char* nvls_uc = nullptr;
+  char* nvls_mc = nullptr;
+  size_t nvls_off[3] = {0, 0, 0};
   uint32_t* epoch_host = nullptr;      // pinned readback of the peers' entry flags (read_peer_epochs)
   cudaStream_t epoch_stream = nullptr;  // on this communicator's device
   cudaEvent_t ev[kEvents];
@@ -433,7 +440,8 @@ extern "C" int lasgd_comm_open(lasgd_comm* c, const void* handles) {
 
 extern "C" int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr) {
   if (!c || !ptr) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
-  if (which == 0 || which == 1) *ptr = c->base + c->off_snap[which];
+  if (c->nvls_uc && which >= 0 && which <= 2) *ptr = c->nvls_uc + c->nvls_off[which];
+  else if (which == 0 || which == 1) *ptr = c->base + c->off_snap[which];
   else if (which == 2) *ptr = c->base + c->off_xbar;
   else return fail(LASGD_ERR_INVALID_ARGUMENT, "buffer index %d", which);
   return LASGD_OK;
@@ -536,7 +544,59 @@ extern "C" int lasgd_comm_info(lasgd_comm* c, int* rank, int* world, void** xbar
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
   if (rank) *rank = c->rank;
   if (world) *world = c->world;
-  if (xbar) *xbar = c->base + c->off_xbar;
+  if (xbar) *xbar = c->nvls_uc ? c->nvls_uc + c->nvls_off[2] : c->base + c->off_xbar;
+  return LASGD_OK;
+}
+
+// ---------------------------------------------------------------- NVLink SHARP setup
+extern "C" int lasgd_comm_nvls_supported(lasgd_comm* c) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  DeviceGuard g(c->device);
+  return c->dtype == LASGD_F32 && c->world >= 2 ? nvls_supported(c->device) : 0;
+}
+
+static size_t nvls_payload(lasgd_comm* c, size_t off[3]) {
+  const size_t slot = round_up(c->n * c->elem, 256);
+  off[0] = 0;
+  off[1] = slot;
+  off[2] = 2 * slot;
+  return 3 * slot;
+}
+
+extern "C" int lasgd_comm_nvls_create(lasgd_comm* c, int* fd_out) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->nvls) return fail(LASGD_ERR_STATE, "NVLS already set up");
+  if (c->dtype != LASGD_F32) return fail(LASGD_ERR_UNSUPPORTED, "the in-switch mean is fp32 only");
+  DeviceGuard g(c->device);
+  return nvls_create(&c->nvls, c->device, c->world, nvls_payload(c, c->nvls_off), fd_out);
+}
+
+extern "C" int lasgd_comm_nvls_import(lasgd_comm* c, int fd) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  DeviceGuard g(c->device);
+  if (!c->nvls) {
+    int rc = nvls_create(&c->nvls, c->device, c->world, nvls_payload(c, c->nvls_off), nullptr);
+    if (rc) return rc;
+  }
+  return nvls_import(c->nvls, fd);
+}
+
+extern "C" int lasgd_comm_nvls_add_device(lasgd_comm* c) {
+  if (!c || !c->nvls) return fail(LASGD_ERR_STATE, "create or import the multicast object first");
+  DeviceGuard g(c->device);
+  return nvls_add_device(c->nvls);
+}
+
+extern "C" int lasgd_comm_nvls_bind(lasgd_comm* c) {
+  if (!c || !c->nvls) return fail(LASGD_ERR_STATE, "create or import the multicast object first");
+  DeviceGuard g(c->device);
+  void *uc = nullptr, *mc = nullptr;
+  int rc = nvls_bind(c->nvls, &uc, &mc);
+  if (rc) return rc;
+  c->nvls_uc = reinterpret_cast<char*>(uc);
+  c->nvls_mc = reinterpret_cast<char*>(mc);
+  c->push_slot = -1;
+  c->end_seq = 0;
   return LASGD_OK;
 }
 
@@ -624,6 +684,29 @@ static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned lo
 
 extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->nvls_uc) {  // NVLS communicator: the data lives in the multicast region
+    if (algo != LASGD_ALGO_AUTO && algo != LASGD_ALGO_NVLS)
+      return fail(LASGD_ERR_UNSUPPORTED, "an NVLS communicator runs the in-switch mean only (algo %d)", algo);
+    DeviceGuard g(c->device);
+    CommArgs a;
+    unsigned long long s = 0;
+    int rc = prepare_launch(c, snap_slot, a, s);
+    if (rc) return rc;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    c->push_slot = -1;
+    c->end_seq = 0;
+    if (c->gate && (rc = launch_gate(c->world, a, cs))) return rc;
+    // the switch, not the SMs, bounds this kernel: half the SMs issue enough loads
+    // (profiles/r02/allreduce_sweep_p4_nvls.jsonl: 37-74 CTAs at least as fast as 148-512)
+    const int nb = c->nblocks < num_sms() / 2 ? c->nblocks : num_sms() / 2;
+    a.nblocks = nb;
+    rc = launch_nvls_mean(c->world, a, c->nvls_mc + c->nvls_off[snap_slot], c->nvls_mc + c->nvls_off[2], nb, cs);
+    if (rc) return rc;
+    LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+    if (seq) *seq = s;
+    return LASGD_OK;
+  }
+  if (algo == LASGD_ALGO_NVLS) return fail(LASGD_ERR_STATE, "the NVLS mean needs lasgd_comm_nvls_bind first");
   algo = resolve_algo(algo, c->world, c->n * c->elem);
   if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   DeviceGuard g(c->device);
@@ -645,6 +728,7 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
                                       void* delta, const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                                       unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->nvls_uc) return fail(LASGD_ERR_UNSUPPORTED, "an NVLS communicator runs the side-stream mean only");
   // SGD-AR (mode 2) averages gradients that backward wrote into the slots, so there is
   // nothing to push ahead: one-shot or two-shot, chosen like the all-reduce
   if (mode == 2 && c->world < 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round needs P >= 2");
@@ -755,6 +839,7 @@ int comm_fused_round_dyn(lasgd_comm* c, int snap_slot, int algo, void* x, const 
                          const lasgd_sgd_params* sgd, double alpha, int mode, int nblocks,
                          unsigned long long* nonfinite, void* stream, const RoundAdv& adv, unsigned long long* seq) {
   if (!c || !adv.rd) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm or round descriptor");
+  if (c->nvls_uc) return fail(LASGD_ERR_UNSUPPORTED, "an NVLS communicator runs the side-stream mean only");
   if (mode == 2) return fail(LASGD_ERR_UNSUPPORTED, "graph replay of SGD-AR rounds is not built");
   if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
   algo = resolve_fused_algo(algo, c->world, c->n * c->elem);
@@ -822,6 +907,7 @@ extern "C" int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off,
                                        void* m, const lasgd_sgd_params* sgd, int nblocks,
                                        unsigned long long* nonfinite, void* stream, unsigned long long* seq) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->nvls_uc) return fail(LASGD_ERR_UNSUPPORTED, "an NVLS communicator runs the side-stream mean only");
   if (c->world < 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round needs P >= 2");
   if (snap_slot != 0 && snap_slot != 1) return fail(LASGD_ERR_INVALID_ARGUMENT, "snapshot slot %d", snap_slot);
   if (len == 0 || off > c->n || len > c->n - off)
@@ -953,6 +1039,7 @@ extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
   if (c->end_ctr) cudaFree(c->end_ctr);
   if (c->trace_buf) cudaFree(c->trace_buf);
   if (c->status_host) cudaFreeHost(c->status_host);
+  if (c->nvls) nvls_destroy(c->nvls);
   if (c->epoch_host) cudaFreeHost(c->epoch_host);
   if (c->epoch_stream) cudaStreamDestroy(c->epoch_stream);
   if (c->base) cudaFree(c->base);

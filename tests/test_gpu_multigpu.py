@@ -377,6 +377,68 @@ def _w_graph_replay(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_nvls(rank, world, port):
+    """NVLink SHARP mean (tolerance mode): within 1e-6 of the ring-order mean relative to
+    the contributions' magnitude (the north star's reduction-order tolerance), the same bits
+    on every rank, and the overlap pipeline on it within rounding of the oracle's loop."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+    from paper_2203_13085_b200 import _native as N
+
+    _init(rank, world, port)
+    try:
+        probe = L.P2PCommunicator(1024, nvls=True, timeout_s=20.0)
+    except ValueError as e:  # no multicast on this box: nothing to check
+        print(f"rank {rank}: NVLS unavailable ({e})")
+        dist.destroy_process_group()
+        return
+    probe.close()
+    for n in (3, 1001, 65_537, 4_000_037):
+        comm = L.P2PCommunicator(n, nvls=True, nblocks=24, timeout_s=20.0)
+        for rnd in range(3):
+            slot = rnd % 2
+            vecs = [_vec(300 * rnd + 7 * r + n % 13, n) for r in range(world)]
+            comm.snapshots[slot].copy_(torch.from_numpy(vecs[rank]))
+            torch.cuda.synchronize()
+            seq = comm.allreduce(slot, N.ALGO_NVLS)
+            assert comm.wait(seq, 30.0) == 1
+            torch.cuda.synchronize()
+            got = comm.xbar.cpu().numpy().astype(np.float64)
+            ref = O.ring_mean(vecs).astype(np.float64)
+            scale = np.sum(np.abs(np.stack(vecs).astype(np.float64)), axis=0) / world
+            assert np.all(np.abs(got - ref) <= 1e-6 * scale + 1e-30), (n, rnd, rank)
+            sums = [None] * world
+            dist.all_gather_object(sums, comm.xbar.cpu().numpy().tobytes())
+            assert all(x == sums[0] for x in sums), "ranks received different means"
+        dist.barrier()
+        comm.close()
+    # the overlap pipeline (side-stream mean + one-pass boundary) on the in-switch mean
+    n, steps = 65_541, 6
+    x0 = _vec(3, n)
+    grads = np.stack([np.stack([_vec(40 * t + r, n) for r in range(world)]) for t in range(steps)])
+    comm = L.P2PCommunicator(n, nvls=True, nblocks=16, timeout_s=20.0)
+    x = torch.from_numpy(x0.copy()).cuda()
+    compute = torch.cuda.Stream()
+    sgd = L.SgdConfig(0.9, 0.0, 1e-4, True)
+    with torch.cuda.stream(compute):
+        w = L.LASGDWorker(x, torch.zeros_like(x), comm=comm, sync_period=2, alpha=0.5, mode="pull", sgd=sgd,
+                          lr=0.05, pipeline="overlap", compute_stream=compute)
+        for t in range(steps):
+            w.g = torch.from_numpy(grads[t, rank]).cuda()
+            w.step()
+        w.drain()
+    torch.cuda.synchronize()
+    ref, _, _, _ = O.run_lasgd_pull(x0, grads, [0.05] * steps, world, 2, 0.5,
+                                    sgd=O.SgdConfig(0.05, 0.9, 0.0, 1e-4, True))
+    np.testing.assert_allclose(x.cpu().numpy(), ref[rank], rtol=1e-5, atol=1e-6)
+    w.close()
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def _w_full_size(rank, world, port):
     """The bench's configuration at BASELINE size: ResNet-50's n, Nesterov momentum +
     weight decay, sync period 1, fused pipeline with the AUTO algorithm (mirror push at
@@ -609,6 +671,11 @@ def test_sgd_ar_bucketed_bit_exact():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_graph_replay_multi_rank_bit_exact():
     _spawn(_w_graph_replay)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_nvls_mean_within_tolerance():
+    _spawn(_w_nvls)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")

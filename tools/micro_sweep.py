@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--threads", type=int, default=256)
     ap.add_argument("--fused-algos", default="auto,oneshot,push",
                     help="fused-round algorithms to time per size ('' to skip)")
+    ap.add_argument("--nvls-nblocks", default="",
+                    help="also time the in-switch (NVLS, tolerance-mode) mean with these CTA counts")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -126,6 +128,32 @@ def main():
                                       "busbw_equiv_gbs": 2 * (world - 1) / world * 4 * n / (f_ms * 1e-3) / 1e9}),
                           flush=True)
             del g, m
+        if a.nvls_nblocks:
+            nc = L.P2PCommunicator(n, nblocks=32, threads=a.threads, timeout_s=60.0, nvls=True)
+            nc.snapshots[0].copy_(x)
+            nc.snapshots[1].copy_(x)
+            torch.cuda.synchronize()
+            for nb in [int(v) for v in a.nvls_nblocks.split(",")]:
+                nc.set_nblocks(nb)
+                with torch.cuda.stream(s):
+                    for i in range(a.warmup):
+                        nc.allreduce(i % 2, N.ALGO_NVLS, stream=s)
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(s)
+                    for i in range(a.reps):
+                        nc.allreduce(i % 2, N.ALGO_NVLS, stream=s)
+                    e1.record(s)
+                    torch.cuda.synchronize()
+                    ar_ms = tmax(e0.elapsed_time(e1) / a.reps)
+                if rank == 0:
+                    print(json.dumps({"P": world, "MB": 4 * n / 1e6, "n": n, "algo": "nvls", "nblocks": nb,
+                                      "allreduce_ms": ar_ms,
+                                      "busbw_gbs": 2 * (world - 1) / world * 4 * n / (ar_ms * 1e-3) / 1e9}),
+                          flush=True)
+            dist.barrier()
+            nc.close()
         # NCCL all-reduce (sum) of the same buffer, for context (not on the product path)
         y = x.clone()
         for _ in range(a.warmup):
