@@ -370,18 +370,31 @@ def share_fd(fd: Optional[int], rank: int, world: int, group=None) -> int:
 
     import torch.distributed as dist
 
+    import os
+    import struct
+
     name = [f"\0lasgd-nvls-{secrets.token_hex(8)}" if rank == 0 else None]
     dist.broadcast_object_list(name, src=0, group=group)
+    pids = [None] * world
+    dist.all_gather_object(pids, os.getpid(), group=group)
     if rank == 0:
         srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
         srv.bind(name[0])
         srv.listen(world)
         dist.barrier(group=group)
         try:
-            for _ in range(world - 1):
+            served = 0
+            while served < world - 1:
                 conn, _ = srv.accept()
                 with conn:
+                    # hand the descriptor only to this job's ranks (the socket name is
+                    # visible to every process on the node)
+                    pid, _, _ = struct.unpack("3i", conn.getsockopt(socket.SOL_SOCKET, socket.SO_PEERCRED,
+                                                                    struct.calcsize("3i")))
+                    if pid not in pids[1:]:
+                        continue
                     socket.send_fds(conn, [b"f"], [fd])
+                    served += 1
         finally:
             srv.close()
         return fd

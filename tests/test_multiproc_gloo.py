@@ -87,3 +87,30 @@ def test_per_rank_protocol_matches_in_process_reference(tmp_path):
     for r in range(2):
         got = np.load(tmp_path / f"x{r}.npy")
         assert np.array_equal(got.view(np.uint32), xs[r].view(np.uint32))
+
+
+def _w_share_fd(rank, world, port):
+    """The NVLS set-up's descriptor hand-off: rank 0's file descriptor reaches every other
+    rank (SCM_RIGHTS over the abstract UNIX socket, peers checked by SO_PEERCRED)."""
+    import tempfile
+
+    dist = _init(rank, world, port)
+    from paper_2203_13085_b200.collective import share_fd
+
+    fd = None
+    if rank == 0:
+        f = tempfile.TemporaryFile()
+        f.write(b"multicast handle stand-in")
+        f.flush()
+        fd = os.dup(f.fileno())
+    got = share_fd(fd, rank, world)
+    os.lseek(got, 0, os.SEEK_SET)
+    assert os.read(got, 64) == b"multicast handle stand-in"
+    if rank != 0:
+        assert got != fd
+    os.close(got)
+    dist.destroy_process_group()
+
+
+def test_share_fd_reaches_every_rank():
+    mp.spawn(_w_share_fd, args=(3, _port()), nprocs=3, join=True)
