@@ -374,6 +374,45 @@ def _w_graph_replay(rank, world, port):
             ref, _, _, _ = O.run_lasgd_pull(x0, gl, [0.05] * total, world, k, alpha,
                                             sgd=O.SgdConfig(0.05, 0.9, 0.0, 1e-4, True))
             assert _same_bits(a[0], ref[rank]), (algo, k, rank)
+    # the whole training step (zero_grad + forward + backward + fused round over NVLink)
+    # captured into one CUDA graph per minibatch: the same bits as eager steps
+    def train(graphed):
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.Tanh(), torch.nn.Linear(256, 8)).cuda()
+        flat = L.FlatParams(model, align_bytes=256)
+        comm = L.P2PCommunicator(flat.numel, nblocks=16, timeout_s=20.0)
+        gen = torch.Generator(device="cuda").manual_seed(5 + rank)
+        inp = torch.randn(32, 64, device="cuda", generator=gen)
+        tgt = torch.randn(32, 8, device="cuda", generator=gen)
+        compute = torch.cuda.Stream()
+        w = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=2, alpha=0.5, mode="pull", sgd=sgd, lr=0.05,
+                          algo=N.ALGO_PUSH, pipeline="fused", compute_stream=compute)
+
+        def fwd_bwd(t=0):
+            flat.zero_grad()
+            torch.nn.functional.mse_loss(model(inp), tgt).backward()
+
+        with torch.cuda.stream(compute):
+            for _ in range(4):  # eager warm-up rounds (also the staging of the push round)
+                fwd_bwd()
+                w.step()
+            if graphed:
+                g = w.capture_with(fwd_bwd, steps=2)
+                for _ in range(4):
+                    g.replay()
+            else:
+                for _ in range(8):
+                    fwd_bwd()
+                    w.step()
+        torch.cuda.synchronize()
+        out = flat.x.cpu()
+        w.close()
+        dist.barrier()
+        comm.close()
+        return out
+
+    a, b = train(True), train(False)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32)), rank
     dist.destroy_process_group()
 
 
