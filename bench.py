@@ -74,7 +74,8 @@ def parse():
     ap.add_argument("--bucket-mb", type=int, default=25, help="gradient bucket size of the bucketed SGD-AR / DDP legs")
     ap.add_argument("--bucket-ctas", type=int, default=0, help="CTAs of each bucketed SGD-AR launch (0: 2 per SM)")
     ap.add_argument("--legs", default="", help="comma list: run only these training legs (and their baselines)")
-    ap.add_argument("--no-nvls-leg", action="store_true", help="skip the NVLS (in-switch mean) training leg at N>=4")
+    ap.add_argument("--nvls-leg", action="store_true",
+                    help="N>1: add a training leg on the NVLS (in-switch, tolerance-mode) side-stream mean")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="training leg: eager fwd/bwd instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -989,7 +990,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
             "overlap": (lasgd_leg(pipeline="overlap"), "nosync"),
             "overlap_adaptive": (lasgd_leg(pipeline="overlap", adaptive=True, tau_max=5), "nosync")}
     ncomm = None
-    if tcomm is not None and world >= 4 and not args.no_nvls_leg:
+    if tcomm is not None and args.nvls_leg:
         # the overlap pipeline on the in-switch (NVLS, tolerance-mode) side-stream mean
         try:
             ncomm = L.P2PCommunicator(flat.numel, nblocks=args.nblocks, timeout_s=60.0, nvls=True)
