@@ -646,12 +646,11 @@ def main():
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(compute):
-        hold.enqueue(compute)
+        # no hold kernel here: end to end includes the host issuing every step
         f0.record(compute)
         copy_stream.wait_event(f0)  # the first H2D starts inside the timed region
         e2e_loop(we, args.steps)
         f1.record(compute)
-        hold.release()
     torch.cuda.synchronize()
     ms_e2e = max_over_ranks(f0.elapsed_time(f1))
     barrier()
