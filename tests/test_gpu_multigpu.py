@@ -453,6 +453,18 @@ def _w_nvls(rank, world, port):
             assert all(x == sums[0] for x in sums), "ranks received different means"
         dist.barrier()
         comm.close()
+    # the reference-facing transport on it: all_reduce_average through CudaP2PTransport
+    n = 10_007
+    comm = L.P2PCommunicator(n, nvls=True, nblocks=8, timeout_s=20.0)
+    tr = L.CudaP2PTransport(comm)
+    vecs = [_vec(55 + r, n) for r in range(world)]
+    h = tr.submit(0, rank, torch.from_numpy(vecs[rank]).cuda())
+    assert h.wait(30.0) and h.status is L.Status.COMPLETE
+    got = h.result.cpu().numpy().astype(np.float64)
+    scale = np.sum(np.abs(np.stack(vecs).astype(np.float64)), axis=0) / world
+    assert np.all(np.abs(got - O.ring_mean(vecs).astype(np.float64)) <= 1e-6 * scale + 1e-30)
+    dist.barrier()
+    comm.close()
     # the overlap pipeline (side-stream mean + one-pass boundary) on the in-switch mean
     n, steps = 65_541, 6
     x0 = _vec(3, n)
