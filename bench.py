@@ -794,6 +794,12 @@ def main():
             "sync_kernels": kernels,
             "virtual_rank_kernels": vkernels,
             "training": training,
+            # the BASELINE metric's ResNet-50 training throughput (images through forward,
+            # backward and the LASGD step per second, all ranks) beside the sync-path value
+            "training_summary": None if not training or "images_per_s_lasgd" not in training else {
+                "images_per_s": training["images_per_s_lasgd"], "nosync_images_per_s": training["images_per_s_nosync"],
+                "frac_of_nosync": training["images_per_s_lasgd"] / training["images_per_s_nosync"],
+                "exposed_sync_ms_per_step": training["exposed_sync_ms_per_step"], "pipeline": args.pipeline},
         }
         print(json.dumps(line), flush=True)
     if comm is not None:
