@@ -18,8 +18,9 @@ Config (YAML or JSON, schema 1; unknown keys are errors):
     schema: 1
     problem: {kind: mlp, n: 4096, d: 784, hidden: [128], noise: 0.1, data_seed: 0, batch: 32}
     algo: lasgd                     # lasgd | sgd_ar
-    lasgd: {tau_max: 4, adaptive: false, alpha: 1.0, mode: pull, pipeline: overlap}
+    lasgd: {tau_max: 4, adaptive: false, alpha: 1.0, mode: pull, pipeline: overlap, nvls: false}
     sgd_ar: {bucketed: false, bucket_mb: 25}   # bucketed: the all-reduce overlapped with backward
+    # lasgd.nvls: the side-stream mean reduced inside the NVSwitch (tolerance mode, overlap pipeline)
     sgd: {momentum: 0.0, dampening: 0.0, weight_decay: 0.0, nesterov: false}
     lr: {base_lr: 0.01, scale_nodes: 1, warmup_epochs: 0.0, decay_epochs: [], decay_factor: 10.0}
     steps: 100
@@ -48,7 +49,7 @@ DEFAULTS = {
     "schema": 1,
     "problem": {"kind": "mlp", "n": 4096, "d": 784, "hidden": [128], "noise": 0.1, "data_seed": 0, "batch": 32},
     "algo": "lasgd",
-    "lasgd": {"tau_max": 4, "adaptive": False, "alpha": 1.0, "mode": "pull", "pipeline": "overlap"},
+    "lasgd": {"tau_max": 4, "adaptive": False, "alpha": 1.0, "mode": "pull", "pipeline": "overlap", "nvls": False},
     "sgd_ar": {"bucketed": False, "bucket_mb": 25},
     "sgd": {"momentum": 0.0, "dampening": 0.0, "weight_decay": 0.0, "nesterov": False},
     "lr": {"base_lr": 0.01, "scale_nodes": 1, "warmup_epochs": 0.0, "decay_epochs": [], "decay_factor": 10.0},
@@ -126,6 +127,9 @@ def resolve(cfg: dict) -> dict:
     if la["mode"] == "delta" and la["alpha"] != 1:
         errors.append("lasgd.mode=delta is the reference LASGD rule, which requires alpha = beta = 1 "
                       "(optimizer.py:71-72); use mode=pull for alpha < 1")
+    need(isinstance(la["nvls"], bool), "lasgd.nvls must be a boolean")
+    if la["nvls"] is True and la["pipeline"] != "overlap":
+        errors.append("lasgd.nvls=true runs the in-switch side-stream mean: it needs pipeline=overlap")
     if la["pipeline"] == "fused" and la["adaptive"]:
         errors.append("lasgd.pipeline=fused implements the deterministic schedule only (adaptive needs overlap)")
     need(isinstance(sa["bucketed"], bool), "sgd_ar.bucketed must be a boolean")
@@ -236,7 +240,8 @@ def cmd_run(cfg: dict, out_dir: str) -> int:
 
         warm_loss = batch_loss
 
-    comm = L.P2PCommunicator(flat.numel, timeout_s=120.0) if world > 1 else None
+    nvls = cfg["algo"] == "lasgd" and la["nvls"]
+    comm = L.P2PCommunicator(flat.numel, timeout_s=120.0, nvls=nvls) if world > 1 else None
     compute = torch.cuda.Stream(device=dev, priority=-1)
     with torch.cuda.stream(compute):  # untimed: cuBLAS/cuDNN/autograd initialisation
         for _ in range(2):

@@ -119,3 +119,12 @@ def test_sgd_ar_bucketed_option_validated():
         cli.resolve({"sgd_ar": {"bucketed": "yes", "bucket_mb": 0, "colour": 1}})
     msg = str(e.value)
     assert "sgd_ar.bucketed" in msg and "sgd_ar.bucket_mb" in msg and "unknown key 'sgd_ar.colour'" in msg
+
+
+def test_nvls_option_needs_the_overlap_pipeline():
+    assert cli.resolve({"lasgd": {"nvls": True}})["lasgd"]["nvls"] is True
+    with pytest.raises(cli.ConfigError) as e:
+        cli.resolve({"lasgd": {"nvls": True, "pipeline": "fused"}})
+    assert "pipeline=overlap" in str(e.value)
+    with pytest.raises(cli.ConfigError):
+        cli.resolve({"lasgd": {"nvls": 1}})

@@ -86,7 +86,8 @@ def _w_cli(rank, world, port, tmp):
 
     for name, over in (("lasgd", {}), ("adaptive", {"lasgd": {"adaptive": True, "tau_max": 3}}),
                        ("sgd_ar", {"algo": "sgd_ar"}),
-                       ("sgd_ar_bucketed", {"algo": "sgd_ar", "sgd_ar": {"bucketed": True, "bucket_mb": 0.1}})):
+                       ("sgd_ar_bucketed", {"algo": "sgd_ar", "sgd_ar": {"bucketed": True, "bucket_mb": 0.1}}),
+                       ("lasgd_nvls", {"lasgd": {"nvls": True}})):
         path = _cfg(tmp, f"{name}_r{rank}", **over)
         assert cli.main(["run", "--config", path, "--out", os.path.join(tmp, name)]) == 0
     dist.destroy_process_group()
@@ -112,6 +113,10 @@ def test_cli_run_multi_gpu(tmp_path):
         if name == "adaptive":
             assert all(t is None or 1 <= t <= 3 for r in rows for t in r["node_tau"])
         assert s["final_loss"] == s["final_loss"]  # finite
+    # LASGD on the in-switch mean (tolerance mode): the same trajectory to rounding
+    a = json.load(open(os.path.join(str(tmp_path / "lasgd"), "summary.json")))
+    b = json.load(open(os.path.join(str(tmp_path / "lasgd_nvls"), "summary.json")))
+    assert abs(a["final_loss"] - b["final_loss"]) <= 1e-4 * abs(a["final_loss"])
     # SGD-AR with the all-reduce bucketed under backward: the same trajectory, bit for bit
     a = json.load(open(os.path.join(str(tmp_path / "sgd_ar"), "summary.json")))
     b = json.load(open(os.path.join(str(tmp_path / "sgd_ar_bucketed"), "summary.json")))
