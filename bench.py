@@ -74,6 +74,11 @@ def parse():
     ap.add_argument("--bucket-mb", type=int, default=25, help="gradient bucket size of the bucketed SGD-AR / DDP legs")
     ap.add_argument("--bucket-ctas", type=int, default=0, help="CTAs of each bucketed SGD-AR launch (0: 2 per SM)")
     ap.add_argument("--legs", default="", help="comma list: run only these training legs (and their baselines)")
+    ap.add_argument("--step-graph", action="store_true",
+                    help="N=1 training legs: capture forward + backward + the sync step in one graph per leg "
+                         "(each leg then replays its own forward/backward graph, whose memory placement alone "
+                         "moves the step time by up to ~0.4 ms; by default every leg replays the same "
+                         "forward/backward graph and issues its sync step after it)")
     ap.add_argument("--nvls-leg", action="store_true",
                     help="N>1: add a training leg on the NVLS (in-switch, tolerance-mode) side-stream mean")
     ap.add_argument("--no-train", action="store_true")
@@ -894,7 +899,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
                                   sync_period=args.sync_period, alpha=args.alpha,
                                   mode="pull", sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
                                   fused_nblocks=args.fused_nblocks, **wkw)
-                if graphed and world == 1 and not wkw.get("adaptive"):
+                if graphed and world == 1 and not wkw.get("adaptive") and args.step_graph:
                     # one CUDA graph: zero_grad + forward + backward + local step (+ round boundary)
                     fwd_bwd()  # the fwd/bwd graph exists: cuDNN autotuned, the shared pool warm
                     k = args.sync_period if wkw.get("sync", True) else 1
@@ -1064,8 +1069,9 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     out = {"model": f"{spec['ctor']} (torchvision, random init, {hw}x{hw}, {spec['classes']} classes)",
            "batch_per_gpu": args.batch, "precision": "bf16 autocast fwd/bwd, fp32 params",
            "flat_align_bytes": args.flat_align, "blocks": f"{R} repetitions x {B} steps per leg, legs interleaved",
-           "fwd_bwd": ("cuda_graph (N=1: zero_grad+fwd+bwd+local step+round in one graph; N>1: fwd/bwd graph, "
-                       "sync launches after it)" if graphed else "eager")}
+           "fwd_bwd": (("cuda_graph (zero_grad+fwd+bwd+local step+round in one graph per leg)" if args.step_graph
+                        and world == 1 else "cuda_graph (one zero_grad+fwd+bwd graph shared by the legs, sync "
+                        "launches after it)") if graphed else "eager")}
     for name, (_, base) in legs.items():
         med = st.median(times[name])
         e = {"images_per_s": world * args.batch / (med / 1e3), "ms_per_step": med, "ms_per_step_blocks": times[name]}
