@@ -242,7 +242,8 @@ def virtual_rank_kernels(n, dev, stream, hbm_peak, traffic, reps=10):
     GPU's HBM instead, so the roofline is HBM.  Algorithmic bytes per round (all ranks;
     B = 4n): push P*(7B + 4(P-1)/P*B) (local step + pull + next snapshot, staged
     contributions read, mean pushed, peers' means read, next-snapshot chunks pushed);
-    two-shot P*(3B - B/P); one-shot 2P*B (each source read once, each mean written)."""
+    two-shot P*(3B - B/P); one-shot P*(P+1)*B (every rank reads all P sources and
+    writes its mean)."""
     import torch
 
     from paper_2203_13085_b200 import _native as N
@@ -297,7 +298,7 @@ def virtual_rank_kernels(n, dev, stream, hbm_peak, traffic, reps=10):
             if P == 2:
                 entry("oneshot_virtual_p2",
                       timeit(lambda: K.mean_virtual(xbars, snaps[0], algo=N.ALGO_ONESHOT, stream=stream)),
-                      2 * P * B, 1)
+                      P * (P + 1) * B, 1)
             del xs, gs, ms_, snaps, xbars, stages
             torch.cuda.empty_cache()
     return out

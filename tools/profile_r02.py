@@ -11,7 +11,7 @@ fp32, B = 102.23 MB), every kernel in the order bench.py times it:
    reduce-scatter + all-gather launches).
 
     python tools/profile_r02.py && ncu --set full --clock-control none --import-source on \\
-        -k regex:'k_sgd_dyn|k_push|k_twoshot' -o gpurun_out/prof_r02 python tools/profile_r02.py
+        -k regex:'k_sgd_dyn|k_push|k_twoshot|k_oneshot' -o gpurun_out/prof_r02 python tools/profile_r02.py
 """
 
 import os
@@ -57,6 +57,9 @@ def main():
                                  weight_decay=1e-4, nesterov=True, first_step=t == 0, alpha=1.0)
         for _ in range(2):
             K.mean_virtual(xbars, snaps[0], algo=N.ALGO_TWOSHOT)
+        if P == 2:
+            for _ in range(2):
+                K.mean_virtual(xbars, snaps[0], algo=N.ALGO_ONESHOT)
         torch.cuda.synchronize()
         del xs, gs, ms, snaps, xbars, stages
         torch.cuda.empty_cache()
