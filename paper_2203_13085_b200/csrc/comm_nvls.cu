@@ -152,10 +152,15 @@ int nvls_create(NvlsState** out, int device, int world, size_t payload_bytes, in
 }
 
 int nvls_import(NvlsState* s, int fd) {
-  if (s->have_mc) return fail(LASGD_ERR_STATE, "multicast object already present");
-  CU_TRY(drv().MemImportFromShareableHandle(&s->mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+  if (s->have_mc) {
+    close(fd);
+    return fail(LASGD_ERR_STATE, "multicast object already present");
+  }
+  const CUresult r =
+      drv().MemImportFromShareableHandle(&s->mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  close(fd);  // the import holds its own reference
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuMemImportFromShareableHandle(multicast)");
   s->have_mc = true;
-  close(fd);
   return LASGD_OK;
 }
 
