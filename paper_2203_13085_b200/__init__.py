@@ -30,6 +30,7 @@ from .collective import (  # noqa: E402
     ring_schedule,
 )
 from .engine import BucketedSGDARWorker, LASGDWorker, SGDARWorker, SyncGraph  # noqa: E402
+from .torch_optim import LASGD  # noqa: E402
 from .graphs import GraphedStep  # noqa: E402
 from .flat import FlatParams  # noqa: E402
 from .optimizer import (  # noqa: E402
@@ -51,7 +52,7 @@ from .params import ChunkSpec, as_device_vector, blend, mean_of_vectors, partiti
 from .problems import LrSchedule, lr_at  # noqa: E402
 
 __all__ = [
-    "BucketedSGDARWorker", "ChunkSpec", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
+    "BucketedSGDARWorker", "ChunkSpec", "LASGD", "CollectiveFailure", "CollectiveHandle", "CudaLoopbackTransport", "CudaP2PTransport",
     "DimensionMismatchError", "FlatParams", "GraphedStep", "HyperParamError", "HyperParams", "LASGDWorker", "LrSchedule", "SyncGraph", "ModelDivergenceError",
     "NodeState", "NonFiniteError", "P2PCommunicator", "RingSchedule", "RingStep", "SGDARWorker", "SgdConfig", "Status", "TickAction", "TransportFault",
     "AllReduceOutcome", "all_reduce_average", "as_device_vector", "execute_allreduce", "blend", "bytes_per_node", "easgd_round_robin_exchange",

@@ -172,10 +172,12 @@ class LASGDWorker:
     def _ensure_lr_table(self, clock_end: int) -> None:
         """Device learning-rate table covering local clocks [0, clock_end)."""
         if self.schedule is None:
-            if getattr(self, "_lr_len", 0) != 1:
+            # a constant rate may have been changed since the last capture (an LR
+            # scheduler writing worker.lr): re-upload whenever it differs
+            if getattr(self, "_lr_len", 0) != 1 or getattr(self, "_lr_const", None) != float(self.lr):
                 table = (ctypes.c_double * 1)(float(self.lr))
                 N.check(N.lib().lasgd_worker_set_lr_table(self._h, table, 1), "lasgd_worker_set_lr_table")
-                self._lr_len = 1
+                self._lr_len, self._lr_const = 1, float(self.lr)
             return
         if getattr(self, "_lr_len", 0) >= clock_end:
             return

@@ -692,6 +692,57 @@ def _w_fault_end_signal(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_torch_optim(rank, world, port):
+    """The torch.optim front end across ranks (comm="auto": x0 broadcast from rank 0, a
+    P2PCommunicator built inside): bit-identical to driving LASGDWorker over an explicit
+    communicator (parameters and snapshot)."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+
+    _init(rank, world, port)
+    g = torch.Generator(device="cuda").manual_seed(100 + rank)  # rank-local data
+    inp, tgt = torch.randn(32, 16, device="cuda", generator=g), torch.randn(32, 3, device="cuda", generator=g)
+
+    def model():
+        torch.manual_seed(rank)  # different init per rank: auto mode must broadcast rank 0's
+        return torch.nn.Sequential(torch.nn.Linear(16, 40), torch.nn.ReLU(), torch.nn.Linear(40, 3)).cuda()
+
+    def run(use_opt):
+        m = model()
+        if use_opt:
+            opt = L.LASGD(m, lr=0.05, momentum=0.9, weight_decay=1e-4, sync_period=3)
+            w, comm = opt.worker, None
+        else:
+            flat = L.FlatParams(m, align_bytes=256)
+            dist.broadcast(flat.x, 0)
+            comm = L.P2PCommunicator(flat.numel)
+            w = L.LASGDWorker(flat.x, flat.g, comm=comm, sync_period=3, lr=0.05, pipeline="fused",
+                              sgd=L.SgdConfig(0.9, 0.0, 1e-4, False))
+        for _ in range(9):
+            if use_opt:
+                opt.zero_grad()
+            else:
+                flat.zero_grad()
+            torch.nn.functional.mse_loss(m(inp), tgt).backward()
+            (opt if use_opt else w).step()
+        (opt if use_opt else w).drain()
+        torch.cuda.synchronize()
+        x = torch.cat([p.detach().reshape(-1) for p in m.parameters()]).cpu().numpy()
+        snap = w.state.x_snapshot.cpu().numpy()
+        dist.barrier()
+        if use_opt:
+            opt.close()
+        else:
+            w.close()
+            comm.close()
+        return x, snap
+
+    (xa, sa), (xb, sb) = run(True), run(False)
+    assert _same_bits(xa, xb) and _same_bits(sa, sb), rank
+    dist.destroy_process_group()
+
+
 def _spawn(fn):
     import torch.multiprocessing as mp
 
@@ -757,3 +808,8 @@ def test_watchdog_missing_end_signal_fails_every_rank():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_watchdog_fault_fails_every_rank():
     _spawn(_w_fault)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_torch_optim_front_end_multi_rank_bit_exact():
+    _spawn(_w_torch_optim)

@@ -104,8 +104,8 @@ def _w_share_fd(rank, world, port):
         f.flush()
         fd = os.dup(f.fileno())
     got = share_fd(fd, rank, world)
-    os.lseek(got, 0, os.SEEK_SET)
-    assert os.read(got, 64) == b"multicast handle stand-in"
+    # the descriptors share one open file description (one offset): read positionally
+    assert os.pread(got, 64, 0) == b"multicast handle stand-in"
     if rank != 0:
         assert got != fd
     os.close(got)
