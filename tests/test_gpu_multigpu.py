@@ -26,7 +26,10 @@ def _free_port():
 def _init(rank, world, port):
     import torch.distributed as dist
 
-    torch.cuda.set_device(rank)
+    import os
+
+    # test_gpu_p2p_one_gpu.py puts every rank on GPU 0 (separate processes and contexts)
+    torch.cuda.set_device(0 if os.environ.get("LASGD_TEST_ONE_GPU") else rank)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
 
 

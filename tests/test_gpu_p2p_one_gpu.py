@@ -1,0 +1,46 @@
+"""The multi-process NVLink-protocol code run with every rank on ONE GPU.
+
+Each rank is its own process with its own CUDA context, exactly as under torchrun; the
+peers' regions are CUDA-IPC mapped (same-device IPC), so every piece of the P2P path
+runs for real — the IPC handle exchange, the entry / mid / end-of-round signals and
+epochs, the host-mapped done_seq, the push staging parity, the cooperative staged push
+at P >= 3, the watchdog — where the virtual-rank tests replace the flag barriers with
+stream order.  The GPU time-slices the contexts, so a CTA spinning on a peer's flag is
+preempted and the peer's kernel runs; the results must be bit-exact against the oracle
+as on separate GPUs.  This is what a 1-GPU box (the round-end test run) sees of the
+multi-rank protocol; tests/test_gpu_multigpu.py runs the same workers one GPU per rank.
+
+Not here: the NVLS mean (multicast needs distinct devices) and the adaptive laggard test
+(time-slicing serialises the ranks, so fast ranks cannot run ahead)."""
+
+import os
+import socket
+
+import pytest
+import torch
+
+import test_gpu_multigpu as M
+
+pytestmark = pytest.mark.gpu
+
+WORKERS = [("_w_allreduce", 2), ("_w_worker_loop", 2), ("_w_sgd_ar", 2), ("_w_sgd_ar_bucketed", 2),
+           ("_w_graph_replay", 2), ("_w_full_size", 2), ("_w_max_size", 2), ("_w_ragged", 2), ("_w_ragged", 3),
+           ("_w_fault", 2), ("_w_fault_end_signal", 2), ("_w_torch_optim", 2),
+           ("_w_allreduce", 4), ("_w_worker_loop", 4), ("_w_graph_replay", 4)]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+@pytest.mark.parametrize("name,world", WORKERS, ids=[f"{n[3:]}-p{w}" for n, w in WORKERS])
+def test_protocol_on_one_gpu(name, world, monkeypatch):
+    import torch.multiprocessing as mp
+
+    monkeypatch.setenv("LASGD_TEST_ONE_GPU", "1")  # inherited by the spawned ranks
+    mp.spawn(getattr(M, name), args=(world, _port()), nprocs=world, join=True)
