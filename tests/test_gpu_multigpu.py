@@ -28,8 +28,9 @@ def _init(rank, world, port):
 
     import os
 
-    # test_gpu_p2p_one_gpu.py puts every rank on GPU 0 (separate processes and contexts)
-    torch.cuda.set_device(0 if os.environ.get("LASGD_TEST_ONE_GPU") else rank)
+    # LASGD_TEST_GPUS=k: rank r on GPU r % k, several ranks (processes, contexts) per GPU
+    # (test_gpu_p2p_one_gpu.py: k = 1)
+    torch.cuda.set_device(rank % int(os.environ.get("LASGD_TEST_GPUS", 1 << 30)))
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
 
 

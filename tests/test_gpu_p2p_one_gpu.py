@@ -8,7 +8,8 @@ at P >= 3, the watchdog — where the virtual-rank tests replace the flag barrie
 stream order.  The GPU time-slices the contexts, so a CTA spinning on a peer's flag is
 preempted and the peer's kernel runs; the results must be bit-exact against the oracle
 as on separate GPUs.  This is what a 1-GPU box (the round-end test run) sees of the
-multi-rank protocol; tests/test_gpu_multigpu.py runs the same workers one GPU per rank.
+multi-rank protocol, and the only place the protocol runs with eight ranks;
+tests/test_gpu_multigpu.py runs the same workers one GPU per rank.
 
 Not here: the NVLS mean (multicast needs distinct devices) and the adaptive laggard test
 (time-slicing serialises the ranks, so fast ranks cannot run ahead)."""
@@ -26,7 +27,10 @@ pytestmark = pytest.mark.gpu
 WORKERS = [("_w_allreduce", 2), ("_w_worker_loop", 2), ("_w_sgd_ar", 2), ("_w_sgd_ar_bucketed", 2),
            ("_w_graph_replay", 2), ("_w_full_size", 2), ("_w_max_size", 2), ("_w_ragged", 2), ("_w_ragged", 3),
            ("_w_fault", 2), ("_w_fault_end_signal", 2), ("_w_torch_optim", 2),
-           ("_w_allreduce", 4), ("_w_worker_loop", 4), ("_w_graph_replay", 4)]
+           ("_w_allreduce", 4), ("_w_worker_loop", 4), ("_w_graph_replay", 4),
+           # P = 8 (no 8-GPU box is reachable from the build pool): the staged push and
+           # two-shot with eight real ranks, at the full ResNet-50 size too
+           ("_w_allreduce", 8), ("_w_worker_loop", 8), ("_w_full_size", 8)]
 
 
 def _port():
@@ -42,5 +46,5 @@ def _port():
 def test_protocol_on_one_gpu(name, world, monkeypatch):
     import torch.multiprocessing as mp
 
-    monkeypatch.setenv("LASGD_TEST_ONE_GPU", "1")  # inherited by the spawned ranks
+    monkeypatch.setenv("LASGD_TEST_GPUS", "1")  # inherited by the spawned ranks
     mp.spawn(getattr(M, name), args=(world, _port()), nprocs=world, join=True)
