@@ -855,6 +855,7 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
     import torchvision
 
     import paper_2203_13085_b200 as L
+    from paper_2203_13085_b200 import _native as N
 
     spec = MODELS[args.model]
     torch.backends.cudnn.benchmark = True
@@ -902,10 +903,12 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
             if key in cached:
                 w, one_graph = cached[key]
             else:
+                kw = dict(wkw)
+                leg_algo = kw.pop("algo", algo_code)
                 w = L.LASGDWorker(flat.x, flat.g, comm=leg_comm if leg_comm is not None else tcomm,
                                   sync_period=args.sync_period, alpha=args.alpha,
-                                  mode="pull", sgd=sgd, lr=lr, algo=algo_code, compute_stream=compute,
-                                  fused_nblocks=args.fused_nblocks, **wkw)
+                                  mode="pull", sgd=sgd, lr=lr, algo=leg_algo, compute_stream=compute,
+                                  fused_nblocks=args.fused_nblocks, **kw)
                 if graphed and world == 1 and not wkw.get("adaptive") and args.step_graph:
                     # one CUDA graph: zero_grad + forward + backward + local step (+ round boundary)
                     fwd_bwd()  # the fwd/bwd graph exists: cuDNN autotuned, the shared pool warm
@@ -1016,6 +1019,13 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         if ncomm is not None:
             legs["overlap_nvls"] = (lasgd_leg(leg_comm=ncomm, pipeline="overlap"), "nosync")
     if tcomm is not None:
+        # the overlap pipeline with the side-stream mean's NVLink traffic on the copy engines
+        # (the overlap leg's AUTO picks it at P >= 3; overlap_sm keeps the SM mean there)
+        legs["overlap_ce"] = (lasgd_leg(pipeline="overlap", algo=N.ALGO_CE), "nosync")
+        if world >= 3:
+            legs["overlap_sm"] = (lasgd_leg(pipeline="overlap", algo=tcomm.resolve_algo(N.ALGO_AUTO)
+                                            if tcomm.resolve_algo(N.ALGO_AUTO) != N.ALGO_CE else N.ALGO_TWOSHOT),
+                                  "nosync")
         legs.update({"sgd_ar": (sgd_ar_leg("p2p"), "nosync"), "sgd_ar_nccl": (sgd_ar_leg("nccl"), "nosync"),
                      "nosync_eager": (nosync_eager_leg(), "nosync_eager"),
                      "sgd_ar_bucketed": (sgd_ar_leg("bucketed"), "nosync_eager"),

@@ -55,6 +55,9 @@ extern "C" {
                             (tolerance mode, see lasgd_comm_nvls_bind) */
 #define LASGD_ALGO_PUSH 3 /* fused round only, data moved by remote stores: P = 2 mirrors the peer's
                              snapshot; P >= 3 owners reduce locally staged chunks, means pushed */
+#define LASGD_ALGO_CE 5 /* all-reduce only: the two-shot mean with the NVLink traffic moved by the
+                           copy engines (SMs reduce the own chunk and flip flags); bit-identical to
+                           LASGD_ALGO_TWOSHOT */
 
 #define LASGD_MAX_RANKS 8
 #define LASGD_MAX_BLOCKS 512

@@ -32,6 +32,7 @@ ALGO_ONESHOT = 1
 ALGO_TWOSHOT = 2
 ALGO_PUSH = 3
 ALGO_NVLS = 4
+ALGO_CE = 5  # side-stream all-reduce with the NVLink traffic on the copy engines
 MAX_RANKS = 8
 MAX_BLOCKS = 512
 IPC_HANDLE_BYTES = 64

@@ -17,7 +17,9 @@ constexpr int kDoneSlots = 64;
 constexpr int kEvents = 64;
 
 // host-mapped status block layout (uint32 words)
-enum { ST_ERR = 0, ST_PEER, ST_PHASE, ST_BLOCK, ST_SEQ_LO, ST_SEQ_HI, ST_RANK, ST_WORDS = 16 };
+// ST_CLAIM: taken (CAS) by the first failure, which fills the fields and publishes
+// ST_ERR last, so a host that sees ST_ERR also sees the fields describing it
+enum { ST_ERR = 0, ST_PEER, ST_PHASE, ST_BLOCK, ST_SEQ_LO, ST_SEQ_HI, ST_RANK, ST_CLAIM, ST_WORDS = 16 };
 enum { ERR_NONE = 0, ERR_TIMEOUT = 1, ERR_INJECTED = 2 };
 
 struct CommArgs {
@@ -200,7 +202,7 @@ __device__ __forceinline__ T mean_div(T s) {
 }
 
 __device__ inline void report_failure(const CommArgs& a, int code, int peer, int phase, int block, int rank) {
-  if (atomicCAS(&a.status[ST_ERR], 0u, (uint32_t)code) == 0u) {
+  if (atomicCAS(&a.status[ST_CLAIM], 0u, 1u) == 0u) {
     a.status[ST_PEER] = peer;
     a.status[ST_PHASE] = phase;
     a.status[ST_BLOCK] = block;
@@ -208,6 +210,7 @@ __device__ inline void report_failure(const CommArgs& a, int code, int peer, int
     a.status[ST_SEQ_HI] = (uint32_t)(cseq(a) >> 32);
     a.status[ST_RANK] = rank;
     __threadfence_system();
+    st_release_sys(&a.status[ST_ERR], (uint32_t)code);
   }
 }
 

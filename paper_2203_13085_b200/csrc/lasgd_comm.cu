@@ -41,6 +41,7 @@
 #include <mutex>
 #include <utility>
 
+#include "comm_ce.h"
 #include "comm_launch.cuh"
 #include "comm_nvls.h"
 #include "lasgd_common.cuh"
@@ -447,9 +448,29 @@ extern "C" int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr) {
   return LASGD_OK;
 }
 
+// The all-reduce's AUTO: the copy-engine two-shot for large buffers at P >= 4 (P=4:
+// 256 MB 0.683 vs 0.710 ms SM two-shot, 1 GB 2.485 vs 2.740, NCCL 2.500; at 102 MB and
+// below the CE round's ~40 us of fixed cost loses; profiles/r02/ce_sweep_p4.jsonl),
+// otherwise resolve_algo.  (Not for SGD-AR buckets or fused rounds: they are SM kernels.)
+static int resolve_allreduce_algo(const lasgd_comm* c, int algo) {
+  const size_t bytes = c->n * c->elem;
+  if (algo == LASGD_ALGO_AUTO && !c->nvls_uc && c->world >= 4 && bytes >= ((size_t)192 << 20)) return LASGD_ALGO_CE;
+  return resolve_algo(algo, c->world, bytes);
+}
+
+int lasgd::comm_side_algo(lasgd_comm* c, int algo) {
+  // under forward/backward the CE mean's NVLink traffic costs no SM time: ResNet-50 at
+  // N=4 exposes 0.241-0.246 ms/step on it against 0.282-0.304 on the SM two-shot (three
+  // runs), at N=3 0.231 against 0.264; at N=2 the SM one-shot exposes less (0.19-0.21 vs
+  // 0.22) (profiles/r02/ce_train_n*.json)
+  if (algo == LASGD_ALGO_AUTO && !c->nvls_uc && c->world >= 3 && c->n * c->elem >= ((size_t)64 << 20))
+    return LASGD_ALGO_CE;
+  return algo;
+}
+
 extern "C" int lasgd_comm_resolve_algo(lasgd_comm* c, int algo) {
   if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
-  return resolve_algo(algo, c->world, c->n * c->elem);
+  return resolve_allreduce_algo(c, algo);
 }
 
 extern "C" int lasgd_resolve_fused_algo_for(int world, size_t bytes) {
@@ -658,6 +679,7 @@ static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned lo
     a.skip_signal_phase = c->fault_phase;
     // collective.py:271-279: the faulting round fails on every rank, this one included
     uint32_t* st = c->status_host;
+    __atomic_store_n(&st[ST_CLAIM], 1u, __ATOMIC_SEQ_CST);
     st[ST_PEER] = c->rank;
     st[ST_PHASE] = c->fault_phase;
     st[ST_BLOCK] = 0;
@@ -707,6 +729,33 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
     return LASGD_OK;
   }
   if (algo == LASGD_ALGO_NVLS) return fail(LASGD_ERR_STATE, "the NVLS mean needs lasgd_comm_nvls_bind first");
+  algo = resolve_allreduce_algo(c, algo);
+  if (algo == LASGD_ALGO_CE && c->world > 1) {  // copy-engine two-shot (comm_ce.cu)
+    DeviceGuard g(c->device);
+    CommArgs a;
+    unsigned long long s = 0;
+    int rc = prepare_launch(c, snap_slot, a, s);
+    if (rc) return rc;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    c->push_slot = -1;  // the contributions overwrite the push round's staging
+    c->end_seq = 0;
+    CeRound r;
+    memset(&r, 0, sizeof(r));
+    r.snap_local = c->base + c->off_snap[snap_slot];
+    r.xbar_local = c->base + c->off_xbar;
+    r.stage_local = c->base + c->off_stage;
+    r.stage_elems = c->stage_elems;
+    for (int q = 0; q < c->world; ++q) {
+      r.stage_peer[q] = c->peer_base[q] + c->off_stage;
+      r.xbar_peer[q] = c->peer_base[q] + c->off_xbar;
+    }
+    rc = launch_ce_mean(c->dtype, c->world, a, r, c->nblocks, cs);  // its own entry gate
+    if (rc) return rc;
+    LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+    if (seq) *seq = s;
+    return LASGD_OK;
+  }
+  if (algo == LASGD_ALGO_CE) algo = LASGD_ALGO_ONESHOT;  // P = 1: the copy
   algo = resolve_algo(algo, c->world, c->n * c->elem);
   if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   DeviceGuard g(c->device);
@@ -733,6 +782,7 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
   // nothing to push ahead: one-shot or two-shot, chosen like the all-reduce
   if (mode == 2 && c->world < 2) return fail(LASGD_ERR_INVALID_ARGUMENT, "the SGD-AR round needs P >= 2");
   if (mode == 2 && algo == LASGD_ALGO_PUSH) return fail(LASGD_ERR_INVALID_ARGUMENT, "no push form of the SGD-AR round");
+  if (algo == LASGD_ALGO_CE) return fail(LASGD_ERR_UNSUPPORTED, "the copy-engine mean is a side-stream all-reduce only");
   algo = mode == 2 ? resolve_algo(algo, c->world, c->n * c->elem) : resolve_fused_algo(algo, c->world, c->n * c->elem);
   const bool push = algo == LASGD_ALGO_PUSH;
   if (!push && algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT)
@@ -924,6 +974,12 @@ extern "C" int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off,
   if (rc) return rc;
   if (nblocks <= 0) nblocks = 2 * num_sms() <= kMaxB ? 2 * num_sms() : kMaxB;
   if (nblocks > kMaxB) return fail(LASGD_ERR_INVALID_ARGUMENT, "nblocks=%d > %d", nblocks, kMaxB);
+  // one-shot, or two-shot for large buckets at P >= 3 (the bucket's own partition decides
+  // who reduces what; the summation order stays the whole vector's).  Validated before
+  // prepare_launch takes a sequence number: a refused call must not desynchronise ranks.
+  algo = resolve_algo(algo == LASGD_ALGO_PUSH ? LASGD_ALGO_AUTO : algo, c->world, len * c->elem);
+  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT)
+    return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d: bucketed SGD-AR rounds are one-shot or two-shot", algo);
   DeviceGuard dg(c->device);
   CommArgs a;
   unsigned long long s = 0;
@@ -940,10 +996,6 @@ extern "C" int lasgd_comm_sgd_ar_range(lasgd_comm* c, int snap_slot, size_t off,
   a.nonfinite = nonfinite;
   c->push_slot = -1;
   c->end_seq = 0;
-  // one-shot, or two-shot for large buckets at P >= 3 (the bucket's own partition decides
-  // who reduces what; the summation order stays the whole vector's)
-  algo = resolve_algo(algo == LASGD_ALGO_PUSH ? LASGD_ALGO_AUTO : algo, c->world, len * c->elem);
-  if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   a.phases = 3;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (c->dtype == LASGD_F32)
@@ -1002,8 +1054,9 @@ extern "C" int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len) {
   if (!c || !buf || !len) return fail(LASGD_ERR_INVALID_ARGUMENT, "null argument");
   const uint32_t* st = c->status_host;
   const unsigned long long fs = (unsigned long long)st[ST_SEQ_LO] | ((unsigned long long)st[ST_SEQ_HI] << 32);
-  static const char* const kPhaseName[] = {"entry", "mid", "end-of-round", "launch gate"};
-  const char* phase = st[ST_PHASE] < 4 ? kPhaseName[st[ST_PHASE]] : "unknown";
+  static const char* const kPhaseName[] = {"entry", "mid", "end-of-round", "launch gate",
+                                           "copy-engine contributions", "copy-engine means"};
+  const char* phase = st[ST_PHASE] < 6 ? kPhaseName[st[ST_PHASE]] : "unknown";
   switch (st[ST_ERR]) {
     case ERR_NONE: snprintf(buf, len, "ok"); break;
     case ERR_TIMEOUT:

@@ -244,6 +244,9 @@ int comm_mirror_get(lasgd_comm* c, CommMirror* m);
 int comm_mirror_set(lasgd_comm* c, const CommMirror& m);
 // Record the completion event of launch c->seq on `stream` (after a graph replay).
 int comm_record_last(lasgd_comm* c, void* stream);
+// Algorithm of the overlap pipeline's side-stream mean for `algo` (AUTO: the copy-engine
+// two-shot where it interferes least with forward/backward, else as lasgd_comm_allreduce).
+int comm_side_algo(lasgd_comm* c, int algo);
 // The fused round (K7 one-shot or K8 push) in graph-replayable form: sequence number,
 // snapshot slot, learning rate, first step and delta reset from adv.rd; requires the
 // steady state of a deterministic loop (the previous launch was a round of the same

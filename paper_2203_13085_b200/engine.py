@@ -104,6 +104,8 @@ class LASGDWorker:
         K._check(x, g)
         if comm is not None and (comm.n != x.numel() or comm.dtype != x.dtype):
             raise ValueError("communicator buffers do not match x")
+        if algo == N.ALGO_CE and pipeline == "fused" and comm is not None and comm.world > 1 and sync:
+            raise ValueError("the copy-engine mean is a side-stream all-reduce: use pipeline='overlap'")
         self.comm = comm
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
@@ -389,8 +391,8 @@ class SGDARWorker:
                  compute_stream: Optional[torch.cuda.Stream] = None, flat=None):
         if (schedule is None) == (lr is None):
             raise ValueError("give exactly one of schedule / lr")
-        if algo == N.ALGO_PUSH:
-            raise ValueError("the push algorithm exists only as a fused LASGD round")
+        if algo in (N.ALGO_PUSH, N.ALGO_CE):
+            raise ValueError("the SGD-AR round is one kernel: one-shot or two-shot (push / copy-engine are LASGD forms)")
         self.sgd = sgd or SgdConfig()
         self.sgd.validate()
         K._check(x)
@@ -496,6 +498,8 @@ class BucketedSGDARWorker:
             raise ValueError("communicator buffers do not match the flat parameters")
         if bucket_bytes <= 0:
             raise ValueError("bucket_bytes must be positive")
+        if algo in (N.ALGO_PUSH, N.ALGO_CE):
+            raise ValueError("bucketed SGD-AR rounds are one-shot or two-shot")
         self.sgd = sgd or SgdConfig()
         self.sgd.validate()
         self.flat, self.comm = flat, comm

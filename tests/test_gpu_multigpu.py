@@ -747,6 +747,106 @@ def _w_torch_optim(rank, world, port):
     dist.destroy_process_group()
 
 
+def _w_ce(rank, world, port):
+    """The copy-engine mean (ALGO_CE: contributions and means moved by cudaMemcpyAsync over
+    the IPC-mapped regions, flags by one-warp kernels): bit-exact against the ring-order
+    oracle at ragged sizes in f32 and f64, interleaved with SM all-reduces and push rounds
+    on the same communicator (the CE mean clobbers the push staging), gated launches, the
+    overlap worker loop on it against the oracle, and a dropped signal failing every rank."""
+    import torch.distributed as dist
+
+    import paper_2203_13085_b200 as L
+    from oracle import lasgd_oracle as O
+    from paper_2203_13085_b200 import _native as N
+
+    _init(rank, world, port)
+    for dtype in (torch.float32, torch.float64):
+        npdt = np.float32 if dtype == torch.float32 else np.float64
+        for n in (1, 3, 1001, 65_537, 4_000_037):
+            comm = L.P2PCommunicator(n, dtype=dtype, nblocks=24, timeout_s=20.0)
+            assert comm.resolve_algo(N.ALGO_CE) == N.ALGO_CE
+            for rnd, algo in enumerate((N.ALGO_CE, N.ALGO_CE, N.ALGO_TWOSHOT, N.ALGO_CE, N.ALGO_ONESHOT, N.ALGO_CE)):
+                slot = rnd % 2
+                vecs = [_vec(5000 * rnd + 10 * r + n, n, npdt) for r in range(world)]
+                comm.snapshots[slot].copy_(torch.from_numpy(vecs[rank]))
+                torch.cuda.synchronize()
+                seq = comm.allreduce(slot, algo)
+                assert comm.wait(seq, 30.0) == 1
+                torch.cuda.synchronize()
+                assert _same_bits(comm.xbar.cpu().numpy(), O.ring_mean(vecs)), (n, rnd, algo, rank)
+            comm.set_gate(True)
+            for rnd in range(2):
+                vecs = [_vec(91 + 10 * r + rnd, n, npdt) for r in range(world)]
+                comm.snapshots[rnd].copy_(torch.from_numpy(vecs[rank]))
+                torch.cuda.synchronize()
+                seq = comm.allreduce(rnd, N.ALGO_CE)
+                assert comm.wait(seq, 30.0) == 1
+                assert _same_bits(comm.xbar.cpu().numpy(), O.ring_mean(vecs)), (n, "gated", rank)
+            comm.set_gate(False)
+            dist.barrier()
+            comm.close()
+    # the overlap pipeline on the CE mean, mixed with fused push rounds on one communicator
+    n, steps = 100_003, 8
+    x0 = _vec(11, n)
+    grads = np.stack([np.stack([_vec(300 * t + r, n) for r in range(world)]) for t in range(steps)])
+    mom = L.SgdConfig(0.9, 0.0, 1e-4, True)
+    comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
+    for k, pipe, algo in ((1, "overlap", N.ALGO_CE), (2, "fused", N.ALGO_PUSH), (1, "overlap", N.ALGO_CE),
+                          (3, "overlap", N.ALGO_CE)):
+        x = torch.from_numpy(x0.copy()).cuda()
+        g = torch.empty_like(x)
+        compute = torch.cuda.Stream()
+        with torch.cuda.stream(compute):
+            w = L.LASGDWorker(x, g, comm=comm, sync_period=k, alpha=0.5, sgd=mom, lr=0.05, mode="pull",
+                              compute_stream=compute, pipeline=pipe, algo=algo)
+            for t in range(steps):
+                g.copy_(torch.from_numpy(grads[t, rank]))
+                w.step()
+            w.drain()
+        torch.cuda.synchronize()
+        xs, _, _, _ = O.run_lasgd_pull(x0, grads, np.full(steps, 0.05), world, k, 0.5,
+                                       sgd=O.SgdConfig(0.05, 0.9, 0.0, 1e-4, True))
+        assert _same_bits(x.cpu().numpy(), xs[rank]), (k, pipe, algo, rank)
+        w.close()
+        dist.barrier()
+    with pytest.raises(ValueError):
+        L.LASGDWorker(x, g, comm=comm, pipeline="fused", algo=N.ALGO_CE, lr=0.1)
+    comm.close()
+    # ResNet-50 size, overlap pipeline with AUTO: the side-stream mean is the CE mean at
+    # P >= 4 (the SM mean below), bit-exact either way
+    n, steps = 25_557_032, 3
+    x0 = _vec(12, n)
+    grads = np.stack([np.stack([_vec(310 * t + r, n) for r in range(world)]) for t in range(steps)])
+    comm = L.P2PCommunicator(n, timeout_s=30.0)
+    x = torch.from_numpy(x0.copy()).cuda()
+    g = torch.empty_like(x)
+    w = L.LASGDWorker(x, g, comm=comm, sync_period=1, lr=0.05, mode="pull", pipeline="overlap")
+    for t in range(steps):
+        g.copy_(torch.from_numpy(grads[t, rank]))
+        w.step()
+    w.drain()
+    torch.cuda.synchronize()
+    xs, _, _, _ = O.run_lasgd_pull(x0, grads, np.full(steps, 0.05), world, 1, 1.0)
+    assert _same_bits(x.cpu().numpy(), xs[rank]), ("full size overlap", rank)
+    w.close()
+    dist.barrier()
+    comm.close()
+    # watchdog: rank 1 drops its contributions signal (phase 1) or its means signal (phase 2)
+    for phase in (1, 2):
+        comm = L.P2PCommunicator(4096, nblocks=8, timeout_s=1.0, fault_seq=2 if rank == 1 else -1, fault_phase=phase)
+        tr = L.CudaP2PTransport(comm, algo=N.ALGO_CE)
+        h1 = tr.submit(0, rank, comm.snapshots[0])
+        assert h1.wait(30.0) and h1.status is L.Status.COMPLETE
+        h2 = tr.submit(1, rank, comm.snapshots[1])
+        assert h2.wait(30.0)
+        assert h2.status is L.Status.FAILED, (rank, h2.status)
+        assert ("copy-engine" in h2.diagnostic) or ("injected" in h2.diagnostic), h2.diagnostic
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.close()
+    dist.destroy_process_group()
+
+
 def _spawn(fn):
     import torch.multiprocessing as mp
 
@@ -817,3 +917,8 @@ def test_watchdog_fault_fails_every_rank():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_torch_optim_front_end_multi_rank_bit_exact():
     _spawn(_w_torch_optim)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_copy_engine_mean_bit_exact():
+    _spawn(_w_ce)

@@ -26,7 +26,7 @@ pytestmark = pytest.mark.gpu
 
 WORKERS = [("_w_allreduce", 2), ("_w_worker_loop", 2), ("_w_sgd_ar", 2), ("_w_sgd_ar_bucketed", 2),
            ("_w_graph_replay", 2), ("_w_full_size", 2), ("_w_max_size", 2), ("_w_ragged", 2), ("_w_ragged", 3),
-           ("_w_fault", 2), ("_w_fault_end_signal", 2), ("_w_torch_optim", 2),
+           ("_w_fault", 2), ("_w_fault_end_signal", 2), ("_w_torch_optim", 2), ("_w_ce", 2), ("_w_ce", 3),
            ("_w_allreduce", 4), ("_w_worker_loop", 4), ("_w_graph_replay", 4),
            # P = 8 (no 8-GPU box is reachable from the build pool): the staged push and
            # two-shot with eight real ranks, at the full ResNet-50 size too
