@@ -73,6 +73,23 @@ class LASGD(torch.optim.Optimizer):
         self.worker.step()
         return loss
 
+    def state_dict(self):
+        """Not provided: the optimizer state lives in the native worker (momentum, snapshot
+        slots, round counters, the communicator's sequence numbers), and the reference
+        has no checkpointing either.  Refusing beats silently returning a
+        state without the momentum."""
+        raise NotImplementedError("LASGD state lives in the native worker; checkpoint the model and re-create the optimizer")
+
+    def load_state_dict(self, state_dict) -> None:
+        raise NotImplementedError("LASGD state lives in the native worker; checkpoint the model and re-create the optimizer")
+
+    def add_param_group(self, param_group) -> None:
+        # the flat buffers are laid out once, at construction (torch.optim.Optimizer's own
+        # __init__ calls this for the module's parameters, before the worker exists)
+        if hasattr(self, "worker"):
+            raise NotImplementedError("the flat parameter buffer is fixed at construction: no new parameter groups")
+        super().add_param_group(param_group)
+
     def drain(self) -> None:
         """Order the compute stream after any in-flight mean (end of training)."""
         self.worker.drain()

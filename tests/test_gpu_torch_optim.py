@@ -67,6 +67,10 @@ def test_optimizer_close_to_torch_sgd_and_scheduler():
     for p1, p2 in zip(m1.parameters(), m2.parameters()):
         torch.testing.assert_close(p1, p2, rtol=1e-5, atol=1e-6)
     assert opt.state_view.local_clock == 8
+    with pytest.raises(NotImplementedError):
+        opt.state_dict()
+    with pytest.raises(NotImplementedError):
+        opt.add_param_group({"params": [torch.zeros(3, device="cuda", requires_grad=True)]})
     opt.close()
 
 
