@@ -81,6 +81,8 @@ def parse():
                          "forward/backward graph and issues its sync step after it)")
     ap.add_argument("--nvls-leg", action="store_true",
                     help="N>1: add a training leg on the NVLS (in-switch, tolerance-mode) side-stream mean")
+    ap.add_argument("--side-priority", type=int, default=0,
+                    help="training legs: CUDA priority of the communicator's side stream (0 low, -1 high)")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="training leg: eager fwd/bwd instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -870,7 +872,8 @@ def run_training(args, dev, comm, world, rank, sgd, lr, algo_code, compute, barr
         # identical x0 on every rank (Algorithm 1 line 1)
         dist.broadcast(flat.x, 0)
         if comm.n != flat.numel:  # 256-B aligned tensors: the flat vector carries padding
-            tcomm = L.P2PCommunicator(flat.numel, nblocks=args.nblocks, timeout_s=60.0)
+            tcomm = L.P2PCommunicator(flat.numel, nblocks=args.nblocks, timeout_s=60.0,
+                                      stream_priority=args.side_priority)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     hw = spec["image"]
