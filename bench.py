@@ -672,6 +672,7 @@ def main():
 
     # ---------------- isolated kernel timings (each kernel alone, for the roofline detail)
     iso = {}
+    ar_iso = {}
     with torch.cuda.stream(compute):
         m = torch.zeros_like(x)
         s0, s1, xb = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
@@ -701,6 +702,15 @@ def main():
                 return seq
 
             iso["allreduce"] = timeit(ar, reps=10)
+            # every transport of the exchange on the same snapshot, beside NCCL's all-reduce
+            # of the same buffer (max over ranks; BASELINE configs[4]'s comparison at this size)
+            for nm, code in (("oneshot", N.ALGO_ONESHOT), ("twoshot", N.ALGO_TWOSHOT), ("ce", N.ALGO_CE)):
+                barrier()
+                ar_iso[nm] = max_over_ranks(timeit(lambda c=code: comm.allreduce(0, c, stream=compute), reps=10))
+            nbuf = comm.snapshots[0].clone()
+            barrier()
+            ar_iso["nccl_allreduce_sum"] = max_over_ranks(timeit(lambda: dist.all_reduce(nbuf), reps=10))
+            del nbuf
         fk = dict(m=m, momentum=0.9, weight_decay=1e-4, nesterov=True, alpha=args.alpha,
                   nblocks=args.fused_nblocks, stream=compute)
         if comm is not None:
@@ -806,6 +816,7 @@ def main():
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "sync_kernels": kernels,
+            "allreduce_isolated_ms": ar_iso or None,
             "virtual_rank_kernels": vkernels,
             "training": training,
             # the BASELINE metric's ResNet-50 training throughput (images through forward,
