@@ -584,6 +584,11 @@ def main():
     w.reset_records()
     with torch.cuda.stream(compute):
         hold.enqueue(compute)
+        if comm is not None:
+            # the holds are released at slightly different host times on each rank; a
+            # one-warp device barrier behind them lines the ranks' clocks up, so the max
+            # over ranks does not count one rank's release skew as step time
+            comm.device_barrier(compute)
         e0.record(compute)
         h0 = time.perf_counter()
         if graph is not None:

@@ -262,6 +262,11 @@ int lasgd_comm_peers_ahead(lasgd_comm* c, unsigned long long seq);
  * all-reduce never holds a CTA per SM while a late peer catches up (which would
  * starve the compute stream).  Collective setting: every rank must use the same. */
 int lasgd_comm_set_gate(lasgd_comm* c, int on);
+/* Stream-ordered device barrier across the ranks (one warp, its own epoch counter and
+ * flag slots: takes no launch sequence number and leaves the round chain and the push
+ * staging untouched).  Collective: every rank calls it the same number of times.  The
+ * benchmark starts its timed region behind it so every rank's clock starts together. */
+int lasgd_comm_barrier(lasgd_comm* c, void* stream);
 /* The caller rewrote a snapshot slot outside the fused rounds (also resets the chain of
  * end-of-round signals the next K7 would otherwise enter on).  The next push round
  * re-stages the current snapshot first. */

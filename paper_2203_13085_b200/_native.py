@@ -153,6 +153,7 @@ SIGNATURES = {
     "lasgd_resolve_fused_algo_for": (_I, [_I, _SZ]),
     "lasgd_comm_peers_ahead": (_I, [_P, ctypes.c_ulonglong]),
     "lasgd_comm_set_gate": (_I, [_P, _I]),
+    "lasgd_comm_barrier": (_I, [_P, _P]),
     "lasgd_comm_set_nblocks": (_I, [_P, _I]),
     "lasgd_comm_set_trace": (_I, [_P, _I]),
     "lasgd_comm_read_trace": (_I, [_P, _P, _I]),

@@ -601,6 +601,12 @@ class P2PCommunicator:
         """Gate every all-reduce behind a one-warp wait for all peers (collective setting)."""
         N.check(N.lib().lasgd_comm_set_gate(self._h, int(bool(on))))
 
+    def device_barrier(self, stream=None) -> None:
+        """Stream-ordered barrier across the ranks (one warp; no launch sequence number, so
+        the round chain and push staging are untouched).  Collective."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        N.check(N.lib().lasgd_comm_barrier(self._h, ctypes.c_void_p(s.cuda_stream)), "lasgd_comm_barrier")
+
     def peers_ahead(self, seq: int) -> bool:
         """True if some peer already entered a launch later than ``seq``."""
         return bool(N.check(N.lib().lasgd_comm_peers_ahead(self._h, seq)))

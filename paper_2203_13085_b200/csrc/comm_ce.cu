@@ -133,6 +133,28 @@ static int ce_mean_t(int P, const CommArgs& a, const CeRound& r, int nblocks, cu
   }
 }
 
+template <int P>
+__global__ void __launch_bounds__(32) k_rank_barrier(CommArgs a) {
+  const size_t slot = (size_t)2 * kMaxB * kMaxR + (size_t)5 * kMaxR;
+  if (threadIdx.x < P) st_release_sys(a.pad[threadIdx.x] + slot + a.rank, a.epoch);
+  rank_wait<P>(a, 5, a.epoch, 0, a.rank);
+}
+
+int launch_rank_barrier(int P, const CommArgs& a, cudaStream_t s) {
+  switch (P) {
+    case 2: k_rank_barrier<2><<<1, 32, 0, s>>>(a); break;
+    case 3: k_rank_barrier<3><<<1, 32, 0, s>>>(a); break;
+    case 4: k_rank_barrier<4><<<1, 32, 0, s>>>(a); break;
+    case 5: k_rank_barrier<5><<<1, 32, 0, s>>>(a); break;
+    case 6: k_rank_barrier<6><<<1, 32, 0, s>>>(a); break;
+    case 7: k_rank_barrier<7><<<1, 32, 0, s>>>(a); break;
+    case 8: k_rank_barrier<8><<<1, 32, 0, s>>>(a); break;
+    default: return fail(LASGD_ERR_UNSUPPORTED, "device barrier needs 2 <= P <= %d, got %d", kMaxR, P);
+  }
+  LASGD_CUDA_TRY(cudaGetLastError());
+  return LASGD_OK;
+}
+
 int launch_ce_mean(int dtype, int P, const CommArgs& a, const CeRound& r, int nblocks, cudaStream_t s) {
   return dtype == LASGD_F64 ? ce_mean_t<double>(P, a, r, nblocks, s) : ce_mean_t<float>(P, a, r, nblocks, s);
 }

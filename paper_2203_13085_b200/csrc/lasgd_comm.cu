@@ -319,6 +319,7 @@ struct lasgd_comm {
   bool trace_on = false;
   bool gate = false;           // launch k_gate ahead of every all-reduce (side-stream use)
   unsigned long long seq = 0;  // launches issued
+  uint32_t bar_epoch = 0;      // lasgd_comm_barrier calls (own flag slots, no sequence number)
   // NVLink SHARP (tolerance mode): once bound, the snapshot slots and the mean buffer live
   // in a multicast-bound allocation: nvls_uc (this rank's view) / nvls_mc (the switch's)
   NvlsState* nvls = nullptr;
@@ -546,6 +547,27 @@ extern "C" int lasgd_comm_peers_ahead(lasgd_comm* c, unsigned long long seq) {
   for (int q = 0; q < c->world; ++q)
     if (q != c->rank && (int32_t)(ep[q] - (uint32_t)seq) > 0) return 1;
   return 0;
+}
+
+extern "C" int lasgd_comm_barrier(lasgd_comm* c, void* stream) {
+  if (!c) return fail(LASGD_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->world < 2) return LASGD_OK;
+  if (!c->opened) return fail(LASGD_ERR_STATE, "lasgd_comm_open has not been called");
+  if (c->poisoned || c->status_host[ST_ERR] != ERR_NONE) {
+    c->poisoned = true;
+    return fail(LASGD_ERR_COLLECTIVE, "communicator failed earlier; re-create it");
+  }
+  DeviceGuard g(c->device);
+  CommArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int r = 0; r < c->world; ++r) a.pad[r] = reinterpret_cast<uint32_t*>(c->peer_base[r]);
+  a.rank = c->rank;
+  a.epoch = ++c->bar_epoch;
+  a.seq = c->seq;  // diagnostics only
+  a.timeout_ns = c->timeout_ns;
+  a.skip_signal_phase = -1;
+  a.status = c->status_dev;
+  return launch_rank_barrier(c->world, a, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int lasgd_comm_invalidate_staging(lasgd_comm* c) {
@@ -1055,8 +1077,8 @@ extern "C" int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len) {
   const uint32_t* st = c->status_host;
   const unsigned long long fs = (unsigned long long)st[ST_SEQ_LO] | ((unsigned long long)st[ST_SEQ_HI] << 32);
   static const char* const kPhaseName[] = {"entry", "mid", "end-of-round", "launch gate",
-                                           "copy-engine contributions", "copy-engine means"};
-  const char* phase = st[ST_PHASE] < 6 ? kPhaseName[st[ST_PHASE]] : "unknown";
+                                           "copy-engine contributions", "copy-engine means", "device"};
+  const char* phase = st[ST_PHASE] < 7 ? kPhaseName[st[ST_PHASE]] : "unknown";
   switch (st[ST_ERR]) {
     case ERR_NONE: snprintf(buf, len, "ok"); break;
     case ERR_TIMEOUT:

@@ -783,6 +783,12 @@ def _w_ce(rank, world, port):
                 assert comm.wait(seq, 30.0) == 1
                 assert _same_bits(comm.xbar.cpu().numpy(), O.ring_mean(vecs)), (n, "gated", rank)
             comm.set_gate(False)
+            # the device barrier takes no launch sequence number
+            before = comm.launches()
+            for _ in range(3):
+                comm.device_barrier()
+            torch.cuda.synchronize()
+            assert comm.launches() == before
             dist.barrier()
             comm.close()
     # the overlap pipeline on the CE mean, mixed with fused push rounds on one communicator
@@ -792,7 +798,7 @@ def _w_ce(rank, world, port):
     mom = L.SgdConfig(0.9, 0.0, 1e-4, True)
     comm = L.P2PCommunicator(n, nblocks=16, timeout_s=20.0)
     for k, pipe, algo in ((1, "overlap", N.ALGO_CE), (2, "fused", N.ALGO_PUSH), (1, "overlap", N.ALGO_CE),
-                          (3, "overlap", N.ALGO_CE)):
+                          (3, "overlap", N.ALGO_CE), (1, "fused", N.ALGO_PUSH)):
         x = torch.from_numpy(x0.copy()).cuda()
         g = torch.empty_like(x)
         compute = torch.cuda.Stream()
@@ -802,6 +808,8 @@ def _w_ce(rank, world, port):
             for t in range(steps):
                 g.copy_(torch.from_numpy(grads[t, rank]))
                 w.step()
+                if t % 3 == 1:  # device barriers between rounds leave the round chain intact
+                    comm.device_barrier(compute)
             w.drain()
         torch.cuda.synchronize()
         xs, _, _, _ = O.run_lasgd_pull(x0, grads, np.full(steps, 0.05), world, k, 0.5,
