@@ -709,7 +709,8 @@ def main():
             iso["allreduce"] = timeit(ar, reps=10)
             # every transport of the exchange on the same snapshot, beside NCCL's all-reduce
             # of the same buffer (max over ranks; BASELINE configs[4]'s comparison at this size)
-            for nm, code in (("oneshot", N.ALGO_ONESHOT), ("twoshot", N.ALGO_TWOSHOT), ("ce", N.ALGO_CE)):
+            for nm, code in (("oneshot", N.ALGO_ONESHOT), ("twoshot", N.ALGO_TWOSHOT), ("push", N.ALGO_PUSH),
+                             ("ce", N.ALGO_CE)):
                 barrier()
                 ar_iso[nm] = max_over_ranks(timeit(lambda c=code: comm.allreduce(0, c, stream=compute), reps=10))
             nbuf = comm.snapshots[0].clone()

@@ -53,8 +53,10 @@ extern "C" {
 #define LASGD_ALGO_TWOSHOT 2
 #define LASGD_ALGO_NVLS 4 /* all-reduce only, NVLS communicators: reduced inside the NVSwitch
                             (tolerance mode, see lasgd_comm_nvls_bind) */
-#define LASGD_ALGO_PUSH 3 /* fused round only, data moved by remote stores: P = 2 mirrors the peer's
-                             snapshot; P >= 3 owners reduce locally staged chunks, means pushed */
+#define LASGD_ALGO_PUSH 3 /* data moved by remote stores.  Fused round: P = 2 mirrors the peer's
+                             snapshot; P >= 3 owners reduce locally staged chunks, means pushed.
+                             All-reduce: the push mean (scatter to owners' staging, owner reduces,
+                             means stored into every rank), bit-identical to the two-shot */
 #define LASGD_ALGO_CE 5 /* all-reduce only: the two-shot mean with the NVLink traffic moved by the
                            copy engines (SMs reduce the own chunk and flip flags); bit-identical to
                            LASGD_ALGO_TWOSHOT */

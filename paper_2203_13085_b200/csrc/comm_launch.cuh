@@ -65,6 +65,12 @@ int launch_fused(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, in
 template <typename T, bool VIRTUAL>
 int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int threads, cudaStream_t s);
 
+// the all-reduce with every byte moved by remote stores (ALGO_PUSH through lasgd_comm_allreduce)
+template <typename T>
+int launch_push_mean(int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s);
+extern template int launch_push_mean<float>(int, const CommArgs&, dim3, int, cudaStream_t);
+extern template int launch_push_mean<double>(int, const CommArgs&, dim3, int, cudaStream_t);
+
 #define LASGD_EXTERN_LAUNCHERS(T, V)                                                                          \
   extern template int launch_allreduce<T, V>(int, int, const CommArgs&, dim3, int, cudaStream_t);            \
   extern template int launch_fused<T, V>(int, const CommArgs&, const FusedRound<T>&, dim3, int, cudaStream_t, \

@@ -40,6 +40,33 @@ int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int
 #undef LASGD_PCASE
 }
 
+template <typename T>
+int launch_push_mean(int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
+#define LASGD_MCASE(PP)                                                       \
+  case PP: {                                                                  \
+    auto kern = k_push_mean<T, PP, (PP <= 4 && sizeof(T) == 4 ? 4 : 2)>;      \
+    CommArgs aa = a;                                                          \
+    const int cap = coop_capacity(kern, threads);                             \
+    if ((int)grid.x > cap) grid.x = cap;                                      \
+    aa.nblocks = grid.x;                                                      \
+    return launch_kernel(true, kern, grid, threads, s, aa);                   \
+  }
+  switch (P) {
+    LASGD_MCASE(2)
+    LASGD_MCASE(3)
+    LASGD_MCASE(4)
+    LASGD_MCASE(5)
+    LASGD_MCASE(6)
+    LASGD_MCASE(7)
+    LASGD_MCASE(8)
+    default: return fail(LASGD_ERR_UNSUPPORTED, "push mean needs 2 <= P <= %d, got %d", kMaxR, P);
+  }
+#undef LASGD_MCASE
+}
+
+template int launch_push_mean<float>(int, const CommArgs&, dim3, int, cudaStream_t);
+template int launch_push_mean<double>(int, const CommArgs&, dim3, int, cudaStream_t);
+
 template int launch_push<float, false>(int, const CommArgs&, const FusedRound<float>&, dim3, int, cudaStream_t);
 template int launch_push<float, true>(int, const CommArgs&, const FusedRound<float>&, dim3, int, cudaStream_t);
 template int launch_push<double, false>(int, const CommArgs&, const FusedRound<double>&, dim3, int, cudaStream_t);

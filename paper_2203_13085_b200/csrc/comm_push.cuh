@@ -225,6 +225,108 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
   if (!VIRTUAL) publish_done(a);
 }
 
+// ------------------------------------------------------------------ push mean (ALGO_PUSH all-reduce)
+// K3's result with every byte moved by remote STORES, one cooperative launch:
+//   scatter: chunk c of my snapshot -> owner c's staging [cur][me] (posted NVLink writes),
+//     rank-level end signal (kind 1, this launch's epoch); wait for every rank's;
+//   reduce: my chunk in ring order from my snapshot + the staged contributions, / P,
+//     stored into my xbar and every peer's;
+//   rank-level mid barrier: every rank's means have landed everywhere.
+// Per rank: NVLink out 2(P-1)/P B as stores (as the push round), all loads local.  The
+// staging slots and end signals are the push round's: lasgd_comm_allreduce marks the
+// staging as not holding round contributions afterwards.
+template <typename T, int P, int U>
+__global__ void __launch_bounds__(256, 2) k_push_mean(CommArgs a) {
+  constexpr int W = Pack<T>::W;
+  const int rank = a.rank;
+  const int b = blockIdx.x;
+  const size_t n = a.n;
+  const int cur = a.cur;
+  const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
+  unsigned long long* const q0 = a.tile_ctr;
+  unsigned long long* const q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
+  auto soff = [&](int c, size_t j) { return j - chunk_bound(n, P, c) / W * W; };
+  trace_mark(a, b, 0);
+  chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
+    [&](int c, size_t p0, size_t p1) {
+      T* dst = stage_ptr<T>(a, c, cur, rank, P);
+      for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+        Pack<T> v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) v[u] = ld_stream(snap_own + pu * W);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) st_plain(dst + soff(c, pu * W), v[u]);
+        }
+      }
+    },
+    [&](int c, size_t j) { stage_ptr<T>(a, c, cur, rank, P)[soff(c, j)] = snap_own[j]; });
+  rank_signal<P>(a, 1, a.end_ctr, rank);
+  bool ok = rank_wait<P>(a, 1, a.epoch, b, rank);
+  trace_mark(a, b, 1);
+  if (ok) {
+    size_t cs, ce, cp0, cp1;
+    chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
+    const size_t base = cs / W * W;
+    const T* const stage0 = stage_ptr<T>(a, rank, cur, 0, P);
+    const size_t selems = a.stage_elems;
+    auto src = [&](int q, size_t j) -> const T* {
+      return q == rank ? snap_own + j : stage0 + (size_t)q * selems + (j - base);
+    };
+    tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
+      for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
+        Pack<T> v[U][P];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) v[u][q] = ld_stream(src(q, pu * W));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t pu = p + (size_t)u * blockDim.x;
+          if (pu < p1) {
+            const size_t j = pu * W;
+            Pack<T> z;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+              T lane[P];
+#pragma unroll
+              for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+              z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+            }
+#pragma unroll
+            for (int q = 0; q < P; ++q) st_plain(reinterpret_cast<T*>(a.xbar[q]) + j, z);
+          }
+        }
+      }
+    });
+    if (b == 0) {  // unaligned head / tail elements of the own chunk
+      const size_t he = cp0 * W < ce ? cp0 * W : ce;
+      const size_t ts = cp1 * W > he ? cp1 * W : he;
+      auto scalar = [&](size_t j) {
+        T lane[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) lane[q] = *src(q, j);
+        const T zb = mean_div<T, P>(rot_sum<T, P>(lane, rank));
+#pragma unroll
+        for (int q = 0; q < P; ++q) reinterpret_cast<T*>(a.xbar[q])[j] = zb;
+      };
+      for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
+      for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
+    }
+  }
+  if (ok) ok = rank_barrier<P>(a, b, rank);
+  trace_mark(a, b, 3);
+  publish_done(a);
+}
+
 // ------------------------------------------------------------------ mirror push round (K8, P = 2)
 // At P = 2 the push round keeps a full mirror of the peer's snapshot in local HBM: the
 // staging area (2 parities x 2 sources x n/2) is re-used as [parity][n].  Each round

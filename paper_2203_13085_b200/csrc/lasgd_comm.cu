@@ -449,14 +449,17 @@ extern "C" int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr) {
   return LASGD_OK;
 }
 
-// The all-reduce's AUTO: the copy-engine two-shot for large buffers at P >= 4 (P=4:
-// 256 MB 0.683 vs 0.710 ms SM two-shot, 1 GB 2.485 vs 2.740, NCCL 2.500; at 102 MB and
-// below the CE round's ~40 us of fixed cost loses; profiles/r02/ce_sweep_p4.jsonl),
-// otherwise resolve_algo.  (Not for SGD-AR buckets or fused rounds: they are SM kernels.)
+// The all-reduce's AUTO at P = 3-4 (measured; profiles/r02/pm_sweep_p{3,4}.jsonl): where
+// resolve_algo picks the two-shot, the push mean (every byte moved by stores) is faster
+// at every size (P=4: 16 MB 0.065 vs 0.079 ms, 102 MB 0.279 vs 0.305; P=3 102 MB 0.248 vs
+// 0.278), and from 192 MB the copy-engine mean is faster still (P=4: 256 MB 0.644 vs
+// 0.665, 1 GB 2.408 vs 2.631).  Otherwise (P = 2: one-shot; P >= 5, unmeasured on
+// hardware) resolve_algo.  Not for SGD-AR buckets or fused rounds: they have their own.
 static int resolve_allreduce_algo(const lasgd_comm* c, int algo) {
   const size_t bytes = c->n * c->elem;
-  if (algo == LASGD_ALGO_AUTO && !c->nvls_uc && c->world >= 4 && bytes >= ((size_t)192 << 20)) return LASGD_ALGO_CE;
-  return resolve_algo(algo, c->world, bytes);
+  const int a = resolve_algo(algo, c->world, bytes);
+  if (algo != LASGD_ALGO_AUTO || c->nvls_uc || c->world < 3 || c->world > 4 || a != LASGD_ALGO_TWOSHOT) return a;
+  return bytes >= ((size_t)192 << 20) ? LASGD_ALGO_CE : LASGD_ALGO_PUSH;
 }
 
 int lasgd::comm_side_algo(lasgd_comm* c, int algo) {
@@ -464,7 +467,7 @@ int lasgd::comm_side_algo(lasgd_comm* c, int algo) {
   // N=4 exposes 0.241-0.246 ms/step on it against 0.282-0.304 on the SM two-shot (three
   // runs), at N=3 0.231 against 0.264; at N=2 the SM one-shot exposes less (0.19-0.21 vs
   // 0.22) (profiles/r02/ce_train_n*.json)
-  if (algo == LASGD_ALGO_AUTO && !c->nvls_uc && c->world >= 3 && c->n * c->elem >= ((size_t)64 << 20))
+  if (algo == LASGD_ALGO_AUTO && !c->nvls_uc && c->world >= 3 && c->world <= 4 && c->n * c->elem >= ((size_t)64 << 20))
     return LASGD_ALGO_CE;
   return algo;
 }
@@ -777,7 +780,24 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
     if (seq) *seq = s;
     return LASGD_OK;
   }
-  if (algo == LASGD_ALGO_CE) algo = LASGD_ALGO_ONESHOT;  // P = 1: the copy
+  if (algo == LASGD_ALGO_PUSH && c->world > 1) {  // the mean by remote stores (comm_push.cuh)
+    DeviceGuard g(c->device);
+    CommArgs a;
+    unsigned long long s = 0;
+    int rc = prepare_launch(c, snap_slot, a, s);
+    if (rc) return rc;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    c->push_slot = -1;  // the staging now holds this mean's contributions, not a round's
+    c->end_seq = 0;
+    if (c->gate && (rc = launch_gate(c->world, a, cs))) return rc;
+    rc = c->dtype == LASGD_F64 ? launch_push_mean<double>(c->world, a, dim3(c->nblocks), c->threads, cs)
+                               : launch_push_mean<float>(c->world, a, dim3(c->nblocks), c->threads, cs);
+    if (rc) return rc;
+    LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
+    if (seq) *seq = s;
+    return LASGD_OK;
+  }
+  if (algo == LASGD_ALGO_CE || algo == LASGD_ALGO_PUSH) algo = LASGD_ALGO_ONESHOT;  // P = 1: the copy
   algo = resolve_algo(algo, c->world, c->n * c->elem);
   if (algo != LASGD_ALGO_ONESHOT && algo != LASGD_ALGO_TWOSHOT) return fail(LASGD_ERR_INVALID_ARGUMENT, "algo %d", algo);
   DeviceGuard g(c->device);

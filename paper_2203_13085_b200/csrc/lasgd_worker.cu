@@ -132,8 +132,8 @@ static int submit_allreduce(lasgd_worker* w, int slot) {
   LASGD_CUDA_TRY(cudaEventRecord(w->ev_snap, w->compute));
   LASGD_CUDA_TRY(cudaStreamWaitEvent(w->side, w->ev_snap, 0));
   unsigned long long s = 0;
-  // the push algorithm exists only as a fused round; the side-stream mean uses auto
-  const int algo = comm_side_algo(w->comm, w->cfg.algo == LASGD_ALGO_PUSH ? LASGD_ALGO_AUTO : w->cfg.algo);
+  // (ALGO_PUSH here is the push mean: the all-reduce with every byte moved by stores)
+  const int algo = comm_side_algo(w->comm, w->cfg.algo);
   int rc = issue(w, K_ALLREDUCE, w->side,
                  [&] { return lasgd_comm_allreduce(w->comm, slot, algo, (void*)w->side, &s); });
   if (rc) return rc;

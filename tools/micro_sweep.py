@@ -42,7 +42,7 @@ def main():
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     s = torch.cuda.Stream(device=dev, priority=-1)
-    codes = {"oneshot": N.ALGO_ONESHOT, "twoshot": N.ALGO_TWOSHOT, "ce": N.ALGO_CE}
+    codes = {"oneshot": N.ALGO_ONESHOT, "twoshot": N.ALGO_TWOSHOT, "ce": N.ALGO_CE, "push": N.ALGO_PUSH}
 
     def tmax(v):
         t = torch.tensor([v], dtype=torch.float64, device=dev)
