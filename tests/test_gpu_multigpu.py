@@ -611,7 +611,7 @@ def _w_fault(rank, world, port):
     from paper_2203_13085_b200 import _native as N
 
     _init(rank, world, port)
-    for algo, phase in ((N.ALGO_TWOSHOT, 1), (N.ALGO_ONESHOT, 0)):
+    for algo, phase in ((N.ALGO_TWOSHOT, 1), (N.ALGO_ONESHOT, 0), (N.ALGO_PUSH, 1), (N.ALGO_PUSH, 2)):
         comm = L.P2PCommunicator(4096, nblocks=8, timeout_s=1.0, fault_seq=2 if rank == 1 else -1, fault_phase=phase)
         tr = L.CudaP2PTransport(comm, algo=algo)
         h1 = tr.submit(0, rank, comm.snapshots[0])
