@@ -495,18 +495,27 @@ static int read_peer_epochs(lasgd_comm* c, int rows, uint32_t* out) {
   // per-communicator pinned buffer and stream, created on c->device (the caller holds a
   // DeviceGuard) and freed by lasgd_comm_destroy
   const size_t entry_words = (size_t)kMaxB * kMaxR;
+  // rank-level rows carrying launch epochs: 0 mid, 1 end, 2 gate, 3-4 copy-engine signals
+  // (the push and CE means have no per-CTA entry flags; row 5, the device barrier, counts
+  // barriers, not launches)
+  constexpr int kRankRows = 5;
   if (!c->epoch_host)
-    LASGD_CUDA_TRY(cudaHostAlloc((void**)&c->epoch_host, (entry_words + kMaxR) * sizeof(uint32_t), cudaHostAllocDefault));
+    LASGD_CUDA_TRY(cudaHostAlloc((void**)&c->epoch_host, (entry_words + kRankRows * kMaxR) * sizeof(uint32_t),
+                                 cudaHostAllocDefault));
   if (!c->epoch_stream) LASGD_CUDA_TRY(cudaStreamCreateWithFlags(&c->epoch_stream, cudaStreamNonBlocking));
   uint32_t* host = c->epoch_host;
   cudaStream_t s = c->epoch_stream;
-  const size_t gate_word = (size_t)2 * kMaxB * kMaxR + (size_t)2 * kMaxR;  // k_gate's rank-level slots
+  const size_t rank_word = (size_t)2 * kMaxB * kMaxR;  // first rank-level slot row
   LASGD_CUDA_TRY(cudaMemcpyAsync(host, c->base, (size_t)rows * kMaxR * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  LASGD_CUDA_TRY(cudaMemcpyAsync(host + entry_words, c->base + gate_word * sizeof(uint32_t), kMaxR * sizeof(uint32_t),
-                                 cudaMemcpyDeviceToHost, s));
+  LASGD_CUDA_TRY(cudaMemcpyAsync(host + entry_words, c->base + rank_word * sizeof(uint32_t),
+                                 (size_t)kRankRows * kMaxR * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   LASGD_CUDA_TRY(cudaStreamSynchronize(s));
   for (int q = 0; q < kMaxR; ++q) {
     uint32_t best = host[entry_words + q];
+    for (int k = 1; k < kRankRows; ++k) {
+      const uint32_t v = host[entry_words + (size_t)k * kMaxR + q];
+      if ((int32_t)(v - best) > 0) best = v;
+    }
     for (int b = 0; b < rows; ++b) {
       const uint32_t v = host[(size_t)b * kMaxR + q];
       if ((int32_t)(v - best) > 0) best = v;
@@ -543,7 +552,7 @@ extern "C" int lasgd_comm_peers_ahead(lasgd_comm* c, unsigned long long seq) {
   if (c->world <= 1) return 0;
   DeviceGuard g(c->device);
   // CTA 0 of every K2/K3 launch writes its entry flag first, so the CTA-0 row (plus
-  // the gate row) holds each peer's latest launch: 64 bytes instead of the whole pad
+  // the rank-level rows: gate, end, CE signals) holds each peer's latest launch
   uint32_t ep[kMaxR];
   int rc = read_peer_epochs(c, 1, ep);
   if (rc) return rc;

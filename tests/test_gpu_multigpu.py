@@ -639,32 +639,38 @@ def _w_adaptive_laggard(rank, world, port):
 
     import paper_2203_13085_b200 as L
 
+    from paper_2203_13085_b200 import _native as N
+
     _init(rank, world, port)
     n = 100_003
     comm = L.P2PCommunicator(n, nblocks=16, timeout_s=30.0)
-    x = torch.randn(n, device="cuda")
-    g = torch.randn(n, device="cuda") * 1e-3
-    w = L.LASGDWorker(x, g, comm=comm, sync_period=4, lr=0.01, mode="pull", adaptive=True, tau_max=4)
-    for _ in range(40):
-        if rank == world - 1:
-            torch.cuda._sleep(3_000_000)  # ~1.5 ms per step on the laggard
-        w.step()
-    w.drain()
-    torch.cuda.synchronize()
-    hist = dict(w.tau_hist)
-    mean_tau = sum(k * v for k, v in hist.items()) / max(1, sum(hist.values()))
-    allm = [None] * world
-    dist.all_gather_object(allm, mean_tau)
-    assert np.isfinite(x.cpu().numpy()).all()
-    if rank == 0:
-        # fast ranks run ahead (several local steps per round); the laggard closes as soon
-        # as it sees its peers ahead, which its host learns at most max_host_lead (2)
-        # steps late, so its rounds last at most ~1 + 2 steps
-        fast, lag = allm[:-1], allm[world - 1]
-        assert all(m > lag for m in fast) and sum(fast) / len(fast) >= lag + 0.5, allm
-        assert lag <= 3.0, allm
-    dist.barrier()
-    w.close()
+    # every side-stream transport: the laggard must see its peers' progress through the
+    # flags each one writes (per-CTA entry flags, or the rank-level rows of the push and
+    # copy-engine means)
+    for algo in (N.ALGO_AUTO, N.ALGO_PUSH, N.ALGO_CE):
+        x = torch.randn(n, device="cuda")
+        g = torch.randn(n, device="cuda") * 1e-3
+        w = L.LASGDWorker(x, g, comm=comm, sync_period=4, lr=0.01, mode="pull", adaptive=True, tau_max=4, algo=algo)
+        for _ in range(40):
+            if rank == world - 1:
+                torch.cuda._sleep(3_000_000)  # ~1.5 ms per step on the laggard
+            w.step()
+        w.drain()
+        torch.cuda.synchronize()
+        hist = dict(w.tau_hist)
+        mean_tau = sum(k * v for k, v in hist.items()) / max(1, sum(hist.values()))
+        allm = [None] * world
+        dist.all_gather_object(allm, mean_tau)
+        assert np.isfinite(x.cpu().numpy()).all()
+        if rank == 0:
+            # fast ranks run ahead (several local steps per round); the laggard closes as soon
+            # as it sees its peers ahead, which its host learns at most max_host_lead (2)
+            # steps late, so its rounds last at most ~1 + 2 steps
+            fast, lag = allm[:-1], allm[world - 1]
+            assert all(m > lag for m in fast) and sum(fast) / len(fast) >= lag + 0.5, (algo, allm)
+            assert lag <= 3.0, (algo, allm)
+        dist.barrier()
+        w.close()
     comm.close()
     dist.destroy_process_group()
 
