@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(256, 2) k_push_mean(CommArgs a) {
       for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
     }
   }
+  trace_mark(a, b, 2);  // this CTA's means issued
   if (ok) ok = rank_barrier<P>(a, b, rank);
   trace_mark(a, b, 3);
   publish_done(a);
