@@ -14,6 +14,7 @@ constexpr int kMaxB = LASGD_MAX_BLOCKS;  // flag slots per phase and rank
 constexpr int kPhases = 3;  // 0 entry (per CTA), 1 mid (per CTA), 2 rank-level mid
 constexpr size_t kPadBytes = (size_t)kPhases * kMaxB * kMaxR * sizeof(uint32_t);
 constexpr int kDoneSlots = 64;
+constexpr int kTileQ = 4;  // work-queue counters per launch slot (the push mean uses four)
 constexpr int kEvents = 64;
 
 // host-mapped status block layout (uint32 words)
@@ -47,6 +48,7 @@ struct CommArgs {
   unsigned long long* tile_ctr;  // two work queues of this launch (nullptr: static slices)
   unsigned int* mid_ctr;         // CTAs of this rank past the reduce-scatter (rank-level barrier)
   unsigned int* end_ctr;         // CTAs of this rank done pushing (push round, rank-level end signal)
+  unsigned int* aux_ctr;         // push mean: CTAs done scattering the second half (row-6 signal)
   // push round (K8): per-rank staging regions and round bookkeeping
   char* stage[kMaxR];            // owner o's staging: [parity][source rank][stage_elems]
   size_t stage_elems;
@@ -90,7 +92,7 @@ __device__ __forceinline__ uint32_t cprev_end(const CommArgs& a) {
   return a.adv.rd ? (a.dyn_chain ? (uint32_t)(s_dyn.seq - 1ull) : 0u) : a.prev_end;
 }
 __device__ __forceinline__ unsigned long long* ctile(const CommArgs& a) {
-  return (a.adv.rd && a.tile_ctr) ? a.tile_ctr + 2 * (s_dyn.seq % kDoneSlots) : a.tile_ctr;
+  return (a.adv.rd && a.tile_ctr) ? a.tile_ctr + kTileQ * (s_dyn.seq % kDoneSlots) : a.tile_ctr;
 }
 __device__ __forceinline__ unsigned* cmid(const CommArgs& a) {
   return (a.adv.rd && a.mid_ctr) ? a.mid_ctr + (s_dyn.seq % kDoneSlots) : a.mid_ctr;
@@ -259,7 +261,8 @@ __device__ inline void publish_done(const CommArgs& a) {
     if (prev == (unsigned)a.nblocks - 1u) {
       a.done_ctr[slot] = 0u;
       unsigned long long* tq = ctile(a);
-      if (tq) tq[0] = tq[1] = 0ull;  // every CTA has left its tile loops
+      if (tq)
+        for (int k = 0; k < kTileQ; ++k) tq[k] = 0ull;  // every CTA has left its tile loops
       if (a.adv.rd) dyn_apply(a.adv.rd, a.adv);
       // done_seq tells the host "launch complete" — it never carries data to the host:
       // everything the launch wrote is read by later device work (stream order, events,

@@ -40,11 +40,15 @@ int launch_push(int P, const CommArgs& a, const FusedRound<T>& f, dim3 grid, int
 #undef LASGD_PCASE
 }
 
+// packs in flight per thread, sized so the P loaded packs fit 128 registers without spills
+template <typename T, int P>
+constexpr int push_mean_unroll() { return sizeof(T) == 4 ? (P <= 3 ? 4 : (P <= 6 ? 2 : 1)) : (P <= 3 ? 2 : 1); }
+
 template <typename T>
 int launch_push_mean(int P, const CommArgs& a, dim3 grid, int threads, cudaStream_t s) {
 #define LASGD_MCASE(PP)                                                       \
   case PP: {                                                                  \
-    auto kern = k_push_mean<T, PP, (PP <= 4 && sizeof(T) == 4 ? 4 : 2)>;      \
+    auto kern = k_push_mean<T, PP, push_mean_unroll<T, PP>()>;                \
     CommArgs aa = a;                                                          \
     const int cap = coop_capacity(kern, threads);                             \
     if ((int)grid.x > cap) grid.x = cap;                                      \

@@ -226,15 +226,19 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
 }
 
 // ------------------------------------------------------------------ push mean (ALGO_PUSH all-reduce)
-// K3's result with every byte moved by remote STORES, one cooperative launch:
-//   scatter: chunk c of my snapshot -> owner c's staging [cur][me] (posted NVLink writes),
-//     rank-level end signal (kind 1, this launch's epoch); wait for every rank's;
-//   reduce: my chunk in ring order from my snapshot + the staged contributions, / P,
-//     stored into my xbar and every peer's;
+// K3's result with every byte moved by remote STORES, one cooperative launch, the chunks
+// split into two halves so the second half's scatter covers the first half's drain and
+// signal latency:
+//   scatter half 0: chunk c of my snapshot -> owner c's staging [cur][me] (posted NVLink
+//     writes), rank-level signal row 1; scatter half 1 (+ the unaligned head/tail
+//     elements), signal row 6;
+//   reduce half 0 once every rank's row-1 signal is in: my chunk in ring order from my
+//     snapshot + the staged contributions, / P, stored into my xbar and every peer's;
+//     reduce half 1 (+ head/tail) once row 6 is in;
 //   rank-level mid barrier: every rank's means have landed everywhere.
-// Per rank: NVLink out 2(P-1)/P B as stores (as the push round), all loads local.  The
-// staging slots and end signals are the push round's: lasgd_comm_allreduce marks the
-// staging as not holding round contributions afterwards.
+// Per rank: NVLink out 2(P-1)/P B as stores (as the push round), all loads local.  Four
+// work queues (kTileQ).  The staging slots are the push round's: lasgd_comm_allreduce marks
+// them as not holding round contributions afterwards.
 template <typename T, int P, int U>
 __global__ void __launch_bounds__(256, 2) k_push_mean(CommArgs a) {
   constexpr int W = Pack<T>::W;
@@ -243,12 +247,38 @@ __global__ void __launch_bounds__(256, 2) k_push_mean(CommArgs a) {
   const size_t n = a.n;
   const int cur = a.cur;
   const T* const snap_own = reinterpret_cast<const T*>(a.snap[rank]);
-  unsigned long long* const q0 = a.tile_ctr;
-  unsigned long long* const q1 = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
+  unsigned long long* const qt = a.tile_ctr;  // [0], [1]: scatter halves; [2], [3]: reduce halves
+  auto q = [&](int k) -> unsigned long long* { return qt ? qt + k : nullptr; };
+  const size_t tile = (size_t)kTileIters * U * blockDim.x;
   auto soff = [&](int c, size_t j) { return j - chunk_bound(n, P, c) / W * W; };
-  trace_mark(a, b, 0);
-  chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
-    [&](int c, size_t p0, size_t p1) {
+  // aligned packs of half h of chunk c
+  // split (phases bit 8, large buffers): two halves; otherwise half 0 is the whole chunk
+  // and there is no second signal (small buffers: one signal less beats the overlap)
+  const bool split = (a.phases & 8) != 0;
+  auto half = [&](int c, int h, size_t& lo, size_t& hi) {
+    size_t cs, ce, cp0, cp1;
+    chunk_packs<T, P>(n, c, cs, ce, cp0, cp1);
+    const size_t mid = split ? cp0 + (cp1 - cp0) / 2 : cp1;
+    lo = h ? mid : cp0;
+    hi = h ? cp1 : mid;
+  };
+  auto scatter = [&](int h) {
+    size_t tmax = 0;
+#pragma unroll
+    for (int c = 0; c < P; ++c) {
+      size_t lo, hi;
+      half(c, h, lo, hi);
+      const size_t tc = (hi - lo + tile - 1) / tile;
+      tmax = tc > tmax ? tc : tmax;
+    }
+    queue_loop(q(h), b, a.nblocks, (unsigned long long)tmax * P, [&](unsigned long long t) {
+      const int c = (rank + 1 + (int)(t % P)) % P;  // every rank starts at a different owner
+      if (c == rank) return;
+      size_t lo, hi;
+      half(c, h, lo, hi);
+      const size_t p0 = lo + (size_t)(t / P) * tile;
+      if (p0 >= hi) return;
+      const size_t p1 = p0 + tile < hi ? p0 + tile : hi;
       T* dst = stage_ptr<T>(a, c, cur, rank, P);
       for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
         Pack<T> v[U];
@@ -263,21 +293,20 @@ __global__ void __launch_bounds__(256, 2) k_push_mean(CommArgs a) {
           if (pu < p1) st_plain(dst + soff(c, pu * W), v[u]);
         }
       }
-    },
-    [&](int c, size_t j) { stage_ptr<T>(a, c, cur, rank, P)[soff(c, j)] = snap_own[j]; });
-  rank_signal<P>(a, 1, a.end_ctr, rank);
-  bool ok = rank_wait<P>(a, 1, a.epoch, b, rank);
-  trace_mark(a, b, 1);
-  if (ok) {
-    size_t cs, ce, cp0, cp1;
-    chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
-    const size_t base = cs / W * W;
-    const T* const stage0 = stage_ptr<T>(a, rank, cur, 0, P);
-    const size_t selems = a.stage_elems;
-    auto src = [&](int q, size_t j) -> const T* {
-      return q == rank ? snap_own + j : stage0 + (size_t)q * selems + (j - base);
-    };
-    tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
+    });
+  };
+  size_t cs, ce, cp0, cp1;
+  chunk_packs<T, P>(n, rank, cs, ce, cp0, cp1);
+  const size_t base = cs / W * W;
+  const T* const stage0 = stage_ptr<T>(a, rank, cur, 0, P);
+  const size_t selems = a.stage_elems;
+  auto src = [&](int qq, size_t j) -> const T* {
+    return qq == rank ? snap_own + j : stage0 + (size_t)qq * selems + (j - base);
+  };
+  auto reduce = [&](int h) {
+    size_t lo, hi;
+    half(rank, h, lo, hi);
+    tile_loop(q(2 + h), b, a.nblocks, lo, hi - lo, tile, [&](size_t p0, size_t p1) {
       for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
         Pack<T> v[U][P];
 #pragma unroll
@@ -285,7 +314,7 @@ __global__ void __launch_bounds__(256, 2) k_push_mean(CommArgs a) {
           const size_t pu = p + (size_t)u * blockDim.x;
           if (pu < p1) {
 #pragma unroll
-            for (int q = 0; q < P; ++q) v[u][q] = ld_stream(src(q, pu * W));
+            for (int qq = 0; qq < P; ++qq) v[u][qq] = ld_stream(src(qq, pu * W));
           }
         }
 #pragma unroll
@@ -298,25 +327,53 @@ __global__ void __launch_bounds__(256, 2) k_push_mean(CommArgs a) {
             for (int k = 0; k < W; ++k) {
               T lane[P];
 #pragma unroll
-              for (int q = 0; q < P; ++q) lane[q] = v[u][q].v[k];
+              for (int qq = 0; qq < P; ++qq) lane[qq] = v[u][qq].v[k];
               z.v[k] = mean_div<T, P>(rot_sum<T, P>(lane, rank));
             }
 #pragma unroll
-            for (int q = 0; q < P; ++q) st_plain(reinterpret_cast<T*>(a.xbar[q]) + j, z);
+            for (int qq = 0; qq < P; ++qq) st_plain(reinterpret_cast<T*>(a.xbar[qq]) + j, z);
           }
         }
       }
     });
+  };
+  trace_mark(a, b, 0);
+  scatter(0);
+  if (split) rank_signal<P>(a, 1, a.end_ctr, rank);
+  scatter(1);
+  if (b == 0) {  // unaligned head / tail elements of every other chunk
+    for (int c = 0; c < P; ++c) {
+      if (c == rank) continue;
+      size_t ccs, cce, ccp0, ccp1;
+      chunk_packs<T, P>(n, c, ccs, cce, ccp0, ccp1);
+      const size_t he = ccp0 * W < cce ? ccp0 * W : cce;
+      const size_t ts = ccp1 * W > he ? ccp1 * W : he;
+      T* dst = stage_ptr<T>(a, c, cur, rank, P);
+      for (size_t j = ccs + threadIdx.x; j < he; j += blockDim.x) dst[soff(c, j)] = snap_own[j];
+      for (size_t j = ts + threadIdx.x; j < cce; j += blockDim.x) dst[soff(c, j)] = snap_own[j];
+    }
+  }
+  if (split) {
+    rank_signal<P>(a, 6, a.aux_ctr, rank);
+  } else {
+    rank_signal<P>(a, 1, a.end_ctr, rank);
+  }
+  bool ok = rank_wait<P>(a, 1, a.epoch, b, rank);
+  trace_mark(a, b, 1);
+  if (ok) reduce(0);
+  if (ok && split) ok = rank_wait<P>(a, 6, a.epoch, b, rank);
+  if (ok) {
+    reduce(1);
     if (b == 0) {  // unaligned head / tail elements of the own chunk
       const size_t he = cp0 * W < ce ? cp0 * W : ce;
       const size_t ts = cp1 * W > he ? cp1 * W : he;
       auto scalar = [&](size_t j) {
         T lane[P];
 #pragma unroll
-        for (int q = 0; q < P; ++q) lane[q] = *src(q, j);
+        for (int qq = 0; qq < P; ++qq) lane[qq] = *src(qq, j);
         const T zb = mean_div<T, P>(rot_sum<T, P>(lane, rank));
 #pragma unroll
-        for (int q = 0; q < P; ++q) reinterpret_cast<T*>(a.xbar[q])[j] = zb;
+        for (int qq = 0; qq < P; ++qq) reinterpret_cast<T*>(a.xbar[qq])[j] = zb;
       };
       for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
       for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);

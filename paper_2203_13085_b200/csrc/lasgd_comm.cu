@@ -305,6 +305,7 @@ struct lasgd_comm {
   unsigned long long last_push = 0;  // launch whose end signals certify them
   unsigned long long end_seq = 0;    // last launch that raised end signals (K7 one-shot, K8)
   unsigned int* end_ctr = nullptr;   // [kDoneSlots] rank-level end-signal counters
+  unsigned int* aux_ctr = nullptr;   // [kDoneSlots] push mean: second-half scatter counters
   char* peer_base[kMaxR] = {nullptr};
   bool opened = false;
   bool poisoned = false;
@@ -313,7 +314,7 @@ struct lasgd_comm {
   unsigned long long* done_host = nullptr;
   unsigned long long* done_dev = nullptr;
   unsigned int* done_ctr = nullptr;
-  unsigned long long* tile_ctr = nullptr;  // [kDoneSlots][2] work queues
+  unsigned long long* tile_ctr = nullptr;  // [kDoneSlots][kTileQ] work queues
   unsigned int* mid_ctr = nullptr;         // [kDoneSlots] rank-level barrier counters
   unsigned long long* trace_buf = nullptr;  // [kMaxB][4] globaltimer stamps of the last traced launch
   bool trace_on = false;
@@ -387,8 +388,10 @@ extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int 
     e = cudaHostGetDevicePointer((void**)&c->status_dev, c->status_host, 0);
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->done_ctr, kDoneSlots * sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMalloc(&c->tile_ctr, 2 * kDoneSlots * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(c->tile_ctr, 0, 2 * kDoneSlots * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->tile_ctr, kTileQ * kDoneSlots * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->tile_ctr, 0, kTileQ * kDoneSlots * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->aux_ctr, kDoneSlots * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->aux_ctr, 0, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMalloc(&c->mid_ctr, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->mid_ctr, 0, kDoneSlots * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMalloc(&c->end_ctr, kDoneSlots * sizeof(unsigned int));
@@ -449,17 +452,21 @@ extern "C" int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr) {
   return LASGD_OK;
 }
 
-// The all-reduce's AUTO at P = 3-4 (measured; profiles/r02/pm_sweep_p{3,4}.jsonl): where
-// resolve_algo picks the two-shot, the push mean (every byte moved by stores) is faster
-// at every size (P=4: 16 MB 0.065 vs 0.079 ms, 102 MB 0.279 vs 0.305; P=3 102 MB 0.248 vs
-// 0.278), and from 192 MB the copy-engine mean is faster still (P=4: 256 MB 0.644 vs
-// 0.665, 1 GB 2.408 vs 2.631).  Otherwise (P = 2: one-shot; P >= 5, unmeasured on
-// hardware) resolve_algo.  Not for SGD-AR buckets or fused rounds: they have their own.
+// The all-reduce's AUTO at P = 3-4 (measured; profiles/r02/pm{2,3}_sweep_p{3,4}.jsonl):
+// where resolve_algo picks the two-shot (and at P=4 from 4 MB), the push mean (every byte
+// moved by stores) is faster at every size (P=4: 16 MB 0.065 vs 0.079 ms, 102 MB 0.276
+// vs 0.301, 256 MB 0.617 vs 0.708; P=3 102 MB 0.248 vs 0.276), and at 1 GB the
+// copy-engine mean is faster still (P=4 2.328 vs 2.372, P=3 2.130 vs 2.247).  Otherwise
+// (P = 2: one-shot; P >= 5, unmeasured on hardware) resolve_algo.  Not for SGD-AR buckets
+// or fused rounds: they have their own.
 static int resolve_allreduce_algo(const lasgd_comm* c, int algo) {
   const size_t bytes = c->n * c->elem;
   const int a = resolve_algo(algo, c->world, bytes);
-  if (algo != LASGD_ALGO_AUTO || c->nvls_uc || c->world < 3 || c->world > 4 || a != LASGD_ALGO_TWOSHOT) return a;
-  return bytes >= ((size_t)192 << 20) ? LASGD_ALGO_CE : LASGD_ALGO_PUSH;
+  if (algo != LASGD_ALGO_AUTO || c->nvls_uc || c->world < 3 || c->world > 4) return a;
+  if (bytes >= ((size_t)512 << 20)) return LASGD_ALGO_CE;
+  if (a == LASGD_ALGO_TWOSHOT) return LASGD_ALGO_PUSH;
+  if (c->world == 4 && bytes >= ((size_t)3 << 20)) return LASGD_ALGO_PUSH;  // 4 MB: 0.0347 vs 0.0372 one-shot
+  return a;
 }
 
 int lasgd::comm_side_algo(lasgd_comm* c, int algo) {
@@ -724,9 +731,10 @@ static int prepare_launch(lasgd_comm* c, int snap_slot, CommArgs& a, unsigned lo
   }
   a.status = c->status_dev;
   a.done_ctr = c->done_ctr;
-  a.tile_ctr = c->tile_ctr + 2 * (s % kDoneSlots);
+  a.tile_ctr = c->tile_ctr + kTileQ * (s % kDoneSlots);
   a.mid_ctr = c->mid_ctr + (s % kDoneSlots);
   a.end_ctr = c->end_ctr + (s % kDoneSlots);
+  a.aux_ctr = c->aux_ctr + (s % kDoneSlots);
   for (int r = 0; r < c->world; ++r) a.stage[r] = c->peer_base[r] + c->off_stage;
   a.stage_elems = c->stage_elems;
   a.cur = snap_slot;
@@ -799,6 +807,9 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
     c->push_slot = -1;  // the staging now holds this mean's contributions, not a round's
     c->end_seq = 0;
     if (c->gate && (rc = launch_gate(c->world, a, cs))) return rc;
+    // halves pipelined from 32 MB (P=4: 64 MB 0.1725 vs 0.1849 ms, 256 MB 0.617 vs 0.667;
+    // at 4-16 MB the second signal costs more than it hides; profiles/r02/pm3_sweep_p*.jsonl)
+    if (c->n * c->elem >= ((size_t)32 << 20)) a.phases |= 8;
     rc = c->dtype == LASGD_F64 ? launch_push_mean<double>(c->world, a, dim3(c->nblocks), c->threads, cs)
                                : launch_push_mean<float>(c->world, a, dim3(c->nblocks), c->threads, cs);
     if (rc) return rc;
@@ -1106,8 +1117,9 @@ extern "C" int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len) {
   const uint32_t* st = c->status_host;
   const unsigned long long fs = (unsigned long long)st[ST_SEQ_LO] | ((unsigned long long)st[ST_SEQ_HI] << 32);
   static const char* const kPhaseName[] = {"entry", "mid", "end-of-round", "launch gate",
-                                           "copy-engine contributions", "copy-engine means", "device"};
-  const char* phase = st[ST_PHASE] < 7 ? kPhaseName[st[ST_PHASE]] : "unknown";
+                                           "copy-engine contributions", "copy-engine means", "device",
+                                           "push-mean second half"};
+  const char* phase = st[ST_PHASE] < 8 ? kPhaseName[st[ST_PHASE]] : "unknown";
   switch (st[ST_ERR]) {
     case ERR_NONE: snprintf(buf, len, "ok"); break;
     case ERR_TIMEOUT:
@@ -1141,6 +1153,7 @@ extern "C" int lasgd_comm_destroy(lasgd_comm* c) {
   if (c->tile_ctr) cudaFree(c->tile_ctr);
   if (c->mid_ctr) cudaFree(c->mid_ctr);
   if (c->end_ctr) cudaFree(c->end_ctr);
+  if (c->aux_ctr) cudaFree(c->aux_ctr);
   if (c->trace_buf) cudaFree(c->trace_buf);
   if (c->status_host) cudaFreeHost(c->status_host);
   if (c->nvls) nvls_destroy(c->nvls);

@@ -799,6 +799,21 @@ def _w_ce(rank, world, port):
             assert comm.launches() == before
             dist.barrier()
             comm.close()
+    # large buffers: the push mean's pipelined halves (>= 32 MB), beside the CE mean
+    for dtype, n in ((torch.float32, 9_000_001), (torch.float64, 4_500_007)):
+        npdt = np.float32 if dtype == torch.float32 else np.float64
+        comm = L.P2PCommunicator(n, dtype=dtype, timeout_s=30.0)
+        for rnd, algo in enumerate((N.ALGO_PUSH, N.ALGO_CE, N.ALGO_PUSH, N.ALGO_AUTO)):
+            slot = rnd % 2
+            vecs = [_vec(7000 * rnd + 10 * r + n, n, npdt) for r in range(world)]
+            comm.snapshots[slot].copy_(torch.from_numpy(vecs[rank]))
+            torch.cuda.synchronize()
+            seq = comm.allreduce(slot, algo)
+            assert comm.wait(seq, 30.0) == 1
+            torch.cuda.synchronize()
+            assert _same_bits(comm.xbar.cpu().numpy(), O.ring_mean(vecs)), (n, rnd, algo, rank)
+        dist.barrier()
+        comm.close()
     # the overlap pipeline on the CE mean, mixed with fused push rounds on one communicator
     n, steps = 100_003, 8
     x0 = _vec(11, n)
