@@ -97,6 +97,9 @@ __device__ __forceinline__ unsigned long long* ctile(const CommArgs& a) {
 __device__ __forceinline__ unsigned* cmid(const CommArgs& a) {
   return (a.adv.rd && a.mid_ctr) ? a.mid_ctr + (s_dyn.seq % kDoneSlots) : a.mid_ctr;
 }
+__device__ __forceinline__ unsigned* caux(const CommArgs& a) {
+  return (a.adv.rd && a.aux_ctr) ? a.aux_ctr + (s_dyn.seq % kDoneSlots) : a.aux_ctr;
+}
 __device__ __forceinline__ unsigned* cend(const CommArgs& a) {
   return (a.adv.rd && a.end_ctr) ? a.end_ctr + (s_dyn.seq % kDoneSlots) : a.end_ctr;
 }

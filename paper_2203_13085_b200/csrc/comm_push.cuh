@@ -44,6 +44,12 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
   unsigned bad = 0;
   unsigned long long* q0 = ctile(a);
   unsigned long long* q1 = ctile(a) ? ctile(a) + 1 : nullptr;
+  // split (phases bit 8, large buffers, P2P only): phase A signals its first half's means
+  // before doing the second, so phase B's first half overlaps the second half's drain
+  const bool split = !VIRTUAL && (a.phases & 8) != 0;
+  unsigned long long* const qA1 = ctile(a) ? ctile(a) + 2 : nullptr;
+  unsigned long long* const qB1 = ctile(a) ? ctile(a) + 3 : nullptr;
+  const size_t tile = (size_t)kTileIters * U * blockDim.x;
   const T* const snap_own = reinterpret_cast<const T*>(csnap(a, rank));
   trace_mark(a, b, 0);
   // offset of element j of chunk c inside a staging slot (keeps 16-byte alignment)
@@ -101,7 +107,7 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
       auto src = [&](int q, size_t j) -> const T* {
         return q == rank ? snap_own + j : stage0 + (size_t)q * selems + (j - base);
       };
-      tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, (size_t)kTileIters * U * blockDim.x, [&](size_t p0, size_t p1) {
+      auto bodyA = [&](size_t p0, size_t p1) {
         for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
           Pack<T> v[U][P], vx[U], vg[U], vm[U], vd[U];
 #pragma unroll
@@ -144,7 +150,15 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
             }
           }
         }
-      });
+      };
+      if (split) {  // half 0's means pushed and signalled before half 1 starts
+        const size_t mid = cp0 + (cp1 - cp0) / 2;
+        tile_loop(q0, b, a.nblocks, cp0, mid - cp0, tile, bodyA);
+        rank_signal<P>(a, 0, cmid(a), rank);
+        tile_loop(qA1, b, a.nblocks, mid, cp1 - mid, tile, bodyA);
+      } else {
+        tile_loop(q0, b, a.nblocks, cp0, cp1 - cp0, tile, bodyA);
+      }
       if (b == 0) {  // unaligned head / tail elements of the own chunk
         const size_t he = cp0 * W < ce ? cp0 * W : ce;
         const size_t ts = cp1 * W > he ? cp1 * W : he;
@@ -166,14 +180,19 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
         for (size_t j = cs + threadIdx.x; j < he; j += blockDim.x) scalar(j);
         for (size_t j = ts + threadIdx.x; j < ce; j += blockDim.x) scalar(j);
       }
+      if (split) rank_signal<P>(a, 6, caux(a), rank);  // half 1's means pushed
     }
   }
   if (a.phases & 2) {
-    if (!VIRTUAL && ok) ok = rank_barrier<P>(a, b, rank);
+    if (split) {
+      if (ok) ok = rank_wait<P>(a, 0, cepoch(a), b, rank);  // every owner's half-0 means landed
+    } else if (!VIRTUAL && ok) {
+      ok = rank_barrier<P>(a, b, rank);
+    }
     trace_mark(a, b, 2);
     if (ok) {
       const T* zl = reinterpret_cast<const T*>(a.xbar[rank]);  // means pushed by their owners
-      chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, (size_t)kTileIters * U * blockDim.x,
+      auto bodyB =
         [&](int c, size_t p0, size_t p1) {
           T* dst = stage_ptr<T>(a, c, nxt, rank, P);
           for (size_t p = p0 + threadIdx.x; p < p1; p += (size_t)U * blockDim.x) {
@@ -207,8 +226,8 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
               }
             }
           }
-        },
-        [&](int c, size_t j) {
+        };
+      auto scalarB = [&](int c, size_t j) {
           T xv = x[j], mv = load_m ? m[j] : T(0), dv = load_d ? dl[j] : T(0);
           element(xv, g[j], mv, dv, f.mode == 0 ? snap_own[j] : T(0), zl[j]);
           x[j] = xv;
@@ -216,8 +235,55 @@ __global__ void __launch_bounds__(256, 2) k_push_round(CommArgs a, FusedRound<T>
           if (store_d) dl[j] = dv;
           sn[j] = xv;
           stage_ptr<T>(a, c, nxt, rank, P)[soff(c, j)] = xv;
-        });
-      if (!VIRTUAL) rank_signal<P>(a, 1, cend(a), rank);
+        };
+      if (split) {
+        // half h of every other chunk, tiles interleaved across owners like chunk_tiles
+        auto half_tiles = [&](unsigned long long* qq, int h) {
+          auto hr = [&](int c, size_t& lo, size_t& hi) {
+            size_t ccs, cce, ccp0, ccp1;
+            chunk_packs<T, P>(n, c, ccs, cce, ccp0, ccp1);
+            const size_t mid = ccp0 + (ccp1 - ccp0) / 2;
+            lo = h ? mid : ccp0;
+            hi = h ? ccp1 : mid;
+          };
+          size_t tmax = 0;
+#pragma unroll
+          for (int c = 0; c < P; ++c) {
+            size_t lo, hi;
+            hr(c, lo, hi);
+            const size_t tc = (hi - lo + tile - 1) / tile;
+            tmax = tc > tmax ? tc : tmax;
+          }
+          queue_loop(qq, b, a.nblocks, (unsigned long long)tmax * P, [&](unsigned long long t) {
+            const int c = (rank + 1 + (int)(t % P)) % P;
+            if (c == rank) return;
+            size_t lo, hi;
+            hr(c, lo, hi);
+            const size_t p0 = lo + (size_t)(t / P) * tile;
+            if (p0 >= hi) return;
+            bodyB(c, p0, p0 + tile < hi ? p0 + tile : hi);
+          });
+        };
+        half_tiles(q1, 0);
+        ok = rank_wait<P>(a, 6, cepoch(a), b, rank);  // every owner's half-1 means landed
+        if (ok) {
+          half_tiles(qB1, 1);
+          if (b == 0) {  // unaligned head / tail elements of every other chunk
+            for (int c = 0; c < P; ++c) {
+              if (c == rank) continue;
+              size_t ccs, cce, ccp0, ccp1;
+              chunk_packs<T, P>(n, c, ccs, cce, ccp0, ccp1);
+              const size_t he = ccp0 * W < cce ? ccp0 * W : cce;
+              const size_t ts = ccp1 * W > he ? ccp1 * W : he;
+              for (size_t j = ccs + threadIdx.x; j < he; j += blockDim.x) scalarB(c, j);
+              for (size_t j = ts + threadIdx.x; j < cce; j += blockDim.x) scalarB(c, j);
+            }
+          }
+        }
+      } else {
+        chunk_tiles<T, P>(q1, b, a.nblocks, n, rank, true, tile, bodyB, scalarB);
+      }
+      if (ok && !VIRTUAL) rank_signal<P>(a, 1, cend(a), rank);
     }
   }
   report_nonfinite(a.nonfinite, bad);

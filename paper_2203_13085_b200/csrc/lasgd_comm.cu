@@ -335,6 +335,12 @@ struct lasgd_comm {
 
 static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// phases bit 8 for the staged push round (P >= 3): phase A signals its first half before
+// the second, so phase B starts on the first half while the second half's means drain
+static int push_split(const lasgd_comm* c) {
+  return (c->world >= 3 && c->n * c->elem >= ((size_t)32 << 20)) ? 8 : 0;
+}
+
 extern "C" int lasgd_comm_create(int rank, int world, int device, size_t n, int dtype, const lasgd_comm_config* cfg,
                                  lasgd_comm** out) {
   if (!out) return fail(LASGD_ERR_INVALID_ARGUMENT, "null out");
@@ -887,7 +893,7 @@ extern "C" int lasgd_comm_fused_round(lasgd_comm* c, int snap_slot, int algo, vo
     if (rc) return rc;
     a.nblocks = nblocks;
     a.nonfinite = nonfinite;
-    a.phases = 3;
+    a.phases = 3 | push_split(c);
     a.prev_push = (uint32_t)c->last_push;
     rc = c->dtype == LASGD_F32 ? launch_push<float, false>(c->world, a, fl, dim3(nblocks, 1), c->threads, cs)
                                : launch_push<double, false>(c->world, a, fd, dim3(nblocks, 1), c->threads, cs);
@@ -982,10 +988,11 @@ int comm_fused_round_dyn(lasgd_comm* c, int snap_slot, int algo, void* x, const 
   a.tile_ctr = c->tile_ctr;  // slot-0 entries: the kernel indexes them by its dynamic sequence number
   a.mid_ctr = c->mid_ctr;
   a.end_ctr = c->end_ctr;
+  a.aux_ctr = c->aux_ctr;
   a.skip_signal_phase = -1;
   a.nblocks = nblocks;
   a.nonfinite = nonfinite;
-  a.phases = 3;
+  a.phases = 3 | (push ? push_split(c) : 0);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (push) {
     rc = c->dtype == LASGD_F32
