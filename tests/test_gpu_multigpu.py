@@ -379,6 +379,36 @@ def _w_graph_replay(rank, world, port):
             ref, _, _, _ = O.run_lasgd_pull(x0, gl, [0.05] * total, world, k, alpha,
                                             sgd=O.SgdConfig(0.05, 0.9, 0.0, 1e-4, True))
             assert _same_bits(a[0], ref[rank]), (algo, k, rank)
+    # >= 32 MB: the staged push round's pipelined halves (P >= 3) in graph form == eager
+    nb = 9_000_001
+    xb0 = _vec(6, nb)
+    gb = [torch.from_numpy(_vec(950 + 10 * i + rank, nb)).cuda() for i in range(2)]
+
+    def run_big(graphed):
+        comm = L.P2PCommunicator(nb, timeout_s=30.0)
+        x = torch.from_numpy(xb0.copy()).cuda()
+        compute = torch.cuda.Stream()
+        with torch.cuda.stream(compute):
+            w = L.LASGDWorker(x, gb[0], comm=comm, sync_period=1, mode="pull", sgd=sgd, lr=0.05,
+                              algo=N.ALGO_PUSH, pipeline="fused", compute_stream=compute)
+            w.step()
+            if graphed:
+                graph = w.capture(gb)
+                for _ in range(3):
+                    graph.replay()
+            else:
+                for t in range(6):
+                    w.g = gb[t % 2]
+                    w.step()
+            w.drain()
+        torch.cuda.synchronize()
+        out = x.cpu().numpy()
+        w.close()
+        dist.barrier()
+        comm.close()
+        return out
+
+    assert _same_bits(run_big(True), run_big(False)), rank
     # the whole training step (zero_grad + forward + backward + fused round over NVLink)
     # captured into one CUDA graph per minibatch: the same bits as eager steps
     def train(graphed):
