@@ -1125,7 +1125,7 @@ extern "C" int lasgd_comm_diagnostic(lasgd_comm* c, char* buf, size_t len) {
   const unsigned long long fs = (unsigned long long)st[ST_SEQ_LO] | ((unsigned long long)st[ST_SEQ_HI] << 32);
   static const char* const kPhaseName[] = {"entry", "mid", "end-of-round", "launch gate",
                                            "copy-engine contributions", "copy-engine means", "device",
-                                           "push-mean second half"};
+                                           "second half (push)"};
   const char* phase = st[ST_PHASE] < 8 ? kPhaseName[st[ST_PHASE]] : "unknown";
   switch (st[ST_ERR]) {
     case ERR_NONE: snprintf(buf, len, "ok"); break;
