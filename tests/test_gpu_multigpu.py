@@ -714,22 +714,27 @@ def _w_fault_end_signal(rank, world, port):
     import paper_2203_13085_b200 as L
 
     _init(rank, world, port)
-    n = 4099
-    comm = L.P2PCommunicator(n, nblocks=8, timeout_s=1.0, fault_seq=3 if rank == 1 else -1, fault_phase=2)
-    x = torch.randn(n, device="cuda")
-    g = torch.randn(n, device="cuda")
-    w = L.LASGDWorker(x, g, comm=comm, sync_period=1, lr=0.01, pipeline="fused", algo=3)
-    with pytest.raises(L.CollectiveFailure):
-        for _ in range(6):  # launch 1 stages the snapshot, 2.. are rounds; rank 1 skips end(3)
+    # small (one-pass round) and >= 32 MB at P >= 3 (pipelined halves: phase 1 drops the
+    # first half's signal, phase 2 the end signal)
+    cases = [(4099, 2), (9_000_001, 2)] + ([(9_000_001, 1)] if world >= 3 else [])  # P=2 mirror: no mid signal
+    for n, phase in cases:
+        comm = L.P2PCommunicator(n, nblocks=8, timeout_s=1.0, fault_seq=3 if rank == 1 else -1, fault_phase=phase)
+        x = torch.randn(n, device="cuda")
+        g = torch.randn(n, device="cuda")
+        w = L.LASGDWorker(x, g, comm=comm, sync_period=1, lr=0.01, pipeline="fused", algo=3)
+        with pytest.raises(L.CollectiveFailure):
+            for _ in range(6):  # launch 1 stages the snapshot, 2.. are rounds; rank 1 skips a signal of 3
+                w.step()
+            torch.cuda.synchronize()  # in-flight rounds time out after 1 s
             w.step()
-        torch.cuda.synchronize()  # in-flight rounds time out after 1 s
-        w.step()
-    torch.cuda.synchronize()
-    diag = comm.diagnostic()
-    assert ("end-of-round" in diag and "timed out" in diag) or "injected" in diag, diag
-    dist.barrier()
-    w.close()
-    comm.close()
+        torch.cuda.synchronize()
+        diag = comm.diagnostic()
+        assert "timed out" in diag or "injected" in diag, (n, phase, diag)
+        if phase == 2:
+            assert "end-of-round" in diag or "injected" in diag, diag
+        dist.barrier()
+        w.close()
+        comm.close()
     dist.destroy_process_group()
 
 
