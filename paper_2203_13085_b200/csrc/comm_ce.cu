@@ -86,7 +86,7 @@ static size_t bound_host(size_t n, int P, int c) {
 }
 
 template <typename T, int P>
-static int ce_mean(const CommArgs& a, const CeRound& r, int nblocks, cudaStream_t s) {
+static int ce_mean(const CommArgs& a, const CeRound& r, cudaStream_t s) {
   const size_t E = sizeof(T), n = a.n;
   const int me = a.rank;
   k_ce_gate<P><<<1, 32, 0, s>>>(a);
@@ -104,7 +104,6 @@ static int ce_mean(const CommArgs& a, const CeRound& r, int nblocks, cudaStream_
   if (len > 0) {
     // a short HBM-bound pass: 2 CTAs per SM whatever the communicator's SM budget
     // (at 1 GB, P=4: 2.408 ms with 296 CTAs vs 2.480 with 128)
-    (void)nblocks;
     size_t blocks = (len + 4 * 256 - 1) / (4 * 256);
     const size_t cap = 2 * (size_t)num_sms();
     if (blocks > cap) blocks = cap;
@@ -124,15 +123,15 @@ static int ce_mean(const CommArgs& a, const CeRound& r, int nblocks, cudaStream_
 }
 
 template <typename T>
-static int ce_mean_t(int P, const CommArgs& a, const CeRound& r, int nblocks, cudaStream_t s) {
+static int ce_mean_t(int P, const CommArgs& a, const CeRound& r, cudaStream_t s) {
   switch (P) {
-    case 2: return ce_mean<T, 2>(a, r, nblocks, s);
-    case 3: return ce_mean<T, 3>(a, r, nblocks, s);
-    case 4: return ce_mean<T, 4>(a, r, nblocks, s);
-    case 5: return ce_mean<T, 5>(a, r, nblocks, s);
-    case 6: return ce_mean<T, 6>(a, r, nblocks, s);
-    case 7: return ce_mean<T, 7>(a, r, nblocks, s);
-    case 8: return ce_mean<T, 8>(a, r, nblocks, s);
+    case 2: return ce_mean<T, 2>(a, r, s);
+    case 3: return ce_mean<T, 3>(a, r, s);
+    case 4: return ce_mean<T, 4>(a, r, s);
+    case 5: return ce_mean<T, 5>(a, r, s);
+    case 6: return ce_mean<T, 6>(a, r, s);
+    case 7: return ce_mean<T, 7>(a, r, s);
+    case 8: return ce_mean<T, 8>(a, r, s);
     default: return fail(LASGD_ERR_UNSUPPORTED, "the copy-engine mean needs 2 <= P <= %d, got %d", kMaxR, P);
   }
 }
@@ -159,8 +158,8 @@ int launch_rank_barrier(int P, const CommArgs& a, cudaStream_t s) {
   return LASGD_OK;
 }
 
-int launch_ce_mean(int dtype, int P, const CommArgs& a, const CeRound& r, int nblocks, cudaStream_t s) {
-  return dtype == LASGD_F64 ? ce_mean_t<double>(P, a, r, nblocks, s) : ce_mean_t<float>(P, a, r, nblocks, s);
+int launch_ce_mean(int dtype, int P, const CommArgs& a, const CeRound& r, cudaStream_t s) {
+  return dtype == LASGD_F64 ? ce_mean_t<double>(P, a, r, s) : ce_mean_t<float>(P, a, r, s);
 }
 
 }  // namespace lasgd

@@ -19,7 +19,7 @@ struct CeRound {
   size_t stage_elems;
 };
 
-int launch_ce_mean(int dtype, int P, const CommArgs& a, const CeRound& r, int nblocks, cudaStream_t s);
+int launch_ce_mean(int dtype, int P, const CommArgs& a, const CeRound& r, cudaStream_t s);
 // One-warp device barrier on rank-level slot kind 5 (epoch = a.epoch): lasgd_comm_barrier.
 int launch_rank_barrier(int P, const CommArgs& a, cudaStream_t s);
 

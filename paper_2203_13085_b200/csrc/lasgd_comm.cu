@@ -797,7 +797,7 @@ extern "C" int lasgd_comm_allreduce(lasgd_comm* c, int snap_slot, int algo, void
       r.stage_peer[q] = c->peer_base[q] + c->off_stage;
       r.xbar_peer[q] = c->peer_base[q] + c->off_xbar;
     }
-    rc = launch_ce_mean(c->dtype, c->world, a, r, c->nblocks, cs);  // its own entry gate
+    rc = launch_ce_mean(c->dtype, c->world, a, r, cs);  // its own entry gate
     if (rc) return rc;
     LASGD_CUDA_TRY(cudaEventRecord(c->ev[s % kEvents], cs));
     if (seq) *seq = s;
