@@ -22,6 +22,10 @@ namespace lasgd {
 //   phase B (bit 2): every other chunk: local step + pull with the mean in the local
 //     xbar, next snapshot written locally and pushed to the owner's staging (other
 //     parity); then the rank-level end signal.
+//   split (bit 8, P2P, large buffers): phase A does its chunk in two halves and signals
+//     each (rank-level rows 0 and 6) instead of the mid barrier; phase B does half 0 of
+//     every other chunk once every owner's row 0 is in, then half 1 after row 6 — the
+//     second half's mean stores drain while phase B already works.
 // Per rank and round: NVLink out 2(P-1)/P*B as posted writes, all reads local.  Same
 // element functions and summation order as K7, so results are bit-identical.
 template <typename T>
