@@ -240,6 +240,9 @@ int lasgd_comm_resolve_fused_algo(lasgd_comm* c, int algo);
 /* What ALGO_AUTO resolves to for a fused round of `bytes` per rank at `world` ranks
  * (host only, no device needed). */
 int lasgd_resolve_fused_algo_for(int world, size_t bytes);
+/* What ALGO_AUTO resolves to for a standalone all-reduce (lasgd_comm_allreduce, no NVLS)
+ * of `bytes` per rank at `world` ranks.  Host only, no device needed. */
+int lasgd_resolve_allreduce_algo_for(int world, size_t bytes);
 /* Change the SM budget (CTAs per launch) for subsequent launches; every rank must
  * make the same call between the same two launches. */
 int lasgd_comm_set_nblocks(lasgd_comm* c, int nblocks);

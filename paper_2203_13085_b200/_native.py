@@ -151,6 +151,7 @@ SIGNATURES = {
     "lasgd_comm_resolve_algo": (_I, [_P, _I]),
     "lasgd_comm_resolve_fused_algo": (_I, [_P, _I]),
     "lasgd_resolve_fused_algo_for": (_I, [_I, _SZ]),
+    "lasgd_resolve_allreduce_algo_for": (_I, [_I, _SZ]),
     "lasgd_comm_peers_ahead": (_I, [_P, ctypes.c_ulonglong]),
     "lasgd_comm_set_gate": (_I, [_P, _I]),
     "lasgd_comm_barrier": (_I, [_P, _P]),

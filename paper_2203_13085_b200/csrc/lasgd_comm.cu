@@ -465,14 +465,23 @@ extern "C" int lasgd_comm_buffer(lasgd_comm* c, int which, void** ptr) {
 // copy-engine mean is faster still (P=4 2.328 vs 2.372, P=3 2.130 vs 2.247).  Otherwise
 // (P = 2: one-shot; P >= 5, unmeasured on hardware) resolve_algo.  Not for SGD-AR buckets
 // or fused rounds: they have their own.
-static int resolve_allreduce_algo(const lasgd_comm* c, int algo) {
-  const size_t bytes = c->n * c->elem;
-  const int a = resolve_algo(algo, c->world, bytes);
-  if (algo != LASGD_ALGO_AUTO || c->nvls_uc || c->world < 3 || c->world > 4) return a;
+static int resolve_allreduce_bytes(int algo, int world, size_t bytes) {
+  const int a = resolve_algo(algo, world, bytes);
+  if (algo != LASGD_ALGO_AUTO || world < 3 || world > 4) return a;
   if (bytes >= ((size_t)512 << 20)) return LASGD_ALGO_CE;
   if (a == LASGD_ALGO_TWOSHOT) return LASGD_ALGO_PUSH;
-  if (c->world == 4 && bytes >= ((size_t)3 << 20)) return LASGD_ALGO_PUSH;  // 4 MB: 0.0347 vs 0.0372 one-shot
+  if (world == 4 && bytes >= ((size_t)3 << 20)) return LASGD_ALGO_PUSH;  // 4 MB: 0.0347 vs 0.0372 one-shot
   return a;
+}
+
+static int resolve_allreduce_algo(const lasgd_comm* c, int algo) {
+  if (c->nvls_uc) return resolve_algo(algo, c->world, c->n * c->elem);
+  return resolve_allreduce_bytes(algo, c->world, c->n * c->elem);
+}
+
+extern "C" int lasgd_resolve_allreduce_algo_for(int world, size_t bytes) {
+  if (world < 1 || world > kMaxR) return fail(LASGD_ERR_UNSUPPORTED, "world size %d outside [1, %d]", world, kMaxR);
+  return resolve_allreduce_bytes(LASGD_ALGO_AUTO, world, bytes);
 }
 
 int lasgd::comm_side_algo(lasgd_comm* c, int algo) {

@@ -110,3 +110,20 @@ def test_entry_points_reject_bad_arguments_without_gpu():
     assert lib.lasgd_comm_create(0, 9, 0, 10, N.F32, None, ctypes.byref(h)) == N.ERR_UNSUPPORTED
     assert lib.lasgd_comm_create(2, 2, 0, 10, N.F32, None, ctypes.byref(h)) == N.ERR_INVALID_ARGUMENT
     assert b"rank" in lib.lasgd_last_error()
+
+
+def test_allreduce_auto_choices():
+    """The standalone all-reduce's AUTO (lasgd_comm_allreduce without NVLS): one-shot at
+    P=2; at the measured P = 3-4 the push mean where the two-shot would run (and at P=4
+    from 4 MB), the copy-engine mean from 512 MB; P >= 5 keeps one-shot / two-shot."""
+    from paper_2203_13085_b200 import _native as N
+
+    MB = 1 << 20
+    f = N.lib().lasgd_resolve_allreduce_algo_for
+    one, two, push, ce = N.ALGO_ONESHOT, N.ALGO_TWOSHOT, N.ALGO_PUSH, N.ALGO_CE
+    cases = [(2, 4 * MB, one), (2, 1024 * MB, one),
+             (3, 4 * MB, one), (3, 16 * MB, push), (3, 102 * MB, push), (3, 1024 * MB, ce),
+             (4, 1 * MB, one), (4, 4 * MB, push), (4, 102 * MB, push), (4, 256 * MB, push), (4, 512 * MB, ce),
+             (8, 1 * MB, one), (8, 16 * MB, two), (8, 1024 * MB, two)]
+    for world, nbytes, want in cases:
+        assert f(world, nbytes) == want, (world, nbytes)
