@@ -508,7 +508,11 @@ class P2PCommunicator:
 
     def allreduce(self, slot: int, algo: int = N.ALGO_AUTO, stream=None) -> int:
         """Launch the mean of snapshot slot ``slot`` over all ranks into ``self.xbar``
-        on ``stream`` (default: the communicator's low-priority side stream)."""
+        on ``stream`` (default: the communicator's low-priority side stream).  ``algo``:
+        ``ALGO_ONESHOT`` / ``ALGO_TWOSHOT`` (SM loads), ``ALGO_PUSH`` (NVLink stores),
+        ``ALGO_CE`` (copy engines) — all the ring order of collective.py:154-203, bit for
+        bit — or ``ALGO_NVLS`` on an NVLS communicator; ``ALGO_AUTO`` picks by world size
+        and buffer size (``resolve_algo``).  Returns the launch's sequence number."""
         s = stream if stream is not None else self.stream
         seq = ctypes.c_ulonglong()
         N.check(N.lib().lasgd_comm_allreduce(self._h, slot, algo, ctypes.c_void_p(s.cuda_stream), ctypes.byref(seq)),
