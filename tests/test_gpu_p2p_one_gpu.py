@@ -30,7 +30,7 @@ WORKERS = [("_w_allreduce", 2), ("_w_worker_loop", 2), ("_w_sgd_ar", 2), ("_w_sg
            ("_w_allreduce", 4), ("_w_worker_loop", 4), ("_w_graph_replay", 4),
            # P = 8 (no 8-GPU box is reachable from the build pool): the staged push and
            # two-shot with eight real ranks, at the full ResNet-50 size too
-           ("_w_allreduce", 8), ("_w_worker_loop", 8), ("_w_full_size", 8)]
+           ("_w_allreduce", 8), ("_w_worker_loop", 8), ("_w_full_size", 8), ("_w_ce", 8)]
 
 
 def _port():
